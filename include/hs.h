@@ -1,0 +1,264 @@
+/* hs.h — C ABI of the B200-native HydraServe cold-start path (arXiv 2502.15524).
+ *
+ * What this library does (§1, lines 88-92; §4; §5.2;
+ * §6): a decoder model's layers are range-sharded into a pipeline-parallel
+ * group of s stages, one GPU per stage.  Each stage streams its contiguous slice of bf16
+ * weights from pinned host memory into HBM in chunks ("pipeline the fetching and loading at
+ * tensor granularity"; "obtain tensors in a streaming manner"),
+ * and per-layer readiness gates the stage's prefill/decode kernels, so inference starts
+ * before loading ends.  Stages hand activations to the next stage ("intermediate results
+ * transmitted sequentially") over NVLink peer memory.  Pipeline
+ * consolidation ("scaling down"; KV-cache migration PAPER.md:622-643)
+ * migrates the weights of the other stages' layers and the paged KV blocks of live
+ * sequences into one full-memory stage, which then decodes alone.
+ *
+ * Conventions (all entry points):
+ *  - Every call returns hs_status; HS_OK == 0.  Out-parameters are written only on HS_OK.
+ *    hs_last_error() returns a thread-local message describing the last failure.
+ *  - Errors are returned, never raised/aborted across the ABI.  HS_E_CUDA is sticky for the
+ *    group: the group may only be destroyed afterwards.
+ *  - Host pointers are caller-owned.  Device memory, streams and events are library-owned.
+ *  - A group is not thread-safe; the caller serialises calls on one group.
+ *  - Multi-process (SPMD) mode: one process per stage GPU; every process calls every entry
+ *    point with identical arguments (except per-process host buffers).  Cross-process
+ *    plumbing (handle exchange, barrier) is supplied by the caller through hs_comm
+ *    (e.g. torch.distributed); the data path itself uses CUDA IPC peer memory over NVLink.
+ */
+#ifndef HS_H_
+#define HS_H_
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t hs_status;
+enum {
+  HS_OK = 0,
+  HS_E_INVAL = 1,       /* bad argument / unsupported shape */
+  HS_E_CUDA = 2,        /* CUDA runtime/kernel failure; sticky: the group must be destroyed */
+  HS_E_OOM = 3,         /* device or pinned-host allocation failed (group left usable) */
+  HS_E_INFEASIBLE = 4,  /* no placement satisfies the request (Alg. 1 has no choice) */
+  HS_E_STATE = 5,       /* call out of order (e.g. prefill before any load was issued) */
+  HS_E_PEER = 6,        /* stage GPUs cannot reach each other over P2P */
+  HS_E_TIMEOUT = 7      /* a cross-stage device wait timed out (peer never signalled) */
+};
+
+#define HS_MAX_STAGES 8
+#define HS_MAX_LAYERS 128
+
+/* Decoder shape.  The paper evaluates the Llama-2 family; this library
+ * implements that architecture: pre-norm RMSNorm, multi-head attention with rotate-half
+ * RoPE, SiLU-gated MLP, no biases, untied lm_head (reading R1).
+ * Requirements: n_kv_heads == n_heads; head_dim in {64,128}; hidden == n_heads*head_dim;
+ * hidden % 64 == 0; ffn % 64 == 0; vocab % 16 == 0; n_layers <= HS_MAX_LAYERS. */
+typedef struct {
+  int32_t n_layers, hidden, n_heads, n_kv_heads, head_dim, ffn, vocab, max_seq;
+  float rms_eps;    /* 1e-5 for Llama-2 */
+  float rope_theta; /* 1e4 for Llama-2 */
+} hs_model_cfg;
+
+/* ---------------------------------------------------------------------------------------
+ * Host weight image ("model file whose metadata header comes first").
+ * Byte layout (all offsets from the start of the image, little endian):
+ *   [0, HS_IMAGE_HEADER_BYTES)  hs_image_header (host-only metadata, never loaded)
+ *   embed region                 embed [vocab, hidden] bf16, row-major
+ *   layer region l (l = 0..L-1)  at layer_off[l], layer_bytes long, tensors at t_* offsets:
+ *       attn_norm [hidden]; w_qkv [3*hidden, hidden] (rows: q then k then v);
+ *       w_o [hidden, hidden]; ffn_norm [hidden];
+ *       w_gu [2*ffn, hidden] with gate/up rows interleaved in blocks of gu_interleave:
+ *            physical row p: b = p / (2*G), j = p % (2*G); j < G -> gate row b*G + j,
+ *            else up row b*G + j - G  (G = gu_interleave = 16);
+ *       w_d [hidden, ffn]
+ *   final region                 final_norm [hidden] at t_final_norm, lm_head [vocab, hidden]
+ *                                at t_lm_head
+ * Every weight matrix is [out_features, in_features] row-major ("K-major"), which is the
+ * layout the tensor-core GEMMs consume directly.  Regions are HS_IMAGE_ALIGN aligned, so a
+ * stage's slice [embed|layers b..e-1|final] is one contiguous byte range.
+ * ------------------------------------------------------------------------------------- */
+#define HS_IMAGE_MAGIC 0x31474D49534853ULL /* "SHSIMG1" */
+#define HS_IMAGE_HEADER_BYTES 65536ULL
+#define HS_IMAGE_ALIGN 65536ULL
+#define HS_TENSOR_ALIGN 256ULL
+#define HS_GU_INTERLEAVE 16
+
+typedef struct {
+  uint64_t magic;
+  uint32_t version;       /* 1 */
+  uint32_t gu_interleave; /* HS_GU_INTERLEAVE */
+  hs_model_cfg cfg;
+  uint64_t total_bytes;   /* whole image incl. header */
+  uint64_t embed_off, embed_bytes;
+  uint64_t layer_off[HS_MAX_LAYERS];
+  uint64_t layer_bytes;   /* padded region size of one layer */
+  uint64_t t_attn_norm, t_wqkv, t_wo, t_ffn_norm, t_wgu, t_wd; /* offsets inside a layer */
+  uint64_t final_off, final_bytes;
+  uint64_t t_final_norm, t_lm_head; /* offsets inside the final region */
+  uint64_t param_bytes;   /* sum of tensor bytes (no padding): 2 * #params */
+} hs_image_header;
+
+/* A (slice of a) host image: data covers image bytes [data_offset, data_offset+data_bytes).
+ * data should be pinned (cudaHostAlloc / cudaHostRegister); pageable memory works but the
+ * copy engine then cannot stream it asynchronously.  Caller-owned; must stay valid until
+ * every load issued from it has completed (hs_stage_load_stats) or the group is destroyed. */
+typedef struct {
+  const hs_image_header* header;
+  const void* data;
+  uint64_t data_offset;
+  uint64_t data_bytes;
+} hs_image;
+
+/* Computes the image layout for cfg (host only).  total_bytes etc. filled in. */
+hs_status hs_image_layout(const hs_model_cfg* cfg, hs_image_header* out);
+
+/* ---------------------------------------------------------------------------------------
+ * Planning (§4.1; Eq. 1; Eq. 5).
+ * ------------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t device;     /* CUDA ordinal (as seen by the process that will own the stage) */
+  double h2d_gbps;    /* p_i: host->device bandwidth of this GPU's link, GB/s (10^9 B/s) */
+  int32_t link_group; /* GPUs sharing one host uplink share a group id (contention, NEXT) */
+  uint64_t free_bytes;/* free HBM */
+} hs_gpu;
+
+typedef struct {
+  int32_t pp;                            /* s */
+  int32_t device[HS_MAX_STAGES];         /* g, in stage order */
+  int32_t layer_begin[HS_MAX_STAGES];    /* [b_k, e_k) */
+  int32_t layer_end[HS_MAX_STAGES];
+  uint64_t stage_bytes[HS_MAX_STAGES];   /* weight bytes each stage must load (image ranges) */
+  uint64_t slice_begin[HS_MAX_STAGES];   /* image byte range of the stage slice */
+  uint64_t slice_end[HS_MAX_STAGES];
+  int32_t full_memory[HS_MAX_STAGES];    /* w flags: stage reserves whole-model memory */
+  double pred_ttft_s;                    /* Eq. 5 specialised (R9) */
+} hs_plan;
+
+/* Builds a plan for pp stages (1..HS_MAX_STAGES; pp = 0 is reserved for SLO-driven choice).
+ * Layers are split into contiguous ranges, floor(L/pp) each, the remainder going to the
+ * earliest stages; stage 0 holds the embedding, the last stage the final norm + lm_head.
+ * GPUs are chosen by the paper's selection rule (smallest 1/p_i first, PAPER.md:408-413;
+ * remote fetch 1/b_i = 0 here) with full_memory_stages stages reserving the whole model
+ * (Alg. 1's w).  Stage 0 is always full-memory when full_memory_stages >= 1, so it can be
+ * the consolidation target.  t_prefill_s / t_hop_s are Eq. 5's t_p, t_n (may be 0).
+ * Errors: HS_E_INVAL (bad cfg/pp), HS_E_INFEASIBLE (not enough GPUs or memory). */
+hs_status hs_plan_stages(const hs_model_cfg* cfg, const hs_gpu* gpus, int32_t n_gpus,
+                         int32_t pp, int32_t full_memory_stages, double t_prefill_s,
+                         double t_hop_s, hs_plan* out);
+
+/* Paper's predictors, exposed for the planner's tests (PAPER.md:398 Eq. 1, :417 Eq. 2,
+ * :579-584 Eq. 5).  Bandwidth arrays have s entries; M in the same unit as b,p numerators. */
+double hs_predict_ttft_eq1(double t_c, double M, int32_t s, int32_t w, const double* b,
+                           const double* p, double t_p, double t_n);
+double hs_predict_tpot_eq2(double t_d, int32_t s, int32_t w, double t_n);
+double hs_predict_ttft_eq5(double t_cc, double t_cu, double t_l, double M, int32_t s,
+                           int32_t w, const double* b, const double* p, double t_p,
+                           double t_n);
+
+/* ---------------------------------------------------------------------------------------
+ * Groups.
+ * ------------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t block_tokens; /* 16 (only value supported) */
+  int32_t num_blocks;   /* KV blocks per layer pool, identical ids on every stage */
+  int32_t max_seqs;     /* max live sequences (block-table rows) */
+  int32_t max_tokens;   /* max tokens in one prefill call (activation buffers) */
+} hs_kv_cfg;
+
+/* Cross-process plumbing for SPMD mode (NULL comm => every stage is driven by this process).
+ * allgather: each of world ranks contributes `bytes` bytes; recv gets world*bytes in rank
+ * order.  barrier: all ranks.  Both return 0 on success. */
+typedef struct {
+  int32_t rank;   /* == the stage index this process owns */
+  int32_t world;  /* == plan->pp */
+  void* ctx;
+  int32_t (*allgather)(void* ctx, const void* send, uint64_t bytes, void* recv);
+  int32_t (*barrier)(void* ctx);
+} hs_comm;
+
+typedef struct hs_group hs_group; /* opaque, library-owned */
+
+/* Creates the group: per owned stage sets the device, enables peer access, allocates the
+ * weight arena (slice, or whole model for full-memory stages), the per-layer KV pools
+ * ([num_blocks][K|V][heads][16][head_dim] bf16 per layer), activation buffers, streams
+ * (compute high priority, copy), per-layer readiness events, and warms the kernels.  All
+ * before T0 (R3).  image: whole-model image (or, in SPMD mode, one covering this
+ * rank's slice); stage_images: optional [pp] per-stage images (NULL => use image).
+ * Errors: HS_E_INVAL, HS_E_OOM, HS_E_PEER, HS_E_CUDA. */
+hs_status hs_group_create(const hs_model_cfg* cfg, const hs_plan* plan,
+                          const hs_image* image, const hs_image* stage_images,
+                          const hs_kv_cfg* kv, const hs_comm* comm, hs_group** out);
+
+/* Issues the chunked H2D load of a stage's slice (critical order: embedding, layers b..e-1
+ * in order, final norm + lm_head last) and returns immediately; each layer's readiness
+ * event is recorded after its last chunk.  chunk_bytes = 0 => 32 MiB.  Calling it again
+ * re-loads (used by benchmarks).  In SPMD mode only the owned stage is issued; stage = -1
+ * means "every stage this process owns".  Errors: HS_E_INVAL, HS_E_CUDA. */
+hs_status hs_load_stage_async(hs_group* g, int32_t stage, uint64_t chunk_bytes);
+
+typedef struct {
+  uint64_t bytes;         /* bytes copied host->device by the last load */
+  float load_ms;          /* device time from first chunk start to last chunk end */
+  int32_t layers_ready;   /* layers of this stage whose readiness event has fired */
+  int32_t done;           /* 1 when the whole slice is resident */
+} hs_load_stats;
+/* Non-blocking when wait == 0 (reports progress); wait != 0 blocks until the load ends. */
+hs_status hs_stage_load_stats(hs_group* g, int32_t stage, int32_t wait, hs_load_stats* out);
+
+/* Prefill n_seqs prompts (packed tokens, lengths seq_lens) through all stages; returns the
+ * greedy first token of each sequence (ties -> lowest id).  May be called right after
+ * hs_load_stage_async: readiness is enforced on the device.  out_logits ([n_seqs*vocab]
+ * fp32, may be NULL) is written only by the process owning the last stage.  Sequence ids
+ * are caller-chosen and must not be live.  Errors: HS_E_INVAL, HS_E_STATE (no load issued),
+ * HS_E_OOM (KV blocks exhausted), HS_E_CUDA, HS_E_TIMEOUT. */
+hs_status hs_prefill(hs_group* g, int32_t n_seqs, const int64_t* seq_ids,
+                     const int32_t* tokens, const int32_t* seq_lens, int32_t* out_tokens,
+                     float* out_logits);
+
+/* One greedy decode step for n_seqs live sequences: in_tokens[i] is appended at position
+ * ctx_i (in_tokens == NULL => the tokens produced by the previous prefill/decode call for
+ * the same seq_ids, fed back on the device).  Errors as hs_prefill; HS_E_INVAL for a
+ * sequence never prefilled. */
+hs_status hs_decode_step(hs_group* g, int32_t n_seqs, const int64_t* seq_ids,
+                         const int32_t* in_tokens, int32_t* out_tokens, float* out_logits);
+
+hs_status hs_release_seq(hs_group* g, int64_t seq_id);
+
+typedef struct {
+  uint64_t weight_bytes; /* weight bytes migrated into the target */
+  uint64_t kv_bytes;     /* KV bytes migrated into the target */
+  double seconds;        /* device time of the migration (first copy start .. last end) */
+  double pause_seconds;  /* host time from call entry to return (drain + migrate + rebind) */
+} hs_consolidate_stats;
+
+/* Scale-down consolidation: drain in-flight work, copy the
+ * weight regions the target lacks and gather the used KV blocks of every live sequence
+ * for the other stages' layers into the target's pools (same block ids), rebind the
+ * target to all layers, release the other stages.  The target must be full_memory.
+ * Afterwards the group is single-stage.  Errors: HS_E_INVAL (target not full-memory),
+ * HS_E_STATE, HS_E_CUDA. */
+hs_status hs_consolidate(hs_group* g, int32_t target_stage, hs_consolidate_stats* out);
+
+hs_status hs_group_destroy(hs_group* g);
+const char* hs_last_error(void);
+
+/* Current pipeline degree (1 after consolidation) and the stage index owned by this process
+ * (SPMD) or -1 (local mode). */
+hs_status hs_group_info(hs_group* g, int32_t* pp, int32_t* owned_stage);
+
+/* ---- test / benchmark helpers (not part of the serving path) ---- */
+/* Reads KV of one sequence, layer, positions [pos0,pos0+n_pos) from the stage that holds
+ * the layer: host_out [n_pos][2][n_heads][head_dim] bf16.  Blocking. */
+hs_status hs_debug_read_kv(hs_group* g, int64_t seq_id, int32_t layer, int32_t pos0,
+                           int32_t n_pos, void* host_out);
+/* Copies bytes [image_off, image_off+bytes) of the device weight arena of `stage` to host. */
+hs_status hs_debug_read_weights(hs_group* g, int32_t stage, uint64_t image_off,
+                                uint64_t bytes, void* host_out);
+/* Fills a stage's weight arena with 0xFF (bf16 NaN) so a missing readiness wait shows up. */
+hs_status hs_debug_poison_weights(hs_group* g, int32_t stage);
+/* Device-side counters: number of kernels this library launched since creation. */
+hs_status hs_debug_launch_count(hs_group* g, uint64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HS_H_ */

@@ -1,0 +1,78 @@
+"""Oracle stage planning: layer split, stage bytes, the paper's predictors and server choice.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+  * Eq. 1: TTFT = t_c + (M/s) max_i(1/b_i + 1/p_i) + t_p (s - w + w/s) + t_n s
+  * Eq. 2: TPOT = t_d (s - w + w/s) + t_n s
+  * Eq. 5: TTFT = max_i( t_cc + t_cu + max((M/s)/p_i, t_l), (M/s)/b_i )
+                                      + t_p (s - w + w/s) + t_n s
+  * selection: the w full-memory workers take the servers with the
+    smallest 1/b + 1/p among those that fit the whole model; the rest are merged with the
+    low-memory-capable servers and the smallest s - w ratios are taken.
+  * DESIGN.md reading R9: on one box there is no remote fetch (1/b = 0), runtime/library
+    terms are paid before T0 (t_cc = t_cu = t_l = 0), and each stage's own byte count
+    replaces M/s, so  TTFT_pred = max_k(bytes_k / p_k) + t_p (s - w + w/s) + t_n s.
+"""
+from __future__ import annotations
+
+from .decoder import embed_param_bytes, final_param_bytes, layer_param_bytes, split_layers
+
+
+def eq1_ttft(t_c, M, s, w, b, p, t_p, t_n):
+    return t_c + (M / s) * max(1.0 / bi + 1.0 / pi for bi, pi in zip(b, p)) + t_p * (s - w + w / s) + t_n * s
+
+
+def eq2_tpot(t_d, s, w, t_n):
+    return t_d * (s - w + w / s) + t_n * s
+
+
+def eq5_ttft(t_cc, t_cu, t_l, M, s, w, b, p, t_p, t_n):
+    fetch = max(max(t_cc + t_cu + max((M / s) / pi, t_l), (M / s) / bi) for bi, pi in zip(b, p))
+    return fetch + t_p * (s - w + w / s) + t_n * s
+
+
+def select_servers(full_capable, low_capable, s, w):
+    """full_capable / low_capable: lists of (server_id, ratio).  Returns s server ids:
+    the w smallest-ratio full-capable, then the s-w smallest-ratio of the merged rest;
+    ties broken by server id."""
+    key = lambda t: (t[1], t[0])  # noqa: E731
+    fc = sorted(full_capable, key=key)
+    if len(fc) < w:
+        raise ValueError("infeasible")
+    first = fc[:w]
+    rest = sorted(list(low_capable) + fc[w:], key=key)
+    if len(rest) < s - w:
+        raise ValueError("infeasible")
+    return [t[0] for t in first + rest[: s - w]]
+
+
+def stage_param_bytes(cfg: dict, pp: int):
+    """Bytes each stage must load (no padding): its layers, + embedding on stage 0,
+    + final norm and lm_head on the last stage."""
+    out = []
+    for k, (b, e) in enumerate(split_layers(cfg["n_layers"], pp)):
+        n = (e - b) * layer_param_bytes(cfg)
+        if k == 0:
+            n += embed_param_bytes(cfg)
+        if k == pp - 1:
+            n += final_param_bytes(cfg)
+        out.append(n)
+    return out
+
+
+def plan(cfg: dict, gpus, pp: int, full_memory_stages: int = 1, t_prefill_s=0.0, t_hop_s=0.0):
+    """gpus: list of dicts {device, h2d_gbps, link_group, free_bytes}.  Mirrors hs_plan_stages:
+    w = full_memory_stages stages reserve the whole model (stage 0 first), chosen by the
+    selection rule with ratio 1/p; returns dict(pp, device, ranges, stage_bytes,
+    full_memory, pred_ttft_s)."""
+    sb = stage_param_bytes(cfg, pp)
+    model_bytes = embed_param_bytes(cfg) + final_param_bytes(cfg) + cfg["n_layers"] * layer_param_bytes(cfg)
+    w = min(full_memory_stages, pp)
+    full = [(g["device"], 1.0 / g["h2d_gbps"]) for g in gpus if g["free_bytes"] >= model_bytes]
+    low = [(g["device"], 1.0 / g["h2d_gbps"]) for g in gpus
+           if max(sb) <= g["free_bytes"] < model_bytes]
+    devs = select_servers(full, low, pp, w)
+    p = {g["device"]: g["h2d_gbps"] for g in gpus}
+    pred = max(sb[k] / (p[devs[k]] * 1e9) for k in range(pp)) + t_prefill_s * (pp - w + w / pp) + t_hop_s * pp
+    return dict(pp=pp, device=devs, ranges=split_layers(cfg["n_layers"], pp), stage_bytes=sb,
+                full_memory=[1 if k < w else 0 for k in range(pp)], pred_ttft_s=pred)
