@@ -1,0 +1,414 @@
+#!/usr/bin/env python3
+"""Benchmark of the HydraServe cold-start path on B200 (BASELINE.json metric).
+
+One *step* = one whole pass of the hot path over one synthetic request:
+  plan (a1) -> T0: issue the chunked pinned-host->HBM load of every stage (a3, a4) ->
+  prefill of the prompt through the stages (a5-a15; stage hand-offs a13) -> first token on
+  the host (TTFT) -> D greedy decode steps (a16) -> [N > 1] consolidation into stage 0 (a17)
+  -> D more decode steps on the single endpoint.
+N = 1 runs BASELINE config 2 (Llama-2-7B shape, 512-token prompt, PP = 1); N > 1 (torchrun,
+one process per GPU) runs config 3 (PP = N, one stage per GPU, CUDA-IPC peer memory over
+NVLink).  --config 4 selects the 13B PP=4 16 x 512 workload.
+
+value   = device-timed cold-start TTFT (s): per rank, CUDA events from the stage's first load
+          chunk to the end of its prefill work (the last stage: token on host), max over ranks.
+e2e     = the same TTFT on the host clock around the C-ABI calls (weights from pinned host
+          memory, prompt H2D and token D2H inside), max over ranks.
+Weights (13.5 GB) are larger than L2 (126 MB): no flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "cold-start TTFT (s) and decode tok/s at PP=1/2/4/8; consolidation GB/s vs NVLink"
+PCIE_H2D_GBS = 55.6        # measured per GPU in isolation (profiles/r01_links_measured.json)
+PCIE_H2D_AGG_CAP = 115.5   # measured 4-GPU concurrent aggregate (host-side cap)
+NVLINK_GBS = 900.0         # nominal per direction per GPU (north star); measured P2P 770
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:  # noqa
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "_fallback": True}
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, path):
+        self.path = path
+        self.p = None
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:  # noqa
+            self.p = None
+
+    def stop(self, n_gpus):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9 or not parts[0].isdigit() or int(parts[0]) >= n_gpus:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def workload(args, world):
+    import hsgen
+    cfgn = args.config or (2 if world == 1 else 3)
+    if args.model:
+        model = args.model
+    else:
+        model = "llama2-13b" if cfgn == 4 else "llama2-7b"
+    cfg = dict(hsgen.CONFIGS[model])
+    if cfgn == 4:
+        n_seqs, plen, dsteps = 16, 512, 64
+    else:
+        n_seqs, plen, dsteps = 1, args.prompt_len, args.decode_steps
+    if model == "tiny":
+        plen = min(plen, 32)
+    cfg["max_seq"] = max(cfg["max_seq"], plen + 2 * dsteps + 16)
+    return cfgn, model, cfg, n_seqs, plen, dsteps
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import hsgen
+    from paper_2502_15524_b200 import hs
+
+    rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
+    local = env_int("LOCAL_RANK", rank)
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    dist = None
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = hs.DistComm()
+    cfgn, model, cfg, n_seqs, plen, dsteps = workload(args, world)
+    pp = world
+    if cfgn == 4 and world == 1:
+        pp = 1
+    hdr = hs.image_layout(cfg)
+    gpus = [dict(device=i, h2d_gbps=PCIE_H2D_GBS, free_bytes=torch.cuda.mem_get_info(local)[1]) for i in range(pp)]
+    plan = hs.plan_stages(cfg, gpus, pp, 1)
+    for k in range(pp):
+        plan.device[k] = k if world > 1 else local
+    pd = plan.as_dict()
+    # host image: this rank's stage slice (whole model at N = 1), pinned, pre-faulted
+    b, e = pd["slices"][rank if world > 1 else 0] if world > 1 else (hdr.embed_off, hdr.total_bytes)
+    t_img = time.time()
+    img = hs.HostImage(hdr, b, e)
+    hsgen.image_fill(hsgen.image_header(cfg), hsgen.WEIGHT_SEED, img.ptr, b, e)
+    t_img = time.time() - t_img
+    prompts = hsgen.prompts(n_seqs, plen, cfg["vocab"])
+    ids = list(range(n_seqs))
+    nb = n_seqs * ((plen + 2 * dsteps + 15) // 16 + 1) + 8
+    kw = dict(num_blocks=nb, max_seqs=max(n_seqs, 1), max_tokens=n_seqs * plen, comm=comm)
+    stage = rank if world > 1 else 0
+    consolidate = world > 1
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def new_group():
+        if world > 1:
+            return hs.Group(cfg, plan, None, [img if k == rank else None for k in range(pp)], **kw)
+        return hs.Group(cfg, plan, img, **kw)
+
+    state = {"g": None}
+
+    def one_step(profile):
+        g = state["g"]
+        if g is None:
+            g = state["g"] = new_group()
+        r = {}
+        barrier()
+        t0 = time.perf_counter()
+        g.load_stage_async(-1, args.chunk_mb << 20)
+        toks, _ = g.prefill(ids, prompts)
+        t1 = time.perf_counter()
+        r["ttft_host"] = t1 - t0
+        r["ttft_dev"] = g.timing(stage).since_load_ms / 1e3
+        r["load_ms"] = g.timing(stage).load_ms
+        r["loaded_bytes"] = g.load_stats(stage).bytes
+        g.profile(profile)
+        dev = 0.0
+        t2 = time.perf_counter()
+        for _ in range(dsteps):
+            g.decode_step(ids)
+            dev += g.timing(stage).call_ms
+        r["decode_host"] = time.perf_counter() - t2
+        r["decode_dev"] = dev / 1e3
+        if consolidate:
+            g.profile(False)
+            st = g.consolidate(0)
+            r["cons_s"] = st.seconds
+            r["cons_pause"] = st.pause_seconds
+            r["cons_bytes"] = st.weight_bytes + st.kv_bytes
+            r["cons_w"], r["cons_kv"] = st.weight_bytes, st.kv_bytes
+            if rank == 0:
+                g.profile(profile)
+                dev2 = 0.0
+                t3 = time.perf_counter()
+                for _ in range(dsteps):
+                    g.decode_step(ids)
+                    dev2 += g.timing(0).call_ms
+                r["decode2_host"] = time.perf_counter() - t3
+                r["decode2_dev"] = dev2 / 1e3
+        r["prof"] = g.profile_read(reset=True) if profile else {}
+        g.profile(False)
+        if consolidate:
+            barrier()
+            g.destroy()
+            state["g"] = None
+        else:
+            for i in ids:
+                g.release_seq(i)
+        return r
+
+    for _ in range(args.warmup):
+        one_step(False)
+    clocks = Clocks(os.path.join(ROOT, "gpurun_out", f"clocks_r{rank}.csv")) if rank == 0 else None
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    barrier()
+    l0 = hs.Group.launch_count()
+    if clocks:
+        clocks.start()
+    steps = [one_step(True) for _ in range(args.steps)]
+    barrier()
+    launches = hs.Group.launch_count() - l0
+    ck = clocks.stop(world) if clocks else None
+
+    def agg_max(v):
+        if not dist:
+            return v
+        t = torch.tensor([float(v)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    def agg_sum(v):
+        if not dist:
+            return v
+        t = torch.tensor([float(v)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return t.item()
+
+    med = lambda k: statistics.median(s[k] for s in steps)  # noqa: E731
+    ttft_dev = agg_max(med("ttft_dev"))
+    ttft_host = agg_max(med("ttft_host"))
+    load_ms = agg_max(med("load_ms"))
+    loaded = agg_sum(med("loaded_bytes"))
+    dec_dev = agg_max(med("decode_dev"))
+    dec_host = agg_max(med("decode_host"))
+    launches = int(agg_sum(launches))
+    # per-kind profile (this rank) -> dominant decode GEMM
+    prof = {}
+    for s in steps:
+        for k, v in s["prof"].items():
+            a = prof.setdefault(k, dict(count=0, ms=0.0, bytes=0.0, flops=0.0))
+            for f in a:
+                a[f] += v[f]
+    pk = peaks()
+    dec_gemm = [v for k, v in prof.items() if k.startswith("gemm_") and k.endswith(".decode") and "lm_head" not in k]
+    g_ms = sum(v["ms"] for v in dec_gemm)
+    g_bytes = sum(v["bytes"] for v in dec_gemm)
+    g_count = sum(v["count"] for v in dec_gemm)
+    achieved = (g_bytes / (g_ms / 1e3) / 1e9) if g_ms > 0 else 0.0
+    roof = {"kernel": "gemm_kernel (tcgen05 swap-AB decode GEMM, qkv/o/gate_up/down, + split-K reduce)",
+            "bound": "hbm", "achieved": round(agg_max(achieved) if False else achieved, 1),
+            "peak": pk.get("hbm_gbs"), "unit": "GB/s",
+            "frac": round(achieved / pk.get("hbm_gbs", 6650.0), 4), "traffic": None,
+            "bytes_per_launch": (g_bytes / g_count) if g_count else None,
+            "ms_per_launch": (g_ms / g_count) if g_count else None,
+            "share_of_kernel_time": round(g_ms / max(1e-9, sum(v["ms"] for v in prof.values())), 3),
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if not pk.get("_fallback") else "fallback"}
+    pre_gemm = [v for k, v in prof.items() if k.startswith("gemm_") and k.endswith(".prefill")]
+    out = None
+    if rank == 0:
+        agg_link = PCIE_H2D_GBS * pp if pp <= 2 else min(PCIE_H2D_GBS * pp, PCIE_H2D_AGG_CAP * (pp / 4))
+        load_gbs = loaded / (load_ms / 1e3) / 1e9
+        out = {
+            "metric": METRIC, "value": round(ttft_dev, 5), "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.median(
+                s["ttft_host"] + s["decode_host"] + s.get("decode2_host", 0) + s.get("cons_pause", 0) for s in steps), 2),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init Llama-2-shaped weights, seeded; uniform random prompt tokens)",
+            "config": {"workload": f"config {cfgn}: {model} PP={pp}, {n_seqs}x{plen}-token prompt, "
+                                   f"{dsteps} greedy decode steps" + (", consolidate to stage 0, "
+                                                                      f"{dsteps} more steps" if consolidate else ""),
+                       "pp": pp, "prompt_tokens": plen, "n_seqs": n_seqs, "decode_steps": dsteps,
+                       "chunk_mb": args.chunk_mb, "l2": "inputs > L2 (weights 13.5 GB), no flush needed",
+                       "parallelism": f"pp{pp} (one process per GPU)" if world > 1 else "pp1"},
+            "ttft": {"device_s": round(ttft_dev, 5), "host_s": round(ttft_host, 5),
+                     "pred_eq5_s": round(pd["pred_ttft_s"], 5),
+                     "per_step_device_s": [round(s["ttft_dev"], 5) for s in steps]},
+            "load": {"bytes_per_stage_max": max(pd["stage_bytes"]), "bytes_total": int(loaded),
+                     "stage_load_ms_max": round(load_ms, 2), "achieved_gbs": round(load_gbs, 2),
+                     "peak_gbs_isolated_sum": round(PCIE_H2D_GBS * pp, 1),
+                     "peak_gbs_measured_concurrent": round(agg_link, 1),
+                     "frac_of_isolated_sum": round(load_gbs / (PCIE_H2D_GBS * pp), 4),
+                     "frac_of_measured_concurrent": round(load_gbs / agg_link, 4)},
+            "decode": {"tok_s_device": round(n_seqs * dsteps / dec_dev, 2), "tok_s_host": round(n_seqs * dsteps / dec_host, 2),
+                       "hbm_roofline_tok_s": None},
+            "roofline": roof,
+            "kernels": {k: {"count": v["count"], "ms": round(v["ms"], 3),
+                            "gbs": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1) if v["ms"] else None,
+                            "tflops": round(v["flops"] / (v["ms"] / 1e3) / 1e12, 2) if v["ms"] and v["flops"] else None}
+                        for k, v in sorted(prof.items())},
+            "prefill_gemm_tflops": round(sum(v["flops"] for v in pre_gemm) / max(1e-9, sum(v["ms"] for v in pre_gemm) / 1e3) / 1e12, 1),
+            "gpu_launches": launches,
+            "clocks": ck,
+            "e2e": {"value": round(ttft_host, 5), "unit": "s", "h2d_bytes_per_step": int(loaded + plen * n_seqs * 4),
+                    "d2h_bytes_per_step": int(4 * n_seqs * (1 + dsteps * (2 if consolidate else 1)))},
+            "image_gen_s": round(t_img, 2),
+        }
+        # decode roofline: weights (minus embedding) + KV read per step
+        H, L, V = cfg["hidden"], cfg["n_layers"], cfg["vocab"]
+        wbytes = hdr.param_bytes - 2 * V * H
+        kv = n_seqs * (plen + dsteps // 2) * 2 * H * 2 * L
+        out["decode"]["hbm_roofline_tok_s"] = round(n_seqs / ((wbytes + kv) / (pk.get("hbm_gbs", 6650) * 1e9)), 1)
+        if consolidate:
+            cs = statistics.median(s["cons_s"] for s in steps)
+            cb = statistics.median(s["cons_bytes"] for s in steps)
+            out["consolidation"] = {"bytes": int(cb), "weight_bytes": int(steps[0]["cons_w"]), "kv_bytes": int(steps[0]["cons_kv"]),
+                                    "seconds": round(cs, 5), "gbs": round(cb / cs / 1e9, 1),
+                                    "frac_of_nvlink_900": round(cb / cs / 1e9 / NVLINK_GBS, 4),
+                                    "pause_s": round(statistics.median(s["cons_pause"] for s in steps), 4)}
+            out["decode"]["after_consolidation_tok_s_device"] = round(
+                n_seqs * dsteps / statistics.median(s["decode2_dev"] for s in steps), 2)
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(cfg, plen, n_seqs)
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return out
+
+
+def oracle_ttft_sample(cfg, plen, n_seqs, layers=1):
+    """The oracle as it stands: prefill of the real prompt through `layers` decoder layers +
+    embedding + final norm/lm_head, extrapolated linearly to all layers.  Weights are drawn
+    before the timer (input generation is not the oracle's work)."""
+    import numpy as np
+
+    import hsgen
+    from oracle.decoder import Group, Weights
+    W = Weights(cfg, cache=True)
+    sub = dict(cfg)
+    sub["n_layers"] = layers
+    for l in range(layers):
+        W.layer(l)
+    W.lm_head()
+    W.final_norm()
+    prompts = hsgen.prompts(n_seqs, plen, cfg["vocab"])
+    g = Group(sub, W, pp=1, num_blocks=n_seqs * (plen // 16 + 2))
+    t0 = time.perf_counter()
+    g.prefill(list(range(n_seqs)), prompts)
+    t = time.perf_counter() - t0
+    return t * cfg["n_layers"] / layers, t
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:  # noqa
+        return os.cpu_count()
+
+
+def cpu_baseline(cfg, plen, n_seqs):
+    est, t = oracle_ttft_sample(cfg, plen, n_seqs, 1)
+    return {"value": round(est, 3), "unit": "s", "cores": cpu_cores(), "kind": "oracle",
+            "sample": f"numpy-fp64 oracle prefill of the {n_seqs}x{plen}-token prompt through 1 of "
+                      f"{cfg['n_layers']} layers (+ embedding, lm_head) in {t:.2f} s, extrapolated x{cfg['n_layers']}; "
+                      "weights resident (no load term)"}
+
+
+def run_reference(args):
+    rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
+    if rank != 0:
+        return
+    cfgn, model, cfg, n_seqs, plen, dsteps = workload(args, world)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        est, t = oracle_ttft_sample(cfg, plen, n_seqs, 1)
+        if i >= args.warmup:
+            vals.append(est)
+    v = statistics.median(vals)
+    samp = (f"numpy-fp64 oracle prefill of {n_seqs}x{plen} tokens through 1 of {cfg['n_layers']} layers per step, "
+            f"extrapolated x{cfg['n_layers']}")
+    out = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "higher_is_better": False, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"config {cfgn}: {model}, {n_seqs}x{plen}-token prompt (oracle TTFT, no load)"},
+           "cpu_baseline": {"value": round(v, 3), "unit": "s", "cores": cpu_cores(), "kind": "oracle", "sample": samp},
+           "e2e": {"value": round(v, 3), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=0)
+    ap.add_argument("--model", default="")
+    ap.add_argument("--prompt-len", type=int, default=512)
+    ap.add_argument("--decode-steps", type=int, default=64)
+    ap.add_argument("--chunk-mb", type=int, default=32)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -255,8 +255,30 @@ hs_status hs_debug_read_weights(hs_group* g, int32_t stage, uint64_t image_off,
                                 uint64_t bytes, void* host_out);
 /* Fills a stage's weight arena with 0xFF (bf16 NaN) so a missing readiness wait shows up. */
 hs_status hs_debug_poison_weights(hs_group* g, int32_t stage);
-/* Device-side counters: number of kernels this library launched since creation. */
+/* Number of kernels this library has launched (process-wide, since load). */
 hs_status hs_debug_launch_count(hs_group* g, uint64_t* out);
+
+/* ---- measurement (benchmarks) ---- */
+/* Device-event timing of a stage for the most recent load and call: load_ms = first chunk ..
+ * last chunk (copy engine); call_ms = start .. end of this stage's work in the last
+ * prefill/decode call; since_load_ms = load start .. end of the last call (for the prefill
+ * issued right after the load this is the device-side TTFT seen by that stage). */
+typedef struct { float load_ms, call_ms, since_load_ms; } hs_stage_timing;
+hs_status hs_stage_timing_get(hs_group* g, int32_t stage, hs_stage_timing* out);
+
+/* Per-kernel-kind CUDA-event profile (off by default).  While enabled, every kernel the
+ * group launches is bracketed by events on its stream; hs_profile_read synchronises and
+ * returns, per kind, the launch count, summed device milliseconds and the algorithmic bytes
+ * and flops of those launches. */
+typedef struct { char name[32]; uint64_t count; double ms, bytes, flops; } hs_prof_entry;
+hs_status hs_profile_enable(hs_group* g, int32_t on);
+hs_status hs_profile_read(hs_group* g, hs_prof_entry* out, int32_t max_entries, int32_t* n,
+                          int32_t reset);
+
+/* Test-only: exercises the SPMD plumbing (allgather of rank-tagged bytes + barrier through
+ * the caller's callbacks) without any device work; returns HS_OK if every rank's bytes came
+ * back in rank order. */
+hs_status hs_debug_comm_selftest(const hs_comm* comm);
 
 #ifdef __cplusplus
 }

@@ -140,8 +140,9 @@ class Worker:
     """One pipeline stage: owns layers [b, e) and their KV pools
     (pool[l] : [num_blocks, 2 (K|V), n_heads, 16, head_dim] bf16 bits)."""
 
-    def __init__(self, cfg, weights: Weights, b: int, e: int, num_blocks: int, rnd=bf16):
+    def __init__(self, cfg, weights: Weights, b: int, e: int, num_blocks: int, rnd=bf16, acc=np.float64):
         self.cfg, self.w, self.rnd = cfg, weights, rnd
+        self.lin = (lambda x, W: linear(x, W, acc))
         self.layers = list(range(b, e))
         self.num_blocks = num_blocks
         nh, d = cfg["n_heads"], cfg["head_dim"]
@@ -165,9 +166,9 @@ class Worker:
         nh, d, eps = cfg["n_heads"], cfg["head_dim"], cfg["rms_eps"]
         T = x.shape[0]
         n = rmsnorm(x, W["attn_norm"], eps, rnd)                                   # step 4.1
-        q = rnd(linear(n, W["wq"])).reshape(T, nh, d)                               # step 4.2
-        k = rnd(linear(n, W["wk"])).reshape(T, nh, d)
-        v = rnd(linear(n, W["wv"])).reshape(T, nh, d)
+        q = rnd(self.lin(n, W["wq"])).reshape(T, nh, d)                               # step 4.2
+        k = rnd(self.lin(n, W["wk"])).reshape(T, nh, d)
+        v = rnd(self.lin(n, W["wv"])).reshape(T, nh, d)
         pos = np.concatenate([np.asarray(p) for (_, p, _, _) in batch])
         c, s = rope_cos_sin(pos, d, cfg["rope_theta"], table_f32=rnd is bf16)      # step 4.3
         q, k = rope(q, c, s, rnd), rope(k, c, s, rnd)
@@ -202,10 +203,10 @@ class Worker:
             e = np.exp(sc - mx)
             o[t0:t0 + m] = rnd(np.einsum("htk,khd->thd", e, Vc) / e.sum(axis=-1).T[:, :, None])
             t0 += m
-        h = rnd(x + linear(o.reshape(T, nh * d), W["wo"]))                          # step 4.6
+        h = rnd(x + self.lin(o.reshape(T, nh * d), W["wo"]))                          # step 4.6
         n2 = rmsnorm(h, W["ffn_norm"], eps, rnd)                                    # step 4.7
-        a = rnd(silu(linear(n2, W["wg"])) * linear(n2, W["wu"]))                    # step 4.8
-        return rnd(h + linear(a, W["wd"]))                                          # step 4.9
+        a = rnd(silu(self.lin(n2, W["wg"])) * self.lin(n2, W["wu"]))                    # step 4.8
+        return rnd(h + self.lin(a, W["wd"]))                                          # step 4.9
 
     _exact_cache: dict = {}
 
@@ -217,7 +218,7 @@ class Worker:
     def head(self, x_last: np.ndarray) -> np.ndarray:
         """Final RMSNorm + lm_head -> float64 logits (unrounded)."""
         nf = rmsnorm(x_last, self.w.final_norm(), self.cfg["rms_eps"], self.rnd)
-        return linear(nf, self.w.lm_head())
+        return self.lin(nf, self.w.lm_head())
 
 
 # ---------------------------------------------------------------- group --------------------
@@ -238,11 +239,11 @@ class Group:
     receives a byte copy of its hidden states."""
 
     def __init__(self, cfg: dict, weights: Weights | None = None, pp: int = 1,
-                 ranges=None, num_blocks: int = 256, rnd=bf16):
+                 ranges=None, num_blocks: int = 256, rnd=bf16, acc=np.float64):
         self.cfg = cfg
         self.w = weights or Weights(cfg)
         self.ranges = ranges or split_layers(cfg["n_layers"], pp)
-        self.workers = [Worker(cfg, self.w, b, e, num_blocks, rnd) for (b, e) in self.ranges]
+        self.workers = [Worker(cfg, self.w, b, e, num_blocks, rnd, acc) for (b, e) in self.ranges]
         self.bm = BlockManager(num_blocks)
         self.rnd = rnd
         self.handoff_bytes = 0

@@ -49,9 +49,14 @@ def rmsnorm(x: np.ndarray, w: np.ndarray, eps: float, rnd=bf16) -> np.ndarray:
     return rnd(x * r * w)
 
 
-def linear(x: np.ndarray, W: np.ndarray) -> np.ndarray:
-    """x [T,K] @ W[N,K]^T in float64, unrounded (the consumer rounds)."""
-    return x @ W.T
+def linear(x: np.ndarray, W: np.ndarray, acc=np.float64) -> np.ndarray:
+    """x [T,K] @ W[N,K]^T accumulated in float64, unrounded (the consumer rounds).
+    ``acc=np.float32`` gives the same product accumulated in float32: it is only used to
+    measure the noise floor any fp32-accumulating implementation has against this oracle
+    (DESIGN.md "Tolerance"), never as the reference."""
+    if acc is np.float64:
+        return x @ W.T
+    return (x.astype(acc) @ W.T.astype(acc)).astype(np.float64)
 
 
 def silu(g: np.ndarray) -> np.ndarray:

@@ -1,0 +1,444 @@
+// gemm.cu — tcgen05 + TMA GEMM (sm_100a) with fused epilogues and deterministic split-K.
+//
+// Kernel anatomy (one output tile of 128 features x BN tokens per CTA, 128 threads):
+//   warp 0 / lane 0 : TMA producer.  Per 64-wide K block it loads the weight tile
+//                     [128 x 64] and the activation tile [BN x 64] (128B swizzle) into a
+//                     ring of STAGES shared-memory slots, arming the slot's "full" mbarrier
+//                     with the expected transaction bytes.
+//   warp 1 / lane 0 : MMA issuer.  Waits "full", issues 4 x tcgen05.mma (M=128, N=BN, K=16)
+//                     accumulating into TMEM, and tcgen05.commit's the slot's "empty"
+//                     mbarrier so the producer can refill it; after the last K block it
+//                     commits the "accumulator ready" barrier.
+//   warp 2          : allocates / frees the TMEM columns.
+//   all 4 warps     : epilogue.  Warp w owns TMEM lanes [32w, 32w+32) = 32 output features;
+//                     tcgen05.ld 32 columns (tokens) at a time, apply the epilogue and store
+//                     out[token][feature] (or fp32 split-K partials).
+// The smem operand layout is the canonical K-major SWIZZLE_128B layout that TMA writes:
+// 8-row x 128-byte atoms, atoms 1024 B apart (SBO = 1024), K advanced inside the atom by
+// moving the descriptor start address by 32 B per UMMA_K = 16 elements.
+#include "gemm.h"
+
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+
+namespace hs {
+
+// ------------------------------------------------------------------ device helpers -------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+// Bounded wait: traps after ~4 s so a protocol bug ends the kernel instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  uint64_t t0 = 0;
+  for (uint32_t it = 0;; ++it) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (done) return;
+    if ((it & 1023) == 0) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 4000000000ull) __trap();
+    }
+  }
+}
+
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(const void* smem_tile) {
+  uint64_t a = smem_u32(smem_tile);
+  uint64_t d = 0;
+  d |= (a >> 4) & 0x3FFFull;             // start address
+  d |= 1ull << 16;                       // leading byte offset (unused for SW128 K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;      // stride byte offset: 8 rows x 128 B
+  d |= 1ull << 46;                       // descriptor version (sm_100)
+  d |= 2ull << 61;                       // SWIZZLE_128B
+  return d;
+}
+
+template <int BN>
+__device__ __forceinline__ constexpr uint32_t instr_desc() {
+  return (1u << 4)                       // D format f32
+         | (1u << 7) | (1u << 10)        // A, B = bf16
+         | ((uint32_t)(BN >> 3) << 17)   // N
+         | ((uint32_t)(128 >> 4) << 24); // M = 128
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db,
+                                          uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accum));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+
+struct KParams {
+  int M, N, K;
+  int kb_per_split;  // K blocks (of 64) per split
+  int nkb;           // total K blocks
+  int epi;           // GemmEpi, or -1 = fp32 partial into workspace
+  void* out;
+  int ldo;
+  const bf16* resid;
+  int ldr;
+  float* ws;
+};
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = 128 * 64 * 2;
+  static constexpr int B_BYTES = BN * 64 * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
+  static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(128, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                KParams p) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* accf = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * 128, n0 = blockIdx.y * BN;
+  const int kb0 = blockIdx.z * p.kb_per_split;
+  const int nk = min(p.kb_per_split, p.nkb - kb0);
+
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(accf, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"((uint32_t)C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer
+    for (int i = 0; i < nk; ++i) {
+      const int s = i % C::STAGES;
+      const uint32_t ph = (i / C::STAGES) & 1;
+      mbar_wait(&empty[s], ph ^ 1);
+      uint8_t* sa = smem + s * C::STAGE_BYTES;
+      uint8_t* sb = sa + C::A_BYTES;
+      mbar_expect_tx(&full[s], C::STAGE_BYTES);
+      const int kc = (kb0 + i) * 64;
+      tma_load_2d(&tmA, &full[s], sa, kc, m0);
+      tma_load_2d(&tmB, &full[s], sb, kc, n0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer
+    constexpr uint32_t idesc = instr_desc<BN>();
+    for (int i = 0; i < nk; ++i) {
+      const int s = i % C::STAGES;
+      const uint32_t ph = (i / C::STAGES) & 1;
+      mbar_wait(&full[s], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint8_t* sa = smem + s * C::STAGE_BYTES;
+      const uint8_t* sb = sa + C::A_BYTES;
+      const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sb);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)  // 64 / UMMA_K(16); +32 B => +2 in the >>4 address field
+        umma_bf16(tmem, da + 2 * k, db + 2 * k, idesc, (i | k) != 0);
+      umma_commit(&empty[s]);
+    }
+    umma_commit(accf);
+  }
+  __syncwarp();
+
+  // ---- epilogue: all 4 warps
+  mbar_wait(accf, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int m = m0 + warp * 32 + lane;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  constexpr int CH = BN < 32 ? 16 : 32;
+  for (int c0 = 0; c0 < BN; c0 += CH) {
+    float v[32];
+    if constexpr (CH == 32) tmem_ld32(trow + c0, v);
+    else tmem_ld16(trow + c0, v);
+    if (n0 + c0 >= p.N) break;  // warp-uniform
+    const int ncol = min(CH, p.N - n0 - c0);
+    if (p.epi < 0) {
+      float* ws = p.ws + ((size_t)blockIdx.z * p.N + n0 + c0) * p.M;
+      if (m < p.M)
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+          if (j < ncol) ws[(size_t)j * p.M + m] = v[j];
+    } else if (p.epi == EPI_F32) {
+      float* o = reinterpret_cast<float*>(p.out) + (size_t)(n0 + c0) * p.ldo;
+      if (m < p.M)
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+          if (j < ncol) o[(size_t)j * p.ldo + m] = v[j];
+    } else if (p.epi == EPI_BF16) {
+      bf16* o = reinterpret_cast<bf16*>(p.out) + (size_t)(n0 + c0) * p.ldo;
+      if (m < p.M)
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+          if (j < ncol) o[(size_t)j * p.ldo + m] = __float2bfloat16_rn(v[j]);
+    } else if (p.epi == EPI_RESID) {
+      bf16* o = reinterpret_cast<bf16*>(p.out) + (size_t)(n0 + c0) * p.ldo;
+      const bf16* r = p.resid + (size_t)(n0 + c0) * p.ldr;
+      if (m < p.M)
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+          if (j < ncol)
+            o[(size_t)j * p.ldo + m] = __float2bfloat16_rn(v[j] + __bfloat162float(r[(size_t)j * p.ldr + m]));
+    } else {  // EPI_SILU_MUL: lanes 0-15 gate rows, 16-31 the matching up rows
+      bf16* o = reinterpret_cast<bf16*>(p.out) + (size_t)(n0 + c0) * p.ldo;
+      const int f = (m0 + warp * 32) / 2 + lane;
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        float u = __shfl_xor_sync(0xffffffffu, v[j], 16);
+        if (lane < 16 && j < ncol && m < p.M) o[(size_t)j * p.ldo + f] = __float2bfloat16_rn(silu_f(v[j]) * u);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"((uint32_t)C::TMEM_COLS));
+  }
+}
+
+// Deterministic split-K reduction: sums the partials in split order, then the epilogue.
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N,
+                                     int epi, void* out, int ldo, const bf16* __restrict__ resid,
+                                     int ldr) {
+  const int n = blockIdx.y;
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  float acc = 0.f;
+  for (int s = 0; s < splits; ++s) acc += ws[((size_t)s * N + n) * M + m];
+  if (epi == EPI_F32) {
+    reinterpret_cast<float*>(out)[(size_t)n * ldo + m] = acc;
+  } else if (epi == EPI_BF16) {
+    reinterpret_cast<bf16*>(out)[(size_t)n * ldo + m] = __float2bfloat16_rn(acc);
+  } else if (epi == EPI_RESID) {
+    reinterpret_cast<bf16*>(out)[(size_t)n * ldo + m] =
+        __float2bfloat16_rn(acc + __bfloat162float(resid[(size_t)n * ldr + m]));
+  } else {  // silu-mul: m indexes physical rows; gate rows are j < 16 in each 32-row block
+    const int j = m & 31;
+    if (j < 16) {
+      float u = 0.f;
+      for (int s = 0; s < splits; ++s) u += ws[((size_t)s * N + n) * M + m + 16];
+      reinterpret_cast<bf16*>(out)[(size_t)n * ldo + (m >> 5) * 16 + j] =
+          __float2bfloat16_rn(silu_f(acc) * u);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host side -----------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  });
+  return fn;
+}
+
+hs_status make_tma(TmaMat* t, const void* ptr, int64_t rows, int64_t cols, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) HS_FAIL(HS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (cols % 64 || (reinterpret_cast<uintptr_t>(ptr) & 15)) HS_FAIL(HS_E_INVAL, "bad matrix for TMA");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&t->map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) HS_FAIL(HS_E_CUDA, "cuTensorMapEncodeTiled failed (%d) rows=%lld cols=%lld box=%d", (int)r,
+                                 (long long)rows, (long long)cols, box_rows);
+  t->ptr = ptr;
+  t->rows = rows;
+  t->cols = cols;
+  t->box_rows = box_rows;
+  return HS_OK;
+}
+
+static const int kBN[] = {16, 32, 64, 128, 256};
+int gemm_bn_count() { return 5; }
+int gemm_bn_value(int i) { return kBN[i]; }
+int gemm_bn(int N) {
+  if (N <= 16) return 16;
+  if (N <= 32) return 32;
+  if (N <= 64) return 64;
+  if (N <= 1024) return 128;
+  return 256;
+}
+
+template <int BN>
+static hs_status launch(const GemmArgs& a, int splits, int kbps, cudaStream_t st) {
+  using C = Cfg<BN>;
+  static bool attr_set[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !attr_set[dev]) {
+    HS_CUDA(cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set[dev] = true;
+  }
+  int bi = 0;
+  while (kBN[bi] != BN) ++bi;
+  const TmaMat& tb = a.B[bi];
+  if (tb.box_rows != BN || a.A->box_rows != 128) HS_FAIL(HS_E_INVAL, "TMA box mismatch");
+  KParams p;
+  p.M = a.M; p.N = a.N; p.K = a.K;
+  p.nkb = a.K / 64;
+  p.kb_per_split = kbps;
+  p.epi = splits > 1 ? -1 : a.epi;
+  p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr; p.ws = a.workspace;
+  dim3 grid(cdiv(a.M, 128), cdiv(a.N, BN), splits);
+  gemm_kernel<BN><<<grid, 128, C::SMEM, st>>>(a.A->map, tb.map, p);
+  count_launch();
+  HS_CUDA(cudaGetLastError());
+  if (splits > 1) {
+    dim3 g2(cdiv(a.M, 256), a.N);
+    splitk_reduce_kernel<<<g2, 256, 0, st>>>(a.workspace, splits, a.M, a.N, a.epi, a.out, a.ldo, a.resid, a.ldr);
+    count_launch();
+    HS_CUDA(cudaGetLastError());
+  }
+  return HS_OK;
+}
+
+template <int BN>
+static void warm_one() {
+  cudaFuncAttributes at;
+  cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM);
+  cudaFuncGetAttributes(&at, gemm_kernel<BN>);
+}
+
+void warm_gemm_kernels() {
+  warm_one<16>();
+  warm_one<32>();
+  warm_one<64>();
+  warm_one<128>();
+  warm_one<256>();
+  cudaFuncAttributes at;
+  cudaFuncGetAttributes(&at, splitk_reduce_kernel);
+}
+
+hs_status gemm(const GemmArgs& a, cudaStream_t st) {
+  if (a.M % 128 || a.K % 64 || a.N <= 0) HS_FAIL(HS_E_INVAL, "gemm shape M=%d N=%d K=%d", a.M, a.N, a.K);
+  const int BN = gemm_bn(a.N);
+  const int tiles = (a.M / 128) * (int)cdiv(a.N, BN);
+  const int nkb = a.K / 64;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int sms = num_sms(dev);
+  // split-K (deterministic: depends on M, N, K only) when the tile grid leaves SMs idle
+  int splits = 1;
+  if (a.workspace && tiles < sms) {
+    int best = 1;
+    double best_u = (double)tiles / sms;
+    for (int s = 2; s <= 16 && nkb / s >= 4; ++s) {
+      const int ctas = tiles * s;
+      const double waves = std::ceil((double)ctas / sms);
+      const double u = (double)ctas / (waves * sms) * std::min(1.0, (double)ctas / sms);
+      if (u > best_u + 1e-9 && (uint64_t)s * a.N * a.M * 4 <= a.workspace_bytes) { best = s; best_u = u; }
+    }
+    splits = best;
+  }
+  const int kbps = (int)cdiv(nkb, splits);
+  splits = (int)cdiv(nkb, kbps);
+  switch (BN) {
+    case 16: return launch<16>(a, splits, kbps, st);
+    case 32: return launch<32>(a, splits, kbps, st);
+    case 64: return launch<64>(a, splits, kbps, st);
+    case 128: return launch<128>(a, splits, kbps, st);
+    default: return launch<256>(a, splits, kbps, st);
+  }
+}
+
+}  // namespace hs

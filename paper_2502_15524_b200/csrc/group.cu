@@ -1,0 +1,1122 @@
+// group.cu — the pipeline-parallel worker group: device arenas, chunked H2D streaming with
+// per-layer readiness (a2-a4), the stage forward (a5-a15), decode (a16), consolidation (a17),
+// local (one process drives every stage GPU) and SPMD (one process per stage GPU, CUDA IPC
+// peer memory) modes.  See include/hs.h for the contract of every entry point.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <set>
+#include <vector>
+
+#include "common.h"
+#include "gemm.h"
+#include "kernels.h"
+
+namespace hs {
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch(uint64_t n) { g_launches += n; }
+uint64_t launch_total() { return g_launches.load(); }
+
+int num_sms(int device) {
+  static int cache[64] = {};
+  if (device < 0 || device >= 64) return 148;
+  if (!cache[device]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    cache[device] = v > 0 ? v : 148;
+  }
+  return cache[device];
+}
+
+static constexpr int kBlock = 16;
+static constexpr uint64_t kDefaultChunk = 32ull << 20;
+static constexpr uint64_t kWorkspace = 64ull << 20;
+static constexpr int kSendCtas = 64;
+
+// Comm block of a stage (one allocation, shared with peers): flags + token / hidden inputs.
+struct CommLayout {
+  static constexpr size_t FLAG_X = 0, FLAG_TOK = 4, DONE = 8, ERR = 12;
+  size_t tok_in = 256, x_in = 0, bytes = 0;
+  void init(int max_seqs, int max_tokens, int H) {
+    x_in = align_up(tok_in + (size_t)align_up(max_seqs * 4, 16), 256);
+    bytes = x_in + (size_t)max_tokens * H * 2;
+  }
+};
+
+struct LayerDev {
+  const bf16 *attn_norm = nullptr, *ffn_norm = nullptr;
+  TmaMat wqkv, wo, wgu, wd;
+  bool maps = false;
+};
+
+struct Share {  // what a stage publishes to its peers (SPMD allgather)
+  cudaIpcMemHandle_t comm, arena, kv;
+  uint64_t arena_off0, arena_bytes, kv_layer_bytes;
+  int32_t kv_lb, kv_le;  // layers whose pools exist in kv
+  int32_t device;
+};
+
+struct Stage {
+  int idx = 0, device = 0;
+  bool owned = false;       // driven by this process
+  bool full_memory = false;
+  int lb = 0, le = 0;       // current layer range
+  uint64_t slice_begin = 0, slice_end = 0;
+  // memory (owned stages: allocated here; remote stages: IPC-mapped, opened lazily)
+  uint8_t* arena = nullptr;
+  uint64_t arena_off0 = 0, arena_bytes = 0;
+  uint8_t* kv_mem = nullptr;
+  int kv_lb = 0, kv_le = 0;
+  uint8_t* comm = nullptr;
+  bool ipc_arena_open = false, ipc_comm_open = false;
+  Share share{};
+  // work buffers (owned)
+  bf16 *xa = nullptr, *xb = nullptr, *nrm = nullptr, *qkv = nullptr, *q = nullptr, *o = nullptr,
+       *act = nullptr, *fin = nullptr;
+  float *logits = nullptr, *ws = nullptr, *attn_ws = nullptr;
+  float2* rope = nullptr;
+  uint8_t* d_meta = nullptr;
+  uint8_t* h_meta = nullptr;  // pinned staging
+  int* h_out = nullptr;       // pinned: tokens + err
+  size_t meta_bytes = 0;
+  int* d_tok_out = nullptr;
+  cudaStream_t comp = nullptr, copy = nullptr;
+  cudaEvent_t ev_embed = nullptr, ev_final = nullptr, ev_l0 = nullptr, ev_l1 = nullptr;
+  cudaEvent_t ev_c0 = nullptr, ev_c1 = nullptr;  // start / end of the last call on comp
+  bool called = false;
+  std::vector<cudaEvent_t> ev_layer;
+  bool load_issued = false;
+  bool owns_streams = true;  // stages on one device share its streams (stream-ordered hand-off)
+  uint64_t loaded_bytes = 0;
+  std::vector<LayerDev> layers;
+  TmaMat lm;
+  TmaMat b_nrm[5], b_o[5], b_act[5], b_fin[5];
+  const hs_image* img = nullptr;
+
+  uint8_t* wptr(uint64_t image_off) const { return arena + (image_off - arena_off0); }
+  bf16* kv_pool(int l, uint64_t layer_bytes) const {
+    return reinterpret_cast<bf16*>(kv_mem + (uint64_t)(l - kv_lb) * layer_bytes);
+  }
+  unsigned* flag_x() const { return reinterpret_cast<unsigned*>(comm + CommLayout::FLAG_X); }
+  unsigned* flag_tok() const { return reinterpret_cast<unsigned*>(comm + CommLayout::FLAG_TOK); }
+  unsigned* done() const { return reinterpret_cast<unsigned*>(comm + CommLayout::DONE); }
+  int* err() const { return reinterpret_cast<int*>(comm + CommLayout::ERR); }
+};
+
+struct SeqState {
+  std::vector<int> blocks;
+  int ctx = 0;
+};
+
+}  // namespace hs
+
+struct hs_group {
+  hs_model_cfg cfg;
+  hs_plan plan;
+  hs_kv_cfg kv;
+  hs_image_header hdr;
+  bool spmd = false;
+  hs_comm comm{};
+  int owned_stage = -1;
+  bool dead = false;
+  std::vector<hs::Stage> st;
+  std::vector<int> active;  // stage indices in pipeline order
+  hs::CommLayout cl;
+  uint64_t kv_layer_bytes = 0, kv_block_bytes = 0;
+  int max_blocks = 0;  // per sequence
+  // centralised block manager (identical on every rank)
+  std::set<int> free_blocks;
+  std::map<int64_t, hs::SeqState> seqs;
+  std::vector<int64_t> last_ids;  // seq order of the previous call (device token feedback)
+  unsigned epoch = 0;
+  // per-kernel-kind event profile (hs_profile_*)
+  bool prof_on = false;
+  struct ProfRec { int kind; int device; cudaEvent_t a, b; double bytes, flops; };
+  std::vector<ProfRec> prof;
+  std::map<int, std::vector<cudaEvent_t>> ev_free;  // per device
+  struct ProfAcc { uint64_t count = 0; double ms = 0, bytes = 0, flops = 0; };
+  std::map<int, ProfAcc> prof_acc;
+};
+
+namespace hs {
+
+static hs_status stage_of_layer(hs_group* g, int layer, int* out) {
+  for (int k : g->active)
+    if (layer >= g->st[k].lb && layer < g->st[k].le) { *out = k; return HS_OK; }
+  HS_FAIL(HS_E_INVAL, "layer %d not held by any active stage", layer);
+}
+
+// ---- per-kernel-kind profile ------------------------------------------------------------
+enum ProfKind { PK_EMBED, PK_RMSNORM, PK_GEMM_QKV, PK_ROPE_KV, PK_ATTN, PK_GEMM_O, PK_GEMM_GU, PK_GEMM_DOWN,
+                PK_LM_HEAD, PK_ARGMAX, PK_SEND, PK_WAIT, PK_N };
+static const char* kProfNames[PK_N] = {"embed", "rmsnorm", "gemm_qkv", "rope_kv", "attention", "gemm_o",
+                                       "gemm_gate_up", "gemm_down", "gemm_lm_head", "argmax", "send", "wait"};
+
+static cudaEvent_t prof_event(hs_group* g, int dev) {
+  auto& v = g->ev_free[dev];
+  if (!v.empty()) { cudaEvent_t e = v.back(); v.pop_back(); return e; }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct ProfScope {
+  hs_group* g; Stage& s; int kind; double bytes, flops; cudaEvent_t a = nullptr;
+  ProfScope(hs_group* g_, Stage& s_, int kind_, bool decode, double bytes_, double flops_)
+      : g(g_), s(s_), kind(kind_ * 2 + (decode ? 1 : 0)), bytes(bytes_), flops(flops_) {
+    if (g->prof_on) { a = prof_event(g, s.device); cudaEventRecord(a, s.comp); }
+  }
+  ~ProfScope() {
+    if (!a) return;
+    cudaEvent_t b = prof_event(g, s.device);
+    cudaEventRecord(b, s.comp);
+    g->prof.push_back({kind, s.device, a, b, bytes, flops});
+  }
+};
+
+static hs_status prof_collect(hs_group* g) {
+  for (auto& r : g->prof) {
+    DeviceGuard dg(r.device);
+    HS_CUDA(cudaEventSynchronize(r.b));
+    float ms = 0;
+    HS_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    auto& acc = g->prof_acc[r.kind];
+    acc.count++; acc.ms += ms; acc.bytes += r.bytes; acc.flops += r.flops;
+    g->ev_free[r.device].push_back(r.a);
+    g->ev_free[r.device].push_back(r.b);
+  }
+  g->prof.clear();
+  return HS_OK;
+}
+
+static double gemm_bytes(double M, double N, double K, double Mout, bool resid) {
+  return 2.0 * (M * K + N * K + N * Mout + (resid ? N * Mout : 0.0));
+}
+
+// Free everything a stage owns (device + pinned).
+static void free_stage(Stage& s) {
+  DeviceGuard dg(s.device);
+  auto F = [](void* p) { if (p) cudaFree(p); };
+  if (s.owned) {
+    F(s.arena); F(s.kv_mem); F(s.comm); F(s.xa); F(s.xb); F(s.nrm); F(s.qkv); F(s.q); F(s.o);
+    F(s.act); F(s.fin); F(s.logits); F(s.ws); F(s.attn_ws); F(s.rope); F(s.d_meta); F(s.d_tok_out);
+    if (s.h_meta) cudaFreeHost(s.h_meta);
+    if (s.h_out) cudaFreeHost(s.h_out);
+    for (auto e : s.ev_layer) if (e) cudaEventDestroy(e);
+    for (auto e : {s.ev_embed, s.ev_final, s.ev_l0, s.ev_l1, s.ev_c0, s.ev_c1}) if (e) cudaEventDestroy(e);
+    if (s.owns_streams && s.comp) cudaStreamDestroy(s.comp);
+    if (s.owns_streams && s.copy) cudaStreamDestroy(s.copy);
+  } else {
+    if (s.ipc_comm_open && s.comm) cudaIpcCloseMemHandle(s.comm);
+    if (s.ipc_arena_open) {
+      if (s.arena) cudaIpcCloseMemHandle(s.arena);
+      if (s.kv_mem) cudaIpcCloseMemHandle(s.kv_mem);
+    }
+  }
+  s = Stage{};
+}
+
+static hs_status make_layer_maps(hs_group* g, Stage& s, int l) {
+  const hs_model_cfg& c = g->cfg;
+  const hs_image_header& h = g->hdr;
+  const uint64_t L0 = h.layer_off[l];
+  LayerDev& d = s.layers[l];
+  d.attn_norm = reinterpret_cast<const bf16*>(s.wptr(L0 + h.t_attn_norm));
+  d.ffn_norm = reinterpret_cast<const bf16*>(s.wptr(L0 + h.t_ffn_norm));
+  HS_TRY(make_tma(&d.wqkv, s.wptr(L0 + h.t_wqkv), 3 * c.hidden, c.hidden, 128));
+  HS_TRY(make_tma(&d.wo, s.wptr(L0 + h.t_wo), c.hidden, c.hidden, 128));
+  HS_TRY(make_tma(&d.wgu, s.wptr(L0 + h.t_wgu), 2 * c.ffn, c.hidden, 128));
+  HS_TRY(make_tma(&d.wd, s.wptr(L0 + h.t_wd), c.hidden, c.ffn, 128));
+  d.maps = true;
+  return HS_OK;
+}
+
+static hs_status make_act_maps(TmaMat* m, const void* p, int64_t rows, int64_t cols) {
+  for (int i = 0; i < gemm_bn_count(); ++i) HS_TRY(make_tma(&m[i], p, rows, cols, gemm_bn_value(i)));
+  return HS_OK;
+}
+
+#define HS_ALLOC(ptr, bytes) HS_CUDA(cudaMalloc(reinterpret_cast<void**>(&(ptr)), (bytes)))
+
+static hs_status setup_owned_stage(hs_group* g, int k) {
+  Stage& s = g->st[k];
+  const hs_model_cfg& c = g->cfg;
+  const hs_image_header& h = g->hdr;
+  const int T = g->kv.max_tokens, S = g->kv.max_seqs;
+  const int H = c.hidden;
+  DeviceGuard dg(s.device);
+  HS_CUDA(cudaSetDevice(s.device));
+  // arena: whole model (full-memory worker) or the stage slice (low-memory worker)
+  s.arena_off0 = s.full_memory ? h.embed_off : s.slice_begin;
+  s.arena_bytes = (s.full_memory ? h.total_bytes : s.slice_end) - s.arena_off0;
+  HS_ALLOC(s.arena, s.arena_bytes);
+  s.kv_lb = s.full_memory ? 0 : s.lb;
+  s.kv_le = s.full_memory ? c.n_layers : s.le;
+  HS_ALLOC(s.kv_mem, (uint64_t)(s.kv_le - s.kv_lb) * g->kv_layer_bytes);
+  HS_ALLOC(s.comm, g->cl.bytes);
+  HS_CUDA(cudaMemset(s.comm, 0, g->cl.bytes));
+  HS_ALLOC(s.xa, (size_t)T * H * 2);
+  HS_ALLOC(s.xb, (size_t)T * H * 2);
+  HS_ALLOC(s.nrm, (size_t)T * H * 2);
+  HS_ALLOC(s.qkv, (size_t)T * 3 * H * 2);
+  HS_ALLOC(s.q, (size_t)T * H * 2);
+  HS_ALLOC(s.o, (size_t)T * H * 2);
+  HS_ALLOC(s.act, (size_t)T * c.ffn * 2);
+  HS_ALLOC(s.fin, (size_t)std::max(S, 16) * H * 2);
+  HS_ALLOC(s.logits, (size_t)S * c.vocab * 4);
+  HS_ALLOC(s.ws, kWorkspace);
+  HS_ALLOC(s.attn_ws, (size_t)S * c.n_heads * 16 * (c.head_dim + 2) * 4);
+  HS_ALLOC(s.d_tok_out, (size_t)align_up(S * 4, 16) + 16);
+  // RoPE table (fp32 cos/sin of angle = p * theta^(-2i/d), computed in double), DESIGN.md
+  {
+    const int hd = c.head_dim / 2;
+    std::vector<float2> tab((size_t)c.max_seq * hd);
+    for (int p = 0; p < c.max_seq; ++p)
+      for (int i = 0; i < hd; ++i) {
+        const double ang = (double)p * std::pow((double)c.rope_theta, -2.0 * i / c.head_dim);
+        tab[(size_t)p * hd + i] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+      }
+    HS_ALLOC(s.rope, tab.size() * sizeof(float2));
+    HS_CUDA(cudaMemcpy(s.rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  }
+  s.meta_bytes = (size_t)T * 12 + (size_t)S * (8 + sizeof(SeqDesc) + (size_t)g->max_blocks * 4) + 1024;
+  HS_ALLOC(s.d_meta, s.meta_bytes);
+  HS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.h_meta), s.meta_bytes, cudaHostAllocDefault));
+  HS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.h_out), (size_t)S * 4 + 64, cudaHostAllocDefault));
+  int lo = 0, hi = 0;
+  HS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  s.owns_streams = true;
+  for (int j = 0; j < k; ++j)
+    if (g->st[j].owned && g->st[j].device == s.device) {
+      s.comp = g->st[j].comp;
+      s.copy = g->st[j].copy;
+      s.owns_streams = false;
+      break;
+    }
+  if (s.owns_streams) {
+    HS_CUDA(cudaStreamCreateWithPriority(&s.comp, cudaStreamNonBlocking, hi));  // critical path
+    HS_CUDA(cudaStreamCreateWithPriority(&s.copy, cudaStreamNonBlocking, lo));
+  }
+  HS_CUDA(cudaEventCreateWithFlags(&s.ev_embed, cudaEventDisableTiming));
+  HS_CUDA(cudaEventCreateWithFlags(&s.ev_final, cudaEventDisableTiming));
+  HS_CUDA(cudaEventCreate(&s.ev_l0));
+  HS_CUDA(cudaEventCreate(&s.ev_l1));
+  HS_CUDA(cudaEventCreate(&s.ev_c0));
+  HS_CUDA(cudaEventCreate(&s.ev_c1));
+  s.ev_layer.assign(c.n_layers, nullptr);
+  for (int l = 0; l < c.n_layers; ++l) HS_CUDA(cudaEventCreateWithFlags(&s.ev_layer[l], cudaEventDisableTiming));
+  // TMA descriptors: weights of every layer the arena holds, activation operands
+  s.layers.assign(c.n_layers, LayerDev{});
+  const int wl0 = s.full_memory ? 0 : s.lb, wl1 = s.full_memory ? c.n_layers : s.le;
+  for (int l = wl0; l < wl1; ++l) HS_TRY(make_layer_maps(g, s, l));
+  if (s.full_memory || s.le == c.n_layers)
+    HS_TRY(make_tma(&s.lm, s.wptr(h.final_off + h.t_lm_head), c.vocab, H, 128));
+  HS_TRY(make_act_maps(s.b_nrm, s.nrm, T, H));
+  HS_TRY(make_act_maps(s.b_o, s.o, T, H));
+  HS_TRY(make_act_maps(s.b_act, s.act, T, c.ffn));
+  HS_TRY(make_act_maps(s.b_fin, s.fin, std::max(S, 16), H));
+  warm_gemm_kernels();
+  warm_kernels();
+  HS_CUDA(cudaDeviceSynchronize());
+  return HS_OK;
+}
+
+static hs_status validate_image(hs_group* g, const hs_image* im, uint64_t b, uint64_t e) {
+  if (!im || !im->data) HS_FAIL(HS_E_INVAL, "missing image for a stage");
+  if (im->data_offset > b || im->data_offset + im->data_bytes < e)
+    HS_FAIL(HS_E_INVAL, "image data [%llu,%llu) does not cover stage slice [%llu,%llu)",
+            (unsigned long long)im->data_offset, (unsigned long long)(im->data_offset + im->data_bytes),
+            (unsigned long long)b, (unsigned long long)e);
+  return HS_OK;
+}
+
+// ------------------------------------------------------------------ create ---------------
+static hs_status create(const hs_model_cfg* cfg, const hs_plan* plan, const hs_image* image,
+                        const hs_image* stage_images, const hs_kv_cfg* kv, const hs_comm* comm,
+                        hs_group** out) {
+  if (!cfg || !plan || !kv || !out) HS_FAIL(HS_E_INVAL, "null argument");
+  std::unique_ptr<hs_group> g(new hs_group());
+  g->cfg = *cfg;
+  if (hs_image_layout(cfg, &g->hdr) != HS_OK) return HS_E_INVAL;
+  const hs_image* any = (image && image->header) ? image : nullptr;
+  for (int k = 0; !any && stage_images && k < plan->pp && k < HS_MAX_STAGES; ++k)
+    if (stage_images[k].header) any = &stage_images[k];
+  if (!any || !any->header) HS_FAIL(HS_E_INVAL, "image header required");
+  const hs_image_header* ih = any->header;
+  if (ih->magic != HS_IMAGE_MAGIC || ih->total_bytes != g->hdr.total_bytes || ih->layer_bytes != g->hdr.layer_bytes ||
+      ih->t_wgu != g->hdr.t_wgu || ih->t_lm_head != g->hdr.t_lm_head || ih->gu_interleave != HS_GU_INTERLEAVE ||
+      memcmp(&ih->cfg, cfg, sizeof(hs_model_cfg)) != 0)
+    HS_FAIL(HS_E_INVAL, "image header does not match the model cfg / layout");
+  if (kv->block_tokens != kBlock || kv->num_blocks <= 0 || kv->max_seqs <= 0 || kv->max_tokens <= 0)
+    HS_FAIL(HS_E_INVAL, "kv cfg: block_tokens must be 16 and sizes > 0");
+  if (plan->pp < 1 || plan->pp > HS_MAX_STAGES) HS_FAIL(HS_E_INVAL, "bad plan");
+  g->plan = *plan;
+  g->kv = *kv;
+  g->kv.max_seqs = std::max(kv->max_seqs, 1);
+  g->max_blocks = (cfg->max_seq + kBlock - 1) / kBlock;
+  g->kv_block_bytes = (uint64_t)kBlock * 2 * cfg->hidden * 2;
+  g->kv_layer_bytes = g->kv_block_bytes * (uint64_t)kv->num_blocks;
+  g->cl.init(g->kv.max_seqs, kv->max_tokens, cfg->hidden);
+  for (int b = 0; b < kv->num_blocks; ++b) g->free_blocks.insert(b);
+  const int pp = plan->pp;
+  g->st.resize(pp);
+  for (int k = 0; k < pp; ++k) {
+    Stage& s = g->st[k];
+    s.idx = k;
+    s.device = plan->device[k];
+    s.full_memory = plan->full_memory[k] != 0;
+    s.lb = plan->layer_begin[k];
+    s.le = plan->layer_end[k];
+    s.slice_begin = plan->slice_begin[k];
+    s.slice_end = plan->slice_end[k];
+    if (s.le <= s.lb || (k > 0 && s.lb != plan->layer_end[k - 1])) HS_FAIL(HS_E_INVAL, "plan ranges not contiguous");
+    g->active.push_back(k);
+  }
+  if (g->st[0].lb != 0 || g->st[pp - 1].le != cfg->n_layers) HS_FAIL(HS_E_INVAL, "plan does not cover all layers");
+  if (comm) {
+    if (comm->world != pp || comm->rank < 0 || comm->rank >= pp || !comm->allgather || !comm->barrier)
+      HS_FAIL(HS_E_INVAL, "comm must have world == pp and allgather/barrier callbacks");
+    g->spmd = true;
+    g->comm = *comm;
+    g->owned_stage = comm->rank;
+  }
+  for (int k = 0; k < pp; ++k) {
+    Stage& s = g->st[k];
+    s.owned = !g->spmd || k == g->owned_stage;
+    if (!s.owned) continue;
+    s.img = stage_images ? &stage_images[k] : image;
+    HS_TRY(validate_image(g.get(), s.img, s.slice_begin, s.slice_end));
+  }
+  // peer access between every pair of stage GPUs this process drives (local mode)
+  if (!g->spmd) {
+    for (int a = 0; a < pp; ++a)
+      for (int b = 0; b < pp; ++b) {
+        const int da = g->st[a].device, db = g->st[b].device;
+        if (da == db) continue;
+        int ok = 0;
+        HS_CUDA(cudaDeviceCanAccessPeer(&ok, da, db));
+        if (!ok) HS_FAIL(HS_E_PEER, "GPU %d cannot access GPU %d", da, db);
+        DeviceGuard dg(da);
+        cudaSetDevice(da);
+        cudaError_t e = cudaDeviceEnablePeerAccess(db, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) HS_CUDA(e);
+        cudaGetLastError();
+      }
+  }
+  for (int k = 0; k < pp; ++k)
+    if (g->st[k].owned) {
+      hs_status r = setup_owned_stage(g.get(), k);
+      if (r != HS_OK) {
+        for (auto& s : g->st) free_stage(s);
+        return r;
+      }
+    }
+  if (g->spmd) {  // exchange IPC handles, map every peer's comm block
+    Stage& me = g->st[g->owned_stage];
+    DeviceGuard dg(me.device);
+    cudaSetDevice(me.device);
+    Share sh{};
+    HS_CUDA(cudaIpcGetMemHandle(&sh.comm, me.comm));
+    HS_CUDA(cudaIpcGetMemHandle(&sh.arena, me.arena));
+    HS_CUDA(cudaIpcGetMemHandle(&sh.kv, me.kv_mem));
+    sh.arena_off0 = me.arena_off0;
+    sh.arena_bytes = me.arena_bytes;
+    sh.kv_layer_bytes = g->kv_layer_bytes;
+    sh.kv_lb = me.kv_lb;
+    sh.kv_le = me.kv_le;
+    sh.device = me.device;
+    std::vector<Share> all(pp);
+    if (g->comm.allgather(g->comm.ctx, &sh, sizeof(Share), all.data()) != 0) HS_FAIL(HS_E_STATE, "allgather failed");
+    for (int k = 0; k < pp; ++k) {
+      if (k == g->owned_stage) continue;
+      Stage& s = g->st[k];
+      s.share = all[k];
+      s.arena_off0 = all[k].arena_off0;
+      s.arena_bytes = all[k].arena_bytes;
+      s.kv_lb = all[k].kv_lb;
+      s.kv_le = all[k].kv_le;
+      void* p = nullptr;
+      HS_CUDA(cudaIpcOpenMemHandle(&p, all[k].comm, cudaIpcMemLazyEnablePeerAccess));
+      s.comm = reinterpret_cast<uint8_t*>(p);
+      s.ipc_comm_open = true;
+    }
+    if (g->comm.barrier(g->comm.ctx) != 0) HS_FAIL(HS_E_STATE, "barrier failed");
+  }
+  *out = g.release();
+  return HS_OK;
+}
+
+// ------------------------------------------------------------------ load (a3, a4) --------
+static hs_status load_stage(hs_group* g, int k, uint64_t chunk) {
+  Stage& s = g->st[k];
+  if (!s.owned) return HS_OK;
+  const hs_image_header& h = g->hdr;
+  const hs_model_cfg& c = g->cfg;
+  if (chunk == 0) chunk = kDefaultChunk;
+  DeviceGuard dg(s.device);
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(s.img->data);
+  auto copy_region = [&](uint64_t off, uint64_t bytes, cudaEvent_t ev) -> hs_status {
+    for (uint64_t o = 0; o < bytes; o += chunk) {
+      const uint64_t n = std::min(chunk, bytes - o);
+      HS_CUDA(cudaMemcpyAsync(s.wptr(off + o), src + (off + o - s.img->data_offset), n, cudaMemcpyHostToDevice, s.copy));
+    }
+    if (ev) HS_CUDA(cudaEventRecord(ev, s.copy));
+    s.loaded_bytes += bytes;
+    return HS_OK;
+  };
+  s.loaded_bytes = 0;
+  HS_CUDA(cudaEventRecord(s.ev_l0, s.copy));
+  // critical order: embedding, layers b..e-1, final norm + lm_head (R4)
+  if (s.lb == 0 && k == g->active.front()) HS_TRY(copy_region(h.embed_off, h.embed_bytes, s.ev_embed));
+  for (int l = s.lb; l < s.le; ++l) HS_TRY(copy_region(h.layer_off[l], h.layer_bytes, s.ev_layer[l]));
+  if (s.le == c.n_layers) HS_TRY(copy_region(h.final_off, h.final_bytes, s.ev_final));
+  HS_CUDA(cudaEventRecord(s.ev_l1, s.copy));
+  s.load_issued = true;
+  return HS_OK;
+}
+
+// ------------------------------------------------------------------ forward --------------
+struct CallMeta {
+  int T = 0, n = 0, max_nq = 0, max_ctx = 0;
+  bool decode = false;
+  double kv_tokens = 0, attn_pairs = 0;  // KV rows read by attention, (query, key) pairs
+  size_t o_tok = 0, o_pos = 0, o_slot = 0, o_last = 0, o_seqs = 0, o_tab = 0, bytes = 0;
+};
+
+static void layout_meta(CallMeta& m, int max_blocks) {
+  size_t o = 0;
+  auto take = [&](size_t b) { size_t r = o; o = align_up(o + b, 16); return r; };
+  m.o_tok = take((size_t)m.T * 4);
+  m.o_pos = take((size_t)m.T * 4);
+  m.o_slot = take((size_t)m.T * 4);
+  m.o_last = take((size_t)m.n * 4);
+  m.o_seqs = take((size_t)m.n * sizeof(SeqDesc));
+  m.o_tab = take((size_t)m.n * max_blocks * 4);
+  m.bytes = o;
+}
+
+static hs_status run_layer(hs_group* g, Stage& s, int l, bf16*& x, const CallMeta& m) {
+  const hs_model_cfg& c = g->cfg;
+  const int H = c.hidden, T = m.T;
+  LayerDev& L = s.layers[l];
+  cudaStream_t st = s.comp;
+  const int* pos = reinterpret_cast<const int*>(s.d_meta + m.o_pos);
+  const int* slot = reinterpret_cast<const int*>(s.d_meta + m.o_slot);
+  const SeqDesc* sd = reinterpret_cast<const SeqDesc*>(s.d_meta + m.o_seqs);
+  const int* tab = reinterpret_cast<const int*>(s.d_meta + m.o_tab);
+  bf16* pool = s.kv_pool(l, g->kv_layer_bytes);
+  bf16* hbuf = (x == s.xb) ? s.xa : s.xb;
+  const bool dec = m.decode;
+  const double TH2 = 2.0 * T * H, F = c.ffn;
+  { ProfScope ps(g, s, PK_RMSNORM, dec, 2 * TH2 + 2.0 * H, 0);
+    launch_rmsnorm(x, nullptr, L.attn_norm, s.nrm, T, H, c.rms_eps, st); }
+  GemmArgs a{};
+  a.N = T; a.K = H; a.workspace = s.ws; a.workspace_bytes = kWorkspace;
+  a.A = &L.wqkv; a.B = s.b_nrm; a.M = 3 * H; a.epi = EPI_BF16; a.out = s.qkv; a.ldo = 3 * H;
+  { ProfScope ps(g, s, PK_GEMM_QKV, dec, gemm_bytes(3.0 * H, T, H, 3.0 * H, false), 2.0 * 3 * H * T * H);
+    HS_TRY(gemm(a, st)); }
+  { ProfScope ps(g, s, PK_ROPE_KV, dec, 3 * TH2 + 3 * TH2, 0);
+    launch_rope_kv(s.qkv, pos, slot, s.rope, s.q, pool, T, c.n_heads, c.head_dim, st); }
+  { ProfScope ps(g, s, PK_ATTN, dec, 2 * TH2 + 2.0 * 2 * H * m.kv_tokens, 4.0 * H * m.attn_pairs);
+    if (m.decode)
+      launch_attn_decode(s.q, pool, sd, m.n, m.max_ctx, tab, g->max_blocks, s.o, c.n_heads, c.head_dim,
+                         s.attn_ws, attn_decode_splits(m.max_ctx), st);
+    else
+      launch_attn_prefill(s.q, pool, sd, m.n, m.max_nq, tab, g->max_blocks, s.o, c.n_heads, c.head_dim, st); }
+  a.A = &L.wo; a.B = s.b_o; a.M = H; a.K = H; a.epi = EPI_RESID; a.out = hbuf; a.ldo = H; a.resid = x; a.ldr = H;
+  { ProfScope ps(g, s, PK_GEMM_O, dec, gemm_bytes(H, T, H, H, true), 2.0 * H * T * H);
+    HS_TRY(gemm(a, st)); }
+  { ProfScope ps(g, s, PK_RMSNORM, dec, 2 * TH2 + 2.0 * H, 0);
+    launch_rmsnorm(hbuf, nullptr, L.ffn_norm, s.nrm, T, H, c.rms_eps, st); }
+  a.A = &L.wgu; a.B = s.b_nrm; a.M = 2 * c.ffn; a.K = H; a.epi = EPI_SILU_MUL; a.out = s.act; a.ldo = c.ffn;
+  a.resid = nullptr;
+  { ProfScope ps(g, s, PK_GEMM_GU, dec, gemm_bytes(2 * F, T, H, F, false), 2.0 * 2 * F * T * H);
+    HS_TRY(gemm(a, st)); }
+  bf16* xout = (hbuf == s.xa) ? s.xb : s.xa;
+  a.A = &L.wd; a.B = s.b_act; a.M = H; a.K = c.ffn; a.epi = EPI_RESID; a.out = xout; a.ldo = H; a.resid = hbuf;
+  a.ldr = H;
+  { ProfScope ps(g, s, PK_GEMM_DOWN, dec, gemm_bytes(H, T, F, H, true), 2.0 * H * T * F);
+    HS_TRY(gemm(a, st)); }
+  x = xout;
+  return HS_OK;
+}
+
+// Enqueues one call (prefill or decode) on every owned stage; returns after the tokens of
+// the call are on the host.
+static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int64_t>& ids,
+                          const std::vector<int>& host_tokens, bool feedback, int32_t* out_tokens,
+                          float* out_logits) {
+  const hs_model_cfg& c = g->cfg;
+  const unsigned ep = ++g->epoch;
+  const int first = g->active.front(), last = g->active.back();
+  CallMeta m = m0;
+  layout_meta(m, g->max_blocks);
+  for (size_t ai = 0; ai < g->active.size(); ++ai) {
+    const int k = g->active[ai];
+    Stage& s = g->st[k];
+    if (!s.owned) continue;
+    if (!s.load_issued) HS_FAIL(HS_E_STATE, "stage %d: no load issued (call hs_load_stage_async first)", k);
+    if (m.bytes > s.meta_bytes) HS_FAIL(HS_E_INVAL, "call metadata too large");
+    DeviceGuard dg(s.device);
+    cudaStream_t st = s.comp;
+    // host metadata (identical on every stage: centralised block manager)
+    uint8_t* hm = s.h_meta;
+    int* tok = reinterpret_cast<int*>(hm + m.o_tok);
+    int* pos = reinterpret_cast<int*>(hm + m.o_pos);
+    int* slot = reinterpret_cast<int*>(hm + m.o_slot);
+    int* lastr = reinterpret_cast<int*>(hm + m.o_last);
+    SeqDesc* sd = reinterpret_cast<SeqDesc*>(hm + m.o_seqs);
+    int* tab = reinterpret_cast<int*>(hm + m.o_tab);
+    // per-sequence descriptors, block tables and per-token positions / KV slots
+    int t = 0;
+    for (int i = 0; i < m.n; ++i) {
+      const SeqState& ss = g->seqs[ids[i]];
+      const int n_new = m.decode ? 1 : ss.ctx;  // prefill: ctx == prompt length
+      const int p0 = ss.ctx - n_new;
+      sd[i].q_start = t;
+      sd[i].n_q = n_new;
+      sd[i].pos0 = p0;
+      for (int j = 0; j < n_new; ++j) {
+        const int p = p0 + j;
+        pos[t] = p;
+        slot[t] = ss.blocks[p / kBlock] * kBlock + p % kBlock;
+        tok[t] = host_tokens.empty() ? 0 : host_tokens[t];
+        ++t;
+      }
+      lastr[i] = t - 1;
+      for (int b = 0; b < g->max_blocks; ++b)
+        tab[(size_t)i * g->max_blocks + b] = b < (int)ss.blocks.size() ? ss.blocks[b] : 0;
+      sd[i].table = i;
+    }
+    HS_CUDA(cudaEventRecord(s.ev_c0, st));
+    HS_CUDA(cudaMemcpyAsync(s.d_meta, hm, m.bytes, cudaMemcpyHostToDevice, st));
+    const int* d_tok = reinterpret_cast<const int*>(s.d_meta + m.o_tok);
+    const bool dec = m.decode;
+    bf16* x = nullptr;
+    if (k == first) {
+      if (s.lb == 0) HS_CUDA(cudaStreamWaitEvent(st, s.ev_embed, 0));
+      const bf16* E = reinterpret_cast<const bf16*>(s.wptr(g->hdr.embed_off));
+      if (feedback) {
+        ProfScope ps(g, s, PK_WAIT, dec, 0, 0);
+        launch_wait(s.flag_tok(), ep - 1, s.err(), st);
+        d_tok = reinterpret_cast<const int*>(s.comm + g->cl.tok_in);
+      }
+      ProfScope ps(g, s, PK_EMBED, dec, 4.0 * m.T * c.hidden, 0);
+      launch_embed(d_tok, E, s.xa, m.T, c.hidden, st);
+      x = s.xa;
+    } else {
+      ProfScope ps(g, s, PK_WAIT, dec, 0, 0);
+      launch_wait(s.flag_x(), ep, s.err(), st);
+      x = reinterpret_cast<bf16*>(s.comm + g->cl.x_in);
+    }
+    for (int l = s.lb; l < s.le; ++l) {
+      HS_CUDA(cudaStreamWaitEvent(st, s.ev_layer[l], 0));
+      HS_TRY(run_layer(g, s, l, x, m));
+    }
+    if (k != last) {
+      Stage& nx = g->st[g->active[ai + 1]];
+      ProfScope ps(g, s, PK_SEND, dec, 2.0 * m.T * c.hidden, 0);
+      launch_send(x, nx.comm + g->cl.x_in, (uint64_t)m.T * c.hidden * 2, s.done(), nx.flag_x(), ep, kSendCtas, st);
+    } else {
+      if (s.le == c.n_layers) HS_CUDA(cudaStreamWaitEvent(st, s.ev_final, 0));
+      const int* d_last = reinterpret_cast<const int*>(s.d_meta + m.o_last);
+      {
+        ProfScope ps(g, s, PK_RMSNORM, dec, 4.0 * m.n * c.hidden, 0);
+        launch_rmsnorm(x, d_last, reinterpret_cast<const bf16*>(s.wptr(g->hdr.final_off + g->hdr.t_final_norm)),
+                       s.fin, m.n, c.hidden, c.rms_eps, st);
+      }
+      GemmArgs a{};
+      a.A = &s.lm; a.B = s.b_fin; a.M = c.vocab; a.N = m.n; a.K = c.hidden; a.epi = EPI_F32; a.out = s.logits;
+      a.ldo = c.vocab; a.workspace = s.ws; a.workspace_bytes = kWorkspace;
+      {
+        ProfScope ps(g, s, PK_LM_HEAD, dec, 2.0 * c.vocab * c.hidden + 2.0 * m.n * c.hidden + 4.0 * m.n * c.vocab,
+                     2.0 * c.vocab * m.n * c.hidden);
+        HS_TRY(gemm(a, st));
+      }
+      {
+        ProfScope ps(g, s, PK_ARGMAX, dec, 4.0 * m.n * c.vocab, 0);
+        launch_argmax(s.logits, c.vocab, m.n, s.d_tok_out, st);
+      }
+      const uint64_t tb = align_up((uint64_t)m.n * 4, 16);
+      // token feedback to the first stage (the next decode embeds it on the device); in SPMD
+      // mode to every stage, so that every rank can return the tokens
+      for (int kk : g->active) {
+        if (!g->spmd && kk != first) continue;
+        Stage& d = g->st[kk];
+        launch_send(s.d_tok_out, d.comm + g->cl.tok_in, tb, s.done(), d.flag_tok(), ep, 1, st);
+      }
+      HS_CUDA(cudaMemcpyAsync(s.h_out, s.d_tok_out, (size_t)m.n * 4, cudaMemcpyDeviceToHost, st));
+      if (out_logits)
+        HS_CUDA(cudaMemcpyAsync(out_logits, s.logits, (size_t)m.n * c.vocab * 4, cudaMemcpyDeviceToHost, st));
+    }
+    if (k != last && g->spmd) {  // non-last SPMD ranks read the broadcast tokens
+      launch_wait(s.flag_tok(), ep, s.err(), st);
+      HS_CUDA(cudaMemcpyAsync(s.h_out, s.comm + g->cl.tok_in, (size_t)m.n * 4, cudaMemcpyDeviceToHost, st));
+    }
+    HS_CUDA(cudaMemcpyAsync(s.h_out + m.n, s.err(), 4, cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaEventRecord(s.ev_c1, st));
+    s.called = true;
+  }
+  // wait for the result on the stage(s) this process owns
+  int err = 0;
+  bool got = false;
+  for (int k : g->active) {
+    Stage& s = g->st[k];
+    if (!s.owned) continue;
+    DeviceGuard dg(s.device);
+    cudaError_t e = cudaStreamSynchronize(s.comp);
+    if (e != cudaSuccess) {
+      g->dead = true;
+      HS_FAIL(HS_E_CUDA, "stage %d: %s", k, cudaGetErrorString(e));
+    }
+    err |= s.h_out[m.n];
+    if (k == last || (g->spmd && !got)) {
+      memcpy(out_tokens, s.h_out, (size_t)m.n * 4);
+      got = true;
+    }
+  }
+  if (err) {
+    g->dead = true;
+    HS_FAIL(HS_E_TIMEOUT, "a cross-stage wait timed out (peer never signalled)");
+  }
+  g->last_ids = ids;
+  return HS_OK;
+}
+
+static hs_status alloc_tokens(hs_group* g, int64_t id, int n_new) {
+  SeqState& ss = g->seqs[id];
+  const int need = (ss.ctx + n_new + kBlock - 1) / kBlock;
+  if (ss.ctx + n_new > g->cfg.max_seq) HS_FAIL(HS_E_INVAL, "sequence exceeds max_seq");
+  while ((int)ss.blocks.size() < need) {
+    if (g->free_blocks.empty()) HS_FAIL(HS_E_OOM, "KV blocks exhausted");
+    ss.blocks.push_back(*g->free_blocks.begin());  // lowest free id first
+    g->free_blocks.erase(g->free_blocks.begin());
+  }
+  ss.ctx += n_new;
+  return HS_OK;
+}
+
+static void release(hs_group* g, int64_t id) {
+  auto it = g->seqs.find(id);
+  if (it == g->seqs.end()) return;
+  for (int b : it->second.blocks) g->free_blocks.insert(b);
+  g->seqs.erase(it);
+}
+
+static hs_status prefill(hs_group* g, int n, const int64_t* ids, const int32_t* tokens, const int32_t* lens,
+                         int32_t* out_tokens, float* out_logits) {
+  if (g->dead) HS_FAIL(HS_E_CUDA, "group is dead after a CUDA error");
+  if (n <= 0 || n > g->kv.max_seqs || !ids || !tokens || !lens || !out_tokens) HS_FAIL(HS_E_INVAL, "bad prefill args");
+  if (g->spmd && std::find(g->active.begin(), g->active.end(), g->owned_stage) == g->active.end())
+    HS_FAIL(HS_E_STATE, "this rank's stage was released by consolidation");
+  int T = 0, maxnq = 0;
+  std::set<int64_t> uniq;
+  for (int i = 0; i < n; ++i) {
+    if (lens[i] <= 0) HS_FAIL(HS_E_INVAL, "empty prompt");
+    if (g->seqs.count(ids[i]) || !uniq.insert(ids[i]).second) HS_FAIL(HS_E_INVAL, "sequence id already live");
+    T += lens[i];
+    maxnq = std::max(maxnq, (int)lens[i]);
+  }
+  if (T > g->kv.max_tokens) HS_FAIL(HS_E_INVAL, "prefill of %d tokens exceeds max_tokens %d", T, g->kv.max_tokens);
+  for (int i = 0; i < T; ++i)
+    if (tokens[i] < 0 || tokens[i] >= g->cfg.vocab) HS_FAIL(HS_E_INVAL, "token id out of range");
+  std::vector<int64_t> v(ids, ids + n);
+  for (int i = 0; i < n; ++i) {
+    hs_status r = alloc_tokens(g, ids[i], lens[i]);
+    if (r != HS_OK) {
+      for (int j = 0; j <= i; ++j) release(g, ids[j]);
+      return r;
+    }
+  }
+  CallMeta m;
+  m.T = T; m.n = n; m.max_nq = maxnq; m.decode = false;
+  for (int i = 0; i < n; ++i) {
+    m.kv_tokens += lens[i];
+    m.attn_pairs += 0.5 * (double)lens[i] * (lens[i] + 1);
+  }
+  std::vector<int> ht(tokens, tokens + T);
+  hs_status r = run_call(g, m, v, ht, false, out_tokens, out_logits);
+  if (r != HS_OK && r != HS_E_CUDA && r != HS_E_TIMEOUT)
+    for (int i = 0; i < n; ++i) release(g, ids[i]);
+  return r;
+}
+
+static hs_status decode(hs_group* g, int n, const int64_t* ids, const int32_t* in_tokens, int32_t* out_tokens,
+                        float* out_logits) {
+  if (g->dead) HS_FAIL(HS_E_CUDA, "group is dead after a CUDA error");
+  if (n <= 0 || n > g->kv.max_seqs || !ids || !out_tokens) HS_FAIL(HS_E_INVAL, "bad decode args");
+  if (g->spmd && std::find(g->active.begin(), g->active.end(), g->owned_stage) == g->active.end())
+    HS_FAIL(HS_E_STATE, "this rank's stage was released by consolidation");
+  std::vector<int64_t> v(ids, ids + n);
+  std::set<int64_t> uniq(v.begin(), v.end());
+  if ((int)uniq.size() != n) HS_FAIL(HS_E_INVAL, "duplicate sequence ids");
+  int maxctx = 0;
+  for (int i = 0; i < n; ++i) {
+    auto it = g->seqs.find(ids[i]);
+    if (it == g->seqs.end()) HS_FAIL(HS_E_INVAL, "sequence %lld was never prefilled", (long long)ids[i]);
+    if (it->second.ctx + 1 > g->cfg.max_seq) HS_FAIL(HS_E_INVAL, "sequence exceeds max_seq");
+  }
+  const bool feedback = in_tokens == nullptr;
+  if (feedback && v != g->last_ids) HS_FAIL(HS_E_INVAL, "device token feedback needs the previous call's seq order");
+  std::vector<int> ht;
+  if (!feedback) {
+    ht.assign(in_tokens, in_tokens + n);
+    for (int t : ht) if (t < 0 || t >= g->cfg.vocab) HS_FAIL(HS_E_INVAL, "token id out of range");
+  }
+  for (int i = 0; i < n; ++i) {
+    hs_status r = alloc_tokens(g, ids[i], 1);
+    if (r != HS_OK) return r;
+    maxctx = std::max(maxctx, g->seqs[ids[i]].ctx);
+  }
+  CallMeta m;
+  m.T = n; m.n = n; m.max_nq = 1; m.max_ctx = maxctx; m.decode = true;
+  for (int i = 0; i < n; ++i) {
+    m.kv_tokens += g->seqs[ids[i]].ctx;
+    m.attn_pairs += g->seqs[ids[i]].ctx;
+  }
+  return run_call(g, m, v, ht, feedback, out_tokens, out_logits);
+}
+
+// ------------------------------------------------------------------ consolidation (a17) --
+static hs_status open_peer_memory(hs_group* g, Stage& s) {
+  if (s.owned || s.ipc_arena_open || !g->spmd) return HS_OK;
+  void* p = nullptr;
+  HS_CUDA(cudaIpcOpenMemHandle(&p, s.share.arena, cudaIpcMemLazyEnablePeerAccess));
+  s.arena = reinterpret_cast<uint8_t*>(p);
+  HS_CUDA(cudaIpcOpenMemHandle(&p, s.share.kv, cudaIpcMemLazyEnablePeerAccess));
+  s.kv_mem = reinterpret_cast<uint8_t*>(p);
+  s.ipc_arena_open = true;
+  return HS_OK;
+}
+
+static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
+  const auto t_enter = std::chrono::steady_clock::now();
+  if (g->dead) HS_FAIL(HS_E_CUDA, "group is dead");
+  if (tgt < 0 || tgt >= (int)g->st.size() || std::find(g->active.begin(), g->active.end(), tgt) == g->active.end())
+    HS_FAIL(HS_E_INVAL, "target stage %d is not active", tgt);
+  if (!g->st[tgt].full_memory) HS_FAIL(HS_E_INVAL, "target stage %d is not a full-memory worker", tgt);
+  const hs_model_cfg& c = g->cfg;
+  hs_consolidate_stats stats{};
+  // 1. drain: "stop scheduling ... wait for all on-the-fly batches"
+  for (int k : g->active) {
+    Stage& s = g->st[k];
+    if (!s.owned) continue;
+    DeviceGuard dg(s.device);
+    HS_CUDA(cudaStreamSynchronize(s.comp));
+    HS_CUDA(cudaStreamSynchronize(s.copy));
+  }
+  if (g->spmd && g->comm.barrier(g->comm.ctx) != 0) HS_FAIL(HS_E_STATE, "barrier failed");
+  Stage& T = g->st[tgt];
+  if (T.owned) {
+    DeviceGuard dg(T.device);
+    cudaSetDevice(T.device);
+    // the target must have its own slice resident before it takes over
+    HS_CUDA(cudaStreamSynchronize(T.copy));
+    cudaStream_t s1 = T.copy, s2 = T.comp;
+    cudaEvent_t e0, e1, e2;
+    HS_CUDA(cudaEventCreate(&e0));
+    HS_CUDA(cudaEventCreate(&e1));
+    HS_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+    HS_CUDA(cudaEventRecord(e0, s1));
+    HS_CUDA(cudaStreamWaitEvent(s2, e0, 0));
+    // 2. KV blocks of every live sequence for the layers the target lacks: block-table driven
+    //    gather, pulled over NVLink by the target's SMs ("collect these blocks from all
+    //    workers with a gather operation")
+    std::vector<uint64_t> src, dst;
+    for (int k : g->active) {
+      if (k == tgt) continue;
+      Stage& S = g->st[k];
+      HS_TRY(open_peer_memory(g, S));
+      for (int l = S.lb; l < S.le; ++l)
+        for (auto& kvp : g->seqs)
+          for (int b : kvp.second.blocks) {
+            src.push_back(reinterpret_cast<uint64_t>(S.kv_pool(l, g->kv_layer_bytes)) + (uint64_t)b * g->kv_block_bytes);
+            dst.push_back(reinterpret_cast<uint64_t>(T.kv_pool(l, g->kv_layer_bytes)) + (uint64_t)b * g->kv_block_bytes);
+          }
+    }
+    uint64_t* d_ptrs = nullptr;
+    if (!src.empty()) {
+      HS_CUDA(cudaMalloc(&d_ptrs, src.size() * 16));
+      HS_CUDA(cudaMemcpy(d_ptrs, src.data(), src.size() * 8, cudaMemcpyHostToDevice));
+      HS_CUDA(cudaMemcpy(d_ptrs + src.size(), dst.data(), dst.size() * 8, cudaMemcpyHostToDevice));
+      launch_span_copy(d_ptrs, d_ptrs + src.size(), (int)src.size(), g->kv_block_bytes, s2);
+    }
+    stats.kv_bytes = (uint64_t)src.size() * g->kv_block_bytes;
+    // 3. weight regions the target lacks: copy-engine pull from each owner's arena
+    for (int k : g->active) {
+      if (k == tgt) continue;
+      Stage& S = g->st[k];
+      const uint64_t b = S.slice_begin, e = S.slice_end;
+      const uint64_t chunk = 256ull << 20;
+      for (uint64_t o = b; o < e; o += chunk) {
+        const uint64_t n = std::min(chunk, e - o);
+        HS_CUDA(cudaMemcpyAsync(T.wptr(o), S.arena + (o - S.arena_off0), n, cudaMemcpyDefault, s1));
+      }
+      stats.weight_bytes += g->plan.stage_bytes[k];
+    }
+    HS_CUDA(cudaEventRecord(e2, s2));
+    HS_CUDA(cudaStreamWaitEvent(s1, e2, 0));
+    HS_CUDA(cudaEventRecord(e1, s1));
+    HS_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    HS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    stats.seconds = ms / 1e3;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    if (d_ptrs) cudaFree(d_ptrs);
+    // 4. rebind the target to every layer (maps already exist for a full-memory arena)
+    T.lb = 0;
+    T.le = c.n_layers;
+    for (int l = 0; l < c.n_layers; ++l)
+      if (!T.layers[l].maps) HS_TRY(make_layer_maps(g, T, l));
+    // every layer is resident now: readiness events must not gate on stale loads
+    for (int l = 0; l < c.n_layers; ++l) HS_CUDA(cudaEventRecord(T.ev_layer[l], T.copy));
+    HS_CUDA(cudaEventRecord(T.ev_embed, T.copy));
+    HS_CUDA(cudaEventRecord(T.ev_final, T.copy));
+    T.load_issued = true;
+  }
+  if (g->spmd && g->comm.barrier(g->comm.ctx) != 0) HS_FAIL(HS_E_STATE, "barrier failed");
+  // 5. release the other stages ("other workers are terminated"); a stage
+  //    sharing the target's device hands its streams over first
+  for (int k : g->active)
+    if (k != tgt && g->st[k].owned && g->st[k].owns_streams && g->st[k].device == T.device && T.owned &&
+        !T.owns_streams) {
+      g->st[k].owns_streams = false;
+      T.owns_streams = true;
+    }
+  for (int k : g->active)
+    if (k != tgt) free_stage(g->st[k]);
+  g->active = {tgt};
+  g->st[tgt].lb = 0;
+  g->st[tgt].le = c.n_layers;
+  g->plan.pp = 1;
+  stats.pause_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_enter).count();
+  if (out) *out = stats;
+  return HS_OK;
+}
+
+}  // namespace hs
+
+// ------------------------------------------------------------------ C ABI -----------------
+using namespace hs;
+
+extern "C" hs_status hs_group_create(const hs_model_cfg* cfg, const hs_plan* plan, const hs_image* image,
+                                     const hs_image* stage_images, const hs_kv_cfg* kv, const hs_comm* comm,
+                                     hs_group** out) {
+  return create(cfg, plan, image, stage_images, kv, comm, out);
+}
+
+extern "C" hs_status hs_load_stage_async(hs_group* g, int32_t stage, uint64_t chunk_bytes) {
+  if (!g) HS_FAIL(HS_E_INVAL, "null group");
+  if (g->dead) HS_FAIL(HS_E_CUDA, "group is dead");
+  if (stage == -1) {
+    for (int k : g->active) HS_TRY(load_stage(g, k, chunk_bytes));
+    return HS_OK;
+  }
+  if (std::find(g->active.begin(), g->active.end(), stage) == g->active.end()) HS_FAIL(HS_E_INVAL, "bad stage %d", stage);
+  return load_stage(g, stage, chunk_bytes);
+}
+
+extern "C" hs_status hs_stage_load_stats(hs_group* g, int32_t stage, int32_t wait, hs_load_stats* out) {
+  if (!g || !out || stage < 0 || stage >= (int)g->st.size()) HS_FAIL(HS_E_INVAL, "bad args");
+  Stage& s = g->st[stage];
+  if (!s.owned) HS_FAIL(HS_E_INVAL, "stage %d is not driven by this process", stage);
+  if (!s.load_issued) HS_FAIL(HS_E_STATE, "no load issued");
+  DeviceGuard dg(s.device);
+  hs_load_stats r{};
+  r.bytes = s.loaded_bytes;
+  if (wait) HS_CUDA(cudaEventSynchronize(s.ev_l1));
+  for (int l = s.lb; l < s.le; ++l) r.layers_ready += cudaEventQuery(s.ev_layer[l]) == cudaSuccess;
+  cudaGetLastError();
+  r.done = cudaEventQuery(s.ev_l1) == cudaSuccess;
+  cudaGetLastError();
+  if (r.done) HS_CUDA(cudaEventElapsedTime(&r.load_ms, s.ev_l0, s.ev_l1));
+  *out = r;
+  return HS_OK;
+}
+
+extern "C" hs_status hs_prefill(hs_group* g, int32_t n_seqs, const int64_t* seq_ids, const int32_t* tokens,
+                                const int32_t* seq_lens, int32_t* out_tokens, float* out_logits) {
+  if (!g) HS_FAIL(HS_E_INVAL, "null group");
+  return prefill(g, n_seqs, seq_ids, tokens, seq_lens, out_tokens, out_logits);
+}
+
+extern "C" hs_status hs_decode_step(hs_group* g, int32_t n_seqs, const int64_t* seq_ids, const int32_t* in_tokens,
+                                    int32_t* out_tokens, float* out_logits) {
+  if (!g) HS_FAIL(HS_E_INVAL, "null group");
+  return decode(g, n_seqs, seq_ids, in_tokens, out_tokens, out_logits);
+}
+
+extern "C" hs_status hs_release_seq(hs_group* g, int64_t seq_id) {
+  if (!g) HS_FAIL(HS_E_INVAL, "null group");
+  if (!g->seqs.count(seq_id)) HS_FAIL(HS_E_INVAL, "unknown sequence");
+  release(g, seq_id);
+  return HS_OK;
+}
+
+extern "C" hs_status hs_consolidate(hs_group* g, int32_t target_stage, hs_consolidate_stats* out) {
+  if (!g) HS_FAIL(HS_E_INVAL, "null group");
+  hs_status r = consolidate(g, target_stage, out);
+  if (r == HS_E_CUDA) g->dead = true;
+  return r;
+}
+
+extern "C" hs_status hs_group_destroy(hs_group* g) {
+  if (!g) return HS_OK;
+  for (auto& s : g->st) {
+    if (s.owned) {
+      DeviceGuard dg(s.device);
+      cudaDeviceSynchronize();
+    }
+  }
+  prof_collect(g);
+  for (auto& kv : g->ev_free) {
+    DeviceGuard dg(kv.first);
+    for (auto e : kv.second) cudaEventDestroy(e);
+  }
+  for (auto& s : g->st)
+    if (!s.owned) free_stage(s);
+  for (auto& s : g->st)
+    if (s.owned) free_stage(s);
+  delete g;
+  return HS_OK;
+}
+
+extern "C" hs_status hs_group_info(hs_group* g, int32_t* pp, int32_t* owned) {
+  if (!g) HS_FAIL(HS_E_INVAL, "null group");
+  if (pp) *pp = (int32_t)g->active.size();
+  if (owned) *owned = g->spmd ? g->owned_stage : -1;
+  return HS_OK;
+}
+
+extern "C" hs_status hs_debug_read_kv(hs_group* g, int64_t seq_id, int32_t layer, int32_t pos0, int32_t n_pos,
+                                      void* host_out) {
+  if (!g || !host_out || layer < 0 || layer >= g->cfg.n_layers) HS_FAIL(HS_E_INVAL, "bad args");
+  auto it = g->seqs.find(seq_id);
+  if (it == g->seqs.end() || pos0 < 0 || pos0 + n_pos > it->second.ctx) HS_FAIL(HS_E_INVAL, "bad sequence/positions");
+  int k = -1;
+  HS_TRY(stage_of_layer(g, layer, &k));
+  Stage& s = g->st[k];
+  if (!s.owned) HS_FAIL(HS_E_INVAL, "layer %d lives on a stage of another process", layer);
+  DeviceGuard dg(s.device);
+  HS_CUDA(cudaStreamSynchronize(s.comp));
+  const int nh = g->cfg.n_heads, d = g->cfg.head_dim;
+  std::vector<uint16_t> blk(g->kv_block_bytes / 2);
+  uint16_t* out = reinterpret_cast<uint16_t*>(host_out);
+  int cur = -1;
+  for (int p = pos0; p < pos0 + n_pos; ++p) {
+    const int b = it->second.blocks[p / kBlock];
+    if (b != cur) {
+      HS_CUDA(cudaMemcpy(blk.data(), reinterpret_cast<uint8_t*>(s.kv_pool(layer, g->kv_layer_bytes)) +
+                                          (uint64_t)b * g->kv_block_bytes,
+                         g->kv_block_bytes, cudaMemcpyDeviceToHost));
+      cur = b;
+    }
+    const int off = p % kBlock;
+    for (int kv = 0; kv < 2; ++kv)
+      for (int h = 0; h < nh; ++h)
+        memcpy(out + (((size_t)(p - pos0) * 2 + kv) * nh + h) * d, blk.data() + (((size_t)kv * nh + h) * kBlock + off) * d,
+               (size_t)d * 2);
+  }
+  return HS_OK;
+}
+
+extern "C" hs_status hs_debug_read_weights(hs_group* g, int32_t stage, uint64_t off, uint64_t bytes, void* host_out) {
+  if (!g || stage < 0 || stage >= (int)g->st.size()) HS_FAIL(HS_E_INVAL, "bad args");
+  Stage& s = g->st[stage];
+  if (!s.owned || !s.arena) HS_FAIL(HS_E_INVAL, "stage not resident in this process");
+  if (off < s.arena_off0 || off + bytes > s.arena_off0 + s.arena_bytes) HS_FAIL(HS_E_INVAL, "range outside arena");
+  DeviceGuard dg(s.device);
+  HS_CUDA(cudaDeviceSynchronize());
+  HS_CUDA(cudaMemcpy(host_out, s.wptr(off), bytes, cudaMemcpyDeviceToHost));
+  return HS_OK;
+}
+
+extern "C" hs_status hs_debug_poison_weights(hs_group* g, int32_t stage) {
+  if (!g || stage < 0 || stage >= (int)g->st.size()) HS_FAIL(HS_E_INVAL, "bad args");
+  Stage& s = g->st[stage];
+  if (!s.owned || !s.arena) HS_FAIL(HS_E_INVAL, "stage not resident in this process");
+  DeviceGuard dg(s.device);
+  HS_CUDA(cudaDeviceSynchronize());
+  HS_CUDA(cudaMemset(s.arena, 0xFF, s.arena_bytes));
+  HS_CUDA(cudaDeviceSynchronize());
+  return HS_OK;
+}
+
+extern "C" hs_status hs_debug_launch_count(hs_group* g, uint64_t* out) {
+  (void)g;
+  if (!out) HS_FAIL(HS_E_INVAL, "null out");
+  *out = launch_total();
+  return HS_OK;
+}
+
+extern "C" hs_status hs_stage_timing_get(hs_group* g, int32_t stage, hs_stage_timing* out) {
+  if (!g || !out || stage < 0 || stage >= (int)g->st.size()) HS_FAIL(HS_E_INVAL, "bad args");
+  Stage& s = g->st[stage];
+  if (!s.owned || !s.comp) HS_FAIL(HS_E_INVAL, "stage %d is not driven by this process", stage);
+  DeviceGuard dg(s.device);
+  hs_stage_timing t{};
+  if (s.load_issued && s.ev_l1) {
+    HS_CUDA(cudaEventSynchronize(s.ev_l1));
+    HS_CUDA(cudaEventElapsedTime(&t.load_ms, s.ev_l0, s.ev_l1));
+  }
+  if (s.called) {
+    HS_CUDA(cudaEventSynchronize(s.ev_c1));
+    HS_CUDA(cudaEventElapsedTime(&t.call_ms, s.ev_c0, s.ev_c1));
+    if (s.load_issued) {
+      cudaError_t e = cudaEventElapsedTime(&t.since_load_ms, s.ev_l0, s.ev_c1);
+      if (e != cudaSuccess) { cudaGetLastError(); t.since_load_ms = -1; }
+    }
+  }
+  *out = t;
+  return HS_OK;
+}
+
+extern "C" hs_status hs_profile_enable(hs_group* g, int32_t on) {
+  if (!g) HS_FAIL(HS_E_INVAL, "null group");
+  g->prof_on = on != 0;
+  return HS_OK;
+}
+
+extern "C" hs_status hs_profile_read(hs_group* g, hs_prof_entry* out, int32_t max_entries, int32_t* n, int32_t reset) {
+  if (!g || !n) HS_FAIL(HS_E_INVAL, "bad args");
+  HS_TRY(prof_collect(g));
+  int i = 0;
+  for (auto& kv : g->prof_acc) {
+    if (out && i < max_entries) {
+      hs_prof_entry& e = out[i];
+      memset(&e, 0, sizeof(e));
+      snprintf(e.name, sizeof(e.name), "%s.%s", kProfNames[kv.first / 2], (kv.first & 1) ? "decode" : "prefill");
+      e.count = kv.second.count;
+      e.ms = kv.second.ms;
+      e.bytes = kv.second.bytes;
+      e.flops = kv.second.flops;
+    }
+    ++i;
+  }
+  *n = i;
+  if (reset) g->prof_acc.clear();
+  return HS_OK;
+}
+
+extern "C" hs_status hs_debug_comm_selftest(const hs_comm* comm) {
+  if (!comm || !comm->allgather || !comm->barrier || comm->world <= 0 || comm->rank < 0 || comm->rank >= comm->world)
+    HS_FAIL(HS_E_INVAL, "bad comm");
+  struct Msg { int32_t rank, world; uint64_t tag; char pad[48]; } me{};
+  me.rank = comm->rank;
+  me.world = comm->world;
+  me.tag = 0x48535350ull * (uint64_t)(comm->rank + 1);
+  std::vector<Msg> all(comm->world);
+  if (comm->allgather(comm->ctx, &me, sizeof(Msg), all.data()) != 0) HS_FAIL(HS_E_STATE, "allgather failed");
+  for (int r = 0; r < comm->world; ++r)
+    if (all[r].rank != r || all[r].world != comm->world || all[r].tag != 0x48535350ull * (uint64_t)(r + 1))
+      HS_FAIL(HS_E_STATE, "allgather returned wrong bytes for rank %d", r);
+  if (comm->barrier(comm->ctx) != 0) HS_FAIL(HS_E_STATE, "barrier failed");
+  return HS_OK;
+}

@@ -1,0 +1,520 @@
+// kernels.cu — non-GEMM kernels of a pipeline stage (sm_100a), with warp-shuffle reductions
+// and 128-bit global accesses.  See kernels.h for the contracts; DESIGN.md lists the
+// roofline each is bounded by.
+#include "kernels.h"
+
+#include <cfloat>
+
+namespace hs {
+
+// ------------------------------------------------------------------ embedding (a5) -------
+__global__ void embed_kernel(const int* __restrict__ tok, const uint4* __restrict__ E,
+                             uint4* __restrict__ x, int H8) {
+  const int t = blockIdx.x;
+  const uint4* src = E + (size_t)tok[t] * H8;
+  uint4* dst = x + (size_t)t * H8;
+  for (int i = threadIdx.x; i < H8; i += blockDim.x) dst[i] = __ldg(src + i);
+}
+
+void launch_embed(const int* tok, const bf16* E, bf16* x, int T, int H, cudaStream_t st) {
+  count_launch();
+  const int H8 = H / 8;
+  embed_kernel<<<T, H8 < 512 ? H8 : 512, 0, st>>>(tok, reinterpret_cast<const uint4*>(E),
+                                                   reinterpret_cast<uint4*>(x), H8);
+}
+
+// ------------------------------------------------------------------ RMSNorm (a6) ---------
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int MAXV>
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const uint4* __restrict__ x, const int* __restrict__ rows,
+                                                      const uint4* __restrict__ w, uint4* __restrict__ y,
+                                                      int H8, float inv_h, float eps) {
+  __shared__ float red[8];
+  const int i = blockIdx.x;
+  const int r = rows ? rows[i] : i;
+  const uint4* xr = x + (size_t)r * H8;
+  uint4 v[MAXV];
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < MAXV; ++j) {
+    const int c = threadIdx.x + j * 256;
+    if (c < H8) {
+      v[j] = xr[c];
+      const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v[j]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float2 f = __bfloat1622float2(p[k]);
+        ss += f.x * f.x + f.y * f.y;
+      }
+    }
+  }
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) tot += red[k];
+  const float rs = 1.0f / sqrtf(tot * inv_h + eps);
+#pragma unroll
+  for (int j = 0; j < MAXV; ++j) {
+    const int c = threadIdx.x + j * 256;
+    if (c < H8) {
+      uint4 wv = w[c], out;
+      const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v[j]);
+      const __nv_bfloat162* q = reinterpret_cast<const __nv_bfloat162*>(&wv);
+      __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(&out);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float2 a = __bfloat1622float2(p[k]), b = __bfloat1622float2(q[k]);
+        o[k] = __floats2bfloat162_rn(a.x * rs * b.x, a.y * rs * b.y);
+      }
+      y[(size_t)i * H8 + c] = out;
+    }
+  }
+}
+
+void launch_rmsnorm(const bf16* x, const int* rows, const bf16* w, bf16* y, int T, int H,
+                    float eps, cudaStream_t st) {
+  count_launch();
+  const int H8 = H / 8;
+  auto X = reinterpret_cast<const uint4*>(x);
+  auto W = reinterpret_cast<const uint4*>(w);
+  auto Y = reinterpret_cast<uint4*>(y);
+  if (H8 <= 256) rmsnorm_kernel<1><<<T, 256, 0, st>>>(X, rows, W, Y, H8, 1.0f / H, eps);
+  else if (H8 <= 512) rmsnorm_kernel<2><<<T, 256, 0, st>>>(X, rows, W, Y, H8, 1.0f / H, eps);
+  else if (H8 <= 1024) rmsnorm_kernel<4><<<T, 256, 0, st>>>(X, rows, W, Y, H8, 1.0f / H, eps);
+  else rmsnorm_kernel<8><<<T, 256, 0, st>>>(X, rows, W, Y, H8, 1.0f / H, eps);
+}
+
+// ------------------------------------------------------------------ RoPE + KV write (a8) -
+__global__ void rope_kv_kernel(const bf16* __restrict__ qkv, const int* __restrict__ pos,
+                               const int* __restrict__ slot, const float2* __restrict__ tab,
+                               bf16* __restrict__ q_out, bf16* __restrict__ pool, int nh, int d) {
+  const int t = blockIdx.x;
+  const int H = nh * d, hd = d / 2;
+  const bf16* row = qkv + (size_t)t * 3 * H;
+  const int p = pos[t], s = slot[t];
+  const size_t blk = (size_t)(s >> 4), off = (size_t)(s & 15);
+  const float2* cs = tab + (size_t)p * hd;
+  for (int idx = threadIdx.x; idx < nh * hd; idx += blockDim.x) {
+    const int h = idx / hd, i = idx % hd;
+    const float2 c = cs[i];  // (cos, sin)
+    const float q1 = __bfloat162float(row[h * d + i]), q2 = __bfloat162float(row[h * d + i + hd]);
+    const float k1 = __bfloat162float(row[H + h * d + i]), k2 = __bfloat162float(row[H + h * d + i + hd]);
+    bf16* qo = q_out + (size_t)t * H + h * d;
+    qo[i] = __float2bfloat16_rn(q1 * c.x - q2 * c.y);
+    qo[i + hd] = __float2bfloat16_rn(q2 * c.x + q1 * c.y);
+    bf16* kd = pool + (((blk * 2 + 0) * nh + h) * 16 + off) * d;
+    kd[i] = __float2bfloat16_rn(k1 * c.x - k2 * c.y);
+    kd[i + hd] = __float2bfloat16_rn(k2 * c.x + k1 * c.y);
+  }
+  const int d8 = d / 8;
+  const uint4* v = reinterpret_cast<const uint4*>(row + 2 * H);
+  for (int idx = threadIdx.x; idx < nh * d8; idx += blockDim.x) {
+    const int h = idx / d8, j = idx % d8;
+    uint4* vd = reinterpret_cast<uint4*>(pool + (((blk * 2 + 1) * nh + h) * 16 + off) * d);
+    vd[j] = v[h * d8 + j];
+  }
+}
+
+void launch_rope_kv(const bf16* qkv, const int* pos, const int* slot, const float2* tab, bf16* q_out,
+                    bf16* pool, int T, int nh, int d, cudaStream_t st) {
+  count_launch();
+  rope_kv_kernel<<<T, 256, 0, st>>>(qkv, pos, slot, tab, q_out, pool, nh, d);
+}
+
+// ------------------------------------------------------------------ attention (a9) -------
+// Scores are computed in the log2 domain: s2 = (q . k) * log2(e) / sqrt(d); softmax with
+// exp2 is identical to the natural-base definition.
+template <int D>
+struct Lanes {
+  static constexpr int E = D / 32;  // elements per lane
+};
+
+template <int D>
+__device__ __forceinline__ void load_lane(const bf16* p, float* out) {
+  constexpr int E = D / 32;
+  if constexpr (E == 4) {
+    uint2 u = *reinterpret_cast<const uint2*>(p);
+    float2 a = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.x));
+    float2 b = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.y));
+    out[0] = a.x; out[1] = a.y; out[2] = b.x; out[3] = b.y;
+  } else {
+    float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p));
+    out[0] = a.x; out[1] = a.y;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void store_lane(bf16* p, const float* v) {
+  constexpr int E = D / 32;
+  if constexpr (E == 4) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(p) = u;
+  } else {
+    *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(v[0], v[1]);
+  }
+}
+
+constexpr int PF_Q = 16;    // queries per CTA (4 warps x 4)
+constexpr int PF_KC = 64;   // keys staged per chunk
+
+template <int D>
+__global__ void __launch_bounds__(128) attn_prefill_kernel(
+    const bf16* __restrict__ q, const bf16* __restrict__ pool, const SeqDesc* __restrict__ seqs,
+    const int* __restrict__ tables, int max_blocks, bf16* __restrict__ o, int nh) {
+  constexpr int E = D / 32;
+  __shared__ __align__(16) bf16 Ks[PF_KC][D];
+  __shared__ __align__(16) bf16 Vs[PF_KC][D];
+  const SeqDesc s = seqs[blockIdx.z];
+  const int head = blockIdx.y;
+  const int qt0 = blockIdx.x * PF_Q;
+  if (qt0 >= s.n_q) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int H = nh * D;
+  const float scale = 1.4426950408889634f / sqrtf((float)D);
+  float qv[4][E], acc[4][E], m[4], l[4];
+  int qpos[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int qi = qt0 + warp * 4 + j;
+    qpos[j] = qi < s.n_q ? s.pos0 + qi : -1;
+    if (qi < s.n_q) load_lane<D>(q + (size_t)(s.q_start + qi) * H + head * D + lane * E, qv[j]);
+    else
+#pragma unroll
+      for (int e = 0; e < E; ++e) qv[j][e] = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) { qv[j][e] *= scale; acc[j][e] = 0.f; }
+    m[j] = -INFINITY;
+    l[j] = 0.f;
+  }
+  const int n_keys = s.pos0 + min(qt0 + PF_Q, s.n_q);
+  const int* tab = tables + (size_t)s.table * max_blocks;
+  constexpr int RU4 = D / 8;  // uint4 per row
+  for (int kc = 0; kc < n_keys; kc += PF_KC) {
+    __syncthreads();
+    const int nk = min(PF_KC, n_keys - kc);
+    for (int idx = threadIdx.x; idx < nk * RU4; idx += 128) {
+      const int jj = idx / RU4, u = idx % RU4;
+      const int j = kc + jj;
+      const size_t blk = (size_t)tab[j >> 4];
+      const size_t base = (((blk * 2) * nh + head) * 16 + (j & 15)) * D;
+      reinterpret_cast<uint4*>(&Ks[jj][0])[u] = reinterpret_cast<const uint4*>(pool + base)[u];
+      reinterpret_cast<uint4*>(&Vs[jj][0])[u] =
+          reinterpret_cast<const uint4*>(pool + base + (size_t)nh * 16 * D)[u];
+    }
+    __syncthreads();
+    for (int jj = 0; jj < nk; ++jj) {
+      const int j = kc + jj;
+      float kf[E], vf[E];
+      load_lane<D>(&Ks[jj][lane * E], kf);
+      load_lane<D>(&Vs[jj][lane * E], vf);
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) {
+        if (j > qpos[qq]) continue;  // causal mask (warp-uniform)
+        float part = 0.f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) part += qv[qq][e] * kf[e];
+        const float sc = warp_sum(part);
+        const float mn = fmaxf(m[qq], sc);
+        const float corr = exp2f(m[qq] - mn), pr = exp2f(sc - mn);
+        l[qq] = l[qq] * corr + pr;
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[qq][e] = acc[qq][e] * corr + pr * vf[e];
+        m[qq] = mn;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int qi = qt0 + warp * 4 + j;
+    if (qi < s.n_q) {
+      float r[E];
+      const float inv = 1.0f / l[j];
+#pragma unroll
+      for (int e = 0; e < E; ++e) r[e] = acc[j][e] * inv;
+      store_lane<D>(o + (size_t)(s.q_start + qi) * H + head * D + lane * E, r);
+    }
+  }
+}
+
+void launch_attn_prefill(const bf16* q, const bf16* pool, const SeqDesc* seqs, int n_seqs, int max_nq,
+                         const int* tables, int max_blocks, bf16* o, int nh, int d, cudaStream_t st) {
+  count_launch();
+  dim3 grid((max_nq + PF_Q - 1) / PF_Q, nh, n_seqs);
+  if (d == 128) attn_prefill_kernel<128><<<grid, 128, 0, st>>>(q, pool, seqs, tables, max_blocks, o, nh);
+  else attn_prefill_kernel<64><<<grid, 128, 0, st>>>(q, pool, seqs, tables, max_blocks, o, nh);
+}
+
+// Decode: CTA = (head, seq, split); warp w takes keys start + w, start + w + 4, ...
+template <int D>
+__global__ void __launch_bounds__(128) attn_decode_kernel(
+    const bf16* __restrict__ q, const bf16* __restrict__ pool, const SeqDesc* __restrict__ seqs,
+    const int* __restrict__ tables, int max_blocks, bf16* __restrict__ o, int nh, float* __restrict__ ws,
+    int splits, int chunk) {
+  constexpr int E = D / 32;
+  __shared__ float sm_m[4], sm_l[4];
+  __shared__ float sm_acc[4][D];
+  const int head = blockIdx.x, si = blockIdx.y, sp = blockIdx.z;
+  const SeqDesc s = seqs[si];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int H = nh * D;
+  const int n_keys = s.pos0 + 1;
+  const int k0 = sp * chunk, k1 = min(n_keys, k0 + chunk);
+  const float scale = 1.4426950408889634f / sqrtf((float)D);
+  float qv[E], acc[E], m = -INFINITY, l = 0.f;
+  load_lane<D>(q + (size_t)s.q_start * H + head * D + lane * E, qv);
+#pragma unroll
+  for (int e = 0; e < E; ++e) { qv[e] *= scale; acc[e] = 0.f; }
+  const int* tab = tables + (size_t)s.table * max_blocks;
+  const size_t vstride = (size_t)nh * 16 * D;
+  int j = k0 + warp;
+  // two keys per iteration to keep two K/V row loads in flight per warp
+  for (; j + 4 < k1; j += 8) {
+    const size_t b0 = ((((size_t)tab[j >> 4] * 2) * nh + head) * 16 + (j & 15)) * D + lane * E;
+    const int j2 = j + 4;
+    const size_t b1 = ((((size_t)tab[j2 >> 4] * 2) * nh + head) * 16 + (j2 & 15)) * D + lane * E;
+    float ka[E], va[E], kb[E], vb[E];
+    load_lane<D>(pool + b0, ka);
+    load_lane<D>(pool + b0 + vstride, va);
+    load_lane<D>(pool + b1, kb);
+    load_lane<D>(pool + b1 + vstride, vb);
+    float pa = 0.f, pb = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) { pa += qv[e] * ka[e]; pb += qv[e] * kb[e]; }
+    pa = warp_sum(pa);
+    pb = warp_sum(pb);
+    const float mn = fmaxf(m, fmaxf(pa, pb));
+    const float corr = exp2f(m - mn), ea = exp2f(pa - mn), eb = exp2f(pb - mn);
+    l = l * corr + ea + eb;
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = acc[e] * corr + ea * va[e] + eb * vb[e];
+    m = mn;
+  }
+  for (; j < k1; j += 4) {
+    const size_t b0 = ((((size_t)tab[j >> 4] * 2) * nh + head) * 16 + (j & 15)) * D + lane * E;
+    float ka[E], va[E];
+    load_lane<D>(pool + b0, ka);
+    load_lane<D>(pool + b0 + vstride, va);
+    float pa = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) pa += qv[e] * ka[e];
+    pa = warp_sum(pa);
+    const float mn = fmaxf(m, pa);
+    const float corr = exp2f(m - mn), ea = exp2f(pa - mn);
+    l = l * corr + ea;
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = acc[e] * corr + ea * va[e];
+    m = mn;
+  }
+  // combine the 4 warps (fixed order)
+  if (lane == 0) { sm_m[warp] = m; sm_l[warp] = l; }
+#pragma unroll
+  for (int e = 0; e < E; ++e) sm_acc[warp][lane * E + e] = acc[e];
+  __syncthreads();
+  if (warp == 0) {
+    float M = fmaxf(fmaxf(sm_m[0], sm_m[1]), fmaxf(sm_m[2], sm_m[3]));
+    float L = 0.f, A[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) A[e] = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float f = sm_m[w] == -INFINITY ? 0.f : exp2f(sm_m[w] - M);
+      L += sm_l[w] * f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) A[e] += sm_acc[w][lane * E + e] * f;
+    }
+    if (splits == 1) {
+      float r[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) r[e] = A[e] / L;
+      store_lane<D>(o + (size_t)s.q_start * H + head * D + lane * E, r);
+    } else {
+      float* w = ws + (((size_t)si * nh + head) * splits + sp) * (D + 2);
+      if (lane == 0) { w[0] = M; w[1] = L; }
+#pragma unroll
+      for (int e = 0; e < E; ++e) w[2 + lane * E + e] = A[e];
+    }
+  }
+}
+
+template <int D>
+__global__ void attn_decode_combine(const float* __restrict__ ws, const SeqDesc* __restrict__ seqs,
+                                    bf16* __restrict__ o, int nh, int splits) {
+  const int head = blockIdx.x, si = blockIdx.y;
+  const int e = threadIdx.x;  // D threads
+  const float* w = ws + ((size_t)si * nh + head) * splits * (D + 2);
+  float M = -INFINITY;
+  for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, w[sp * (D + 2)]);
+  float L = 0.f, A = 0.f;
+  for (int sp = 0; sp < splits; ++sp) {
+    const float ms = w[sp * (D + 2)];
+    const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
+    L += w[sp * (D + 2) + 1] * f;
+    A += w[sp * (D + 2) + 2 + e] * f;
+  }
+  o[(size_t)seqs[si].q_start * nh * D + head * D + e] = __float2bfloat16_rn(A / L);
+}
+
+int attn_decode_splits(int max_ctx) {
+  int s = (max_ctx + 127) / 128;
+  return s < 1 ? 1 : (s > 16 ? 16 : s);
+}
+
+void launch_attn_decode(const bf16* q, const bf16* pool, const SeqDesc* seqs, int n_seqs, int max_ctx,
+                        const int* tables, int max_blocks, bf16* o, int nh, int d, float* ws, int splits,
+                        cudaStream_t st) {
+  count_launch(splits > 1 ? 2 : 1);
+  const int chunk = (max_ctx + splits - 1) / splits;
+  dim3 grid(nh, n_seqs, splits);
+  if (d == 128) {
+    attn_decode_kernel<128><<<grid, 128, 0, st>>>(q, pool, seqs, tables, max_blocks, o, nh, ws, splits, chunk);
+    if (splits > 1) attn_decode_combine<128><<<dim3(nh, n_seqs), 128, 0, st>>>(ws, seqs, o, nh, splits);
+  } else {
+    attn_decode_kernel<64><<<grid, 128, 0, st>>>(q, pool, seqs, tables, max_blocks, o, nh, ws, splits, chunk);
+    if (splits > 1) attn_decode_combine<64><<<dim3(nh, n_seqs), 64, 0, st>>>(ws, seqs, o, nh, splits);
+  }
+}
+
+// ------------------------------------------------------------------ argmax (a15) ---------
+__global__ void __launch_bounds__(1024) argmax_kernel(const float* __restrict__ logits, int V,
+                                                      int* __restrict__ out) {
+  __shared__ float bv[32];
+  __shared__ int bi[32];
+  const float* row = logits + (size_t)blockIdx.x * V;
+  float best = -INFINITY;
+  int idx = 0x7fffffff;
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    const float x = row[v];
+    if (x > best) { best = x; idx = v; }  // strided ascending scan keeps the lowest id on ties
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ob > best || (ob == best && oi < idx)) { best = ob; idx = oi; }
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { bv[w] = best; bi[w] = idx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+      if (bv[k] > best || (bv[k] == best && bi[k] < idx)) { best = bv[k]; idx = bi[k]; }
+    bv[0] = best;
+    bi[0] = idx;
+    out[blockIdx.x] = idx == 0x7fffffff ? 0 : idx;
+  }
+}
+
+void launch_argmax(const float* logits, int V, int n, int* tokens, cudaStream_t st) {
+  count_launch();
+  argmax_kernel<<<n, 1024, 0, st>>>(logits, V, tokens);
+}
+
+// ------------------------------------------------------------------ hand-off (a13) -------
+__global__ void __launch_bounds__(256) send_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                   uint64_t n16, unsigned* done_ctr, unsigned* flag,
+                                                   unsigned epoch) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    uint4 a = src[i], b = src[i + stride], c = src[i + 2 * stride], d = src[i + 3 * stride];
+    dst[i] = a; dst[i + stride] = b; dst[i + 2 * stride] = c; dst[i + 3 * stride] = d;
+  }
+  for (; i < n16; i += stride) dst[i] = src[i];
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(done_ctr, 1u);
+    if (prev == gridDim.x - 1) {
+      *done_ctr = 0;
+      __threadfence_system();
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
+    }
+  }
+}
+
+void launch_send(const void* src, void* dst, uint64_t bytes, unsigned* done_ctr, unsigned* flag,
+                 unsigned epoch, int ctas, cudaStream_t st) {
+  count_launch();
+  send_kernel<<<ctas, 256, 0, st>>>(reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst),
+                                    bytes / 16, done_ctr, flag, epoch);
+}
+
+__global__ void wait_kernel(const unsigned* flag, unsigned epoch, int* err) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if ((int)(v - epoch) >= 0) return;
+    __nanosleep(200);
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 20000000000ull) {  // 20 s: the peer never signalled
+      *err = 1;
+      return;
+    }
+  }
+}
+
+void launch_wait(const unsigned* flag, unsigned epoch, int* err, cudaStream_t st) {
+  count_launch();
+  wait_kernel<<<1, 1, 0, st>>>(flag, epoch, err);
+}
+
+// ------------------------------------------------------------------ span copy (a17) ------
+__global__ void __launch_bounds__(256) span_copy_kernel(const uint64_t* __restrict__ src,
+                                                        const uint64_t* __restrict__ dst, uint64_t n16,
+                                                        int parts) {
+  const int span = blockIdx.x / parts, part = blockIdx.x % parts;
+  const uint4* s = reinterpret_cast<const uint4*>(src[span]);
+  uint4* d = reinterpret_cast<uint4*>(dst[span]);
+  const uint64_t per = (n16 + parts - 1) / parts;
+  const uint64_t b = per * part, e = min(n16, b + per);
+  uint64_t i = b + threadIdx.x;
+  for (; i + 768 < e; i += 1024) {
+    uint4 x0 = s[i], x1 = s[i + 256], x2 = s[i + 512], x3 = s[i + 768];
+    d[i] = x0; d[i + 256] = x1; d[i + 512] = x2; d[i + 768] = x3;
+  }
+  for (; i < e; i += 256) d[i] = s[i];
+}
+
+void launch_span_copy(const uint64_t* src, const uint64_t* dst, int n, uint64_t span_bytes, cudaStream_t st) {
+  if (n <= 0) return;
+  count_launch();
+  const uint64_t n16 = span_bytes / 16;
+  int parts = (int)((span_bytes + 65535) / 65536);
+  if (parts < 1) parts = 1;
+  span_copy_kernel<<<n * parts, 256, 0, st>>>(src, dst, n16, parts);
+}
+
+void warm_kernels() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, embed_kernel);
+  cudaFuncGetAttributes(&a, rmsnorm_kernel<1>);
+  cudaFuncGetAttributes(&a, rmsnorm_kernel<2>);
+  cudaFuncGetAttributes(&a, rmsnorm_kernel<4>);
+  cudaFuncGetAttributes(&a, rmsnorm_kernel<8>);
+  cudaFuncGetAttributes(&a, rope_kv_kernel);
+  cudaFuncGetAttributes(&a, attn_prefill_kernel<64>);
+  cudaFuncGetAttributes(&a, attn_prefill_kernel<128>);
+  cudaFuncGetAttributes(&a, attn_decode_kernel<64>);
+  cudaFuncGetAttributes(&a, attn_decode_kernel<128>);
+  cudaFuncGetAttributes(&a, attn_decode_combine<64>);
+  cudaFuncGetAttributes(&a, attn_decode_combine<128>);
+  cudaFuncGetAttributes(&a, argmax_kernel);
+  cudaFuncGetAttributes(&a, send_kernel);
+  cudaFuncGetAttributes(&a, wait_kernel);
+  cudaFuncGetAttributes(&a, span_copy_kernel);
+}
+
+}  // namespace hs

@@ -1,0 +1,411 @@
+"""ctypes binding of libhs.so (include/hs.h, include/hs_kernels.h) — argument marshalling only.
+
+Every step of the path runs in the library's CUDA kernels / copy engines; this module only
+converts Python values to C structs and pointers.  There is no fallback: if libhs.so is not
+built, importing raises (build it with ``python -m paper_2502_15524_b200.build``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(HERE, "libhs.so")
+
+HS_MAX_STAGES = 8
+HS_MAX_LAYERS = 128
+STATUS = {0: "HS_OK", 1: "HS_E_INVAL", 2: "HS_E_CUDA", 3: "HS_E_OOM", 4: "HS_E_INFEASIBLE",
+          5: "HS_E_STATE", 6: "HS_E_PEER", 7: "HS_E_TIMEOUT"}
+
+
+class HsError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class ModelCfg(C.Structure):
+    _fields_ = [("n_layers", C.c_int32), ("hidden", C.c_int32), ("n_heads", C.c_int32),
+                ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32), ("ffn", C.c_int32),
+                ("vocab", C.c_int32), ("max_seq", C.c_int32), ("rms_eps", C.c_float),
+                ("rope_theta", C.c_float)]
+
+
+class ImageHeader(C.Structure):
+    _fields_ = [("magic", C.c_uint64), ("version", C.c_uint32), ("gu_interleave", C.c_uint32),
+                ("cfg", ModelCfg), ("total_bytes", C.c_uint64), ("embed_off", C.c_uint64),
+                ("embed_bytes", C.c_uint64), ("layer_off", C.c_uint64 * HS_MAX_LAYERS),
+                ("layer_bytes", C.c_uint64), ("t_attn_norm", C.c_uint64), ("t_wqkv", C.c_uint64),
+                ("t_wo", C.c_uint64), ("t_ffn_norm", C.c_uint64), ("t_wgu", C.c_uint64),
+                ("t_wd", C.c_uint64), ("final_off", C.c_uint64), ("final_bytes", C.c_uint64),
+                ("t_final_norm", C.c_uint64), ("t_lm_head", C.c_uint64), ("param_bytes", C.c_uint64)]
+
+
+class Image(C.Structure):
+    _fields_ = [("header", C.POINTER(ImageHeader)), ("data", C.c_void_p),
+                ("data_offset", C.c_uint64), ("data_bytes", C.c_uint64)]
+
+
+class Gpu(C.Structure):
+    _fields_ = [("device", C.c_int32), ("h2d_gbps", C.c_double), ("link_group", C.c_int32),
+                ("free_bytes", C.c_uint64)]
+
+
+class Plan(C.Structure):
+    _fields_ = [("pp", C.c_int32), ("device", C.c_int32 * HS_MAX_STAGES),
+                ("layer_begin", C.c_int32 * HS_MAX_STAGES), ("layer_end", C.c_int32 * HS_MAX_STAGES),
+                ("stage_bytes", C.c_uint64 * HS_MAX_STAGES), ("slice_begin", C.c_uint64 * HS_MAX_STAGES),
+                ("slice_end", C.c_uint64 * HS_MAX_STAGES), ("full_memory", C.c_int32 * HS_MAX_STAGES),
+                ("pred_ttft_s", C.c_double)]
+
+    def as_dict(self):
+        n = self.pp
+        return dict(pp=n, device=list(self.device[:n]),
+                    ranges=[(self.layer_begin[k], self.layer_end[k]) for k in range(n)],
+                    stage_bytes=list(self.stage_bytes[:n]),
+                    slices=[(self.slice_begin[k], self.slice_end[k]) for k in range(n)],
+                    full_memory=list(self.full_memory[:n]), pred_ttft_s=self.pred_ttft_s)
+
+
+class KvCfg(C.Structure):
+    _fields_ = [("block_tokens", C.c_int32), ("num_blocks", C.c_int32), ("max_seqs", C.c_int32),
+                ("max_tokens", C.c_int32)]
+
+
+ALLGATHER = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p)
+BARRIER = C.CFUNCTYPE(C.c_int32, C.c_void_p)
+
+
+class Comm(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("ctx", C.c_void_p),
+                ("allgather", ALLGATHER), ("barrier", BARRIER)]
+
+
+class LoadStats(C.Structure):
+    _fields_ = [("bytes", C.c_uint64), ("load_ms", C.c_float), ("layers_ready", C.c_int32),
+                ("done", C.c_int32)]
+
+
+class StageTiming(C.Structure):
+    _fields_ = [("load_ms", C.c_float), ("call_ms", C.c_float), ("since_load_ms", C.c_float)]
+
+
+class ProfEntry(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("count", C.c_uint64), ("ms", C.c_double), ("bytes", C.c_double),
+                ("flops", C.c_double)]
+
+
+class ConsolidateStats(C.Structure):
+    _fields_ = [("weight_bytes", C.c_uint64), ("kv_bytes", C.c_uint64), ("seconds", C.c_double),
+                ("pause_seconds", C.c_double)]
+
+
+# exported symbols (include/hs.h + include/hs_kernels.h); tests check every one is present
+SYMBOLS = ["hs_image_layout", "hs_plan_stages", "hs_predict_ttft_eq1", "hs_predict_tpot_eq2",
+           "hs_predict_ttft_eq5", "hs_group_create", "hs_load_stage_async", "hs_stage_load_stats",
+           "hs_prefill", "hs_decode_step", "hs_release_seq", "hs_consolidate", "hs_group_destroy",
+           "hs_last_error", "hs_group_info", "hs_debug_read_kv", "hs_debug_read_weights",
+           "hs_debug_poison_weights", "hs_debug_launch_count", "hs_stage_timing_get", "hs_profile_enable",
+           "hs_profile_read", "hs_debug_comm_selftest",
+           "hs_k_gemm", "hs_k_rmsnorm", "hs_k_rope_kv", "hs_k_attention", "hs_k_argmax", "hs_k_embed",
+           "hs_k_span_copy"]
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(SO):
+        raise ImportError(f"{SO} is missing: build the CUDA library first "
+                          "(python -m paper_2502_15524_b200.build); there is no fallback path")
+    L = C.CDLL(SO)
+    P, I32, U64, VP = C.POINTER, C.c_int32, C.c_uint64, C.c_void_p
+    L.hs_last_error.restype = C.c_char_p
+    L.hs_image_layout.argtypes = [P(ModelCfg), P(ImageHeader)]
+    L.hs_plan_stages.argtypes = [P(ModelCfg), P(Gpu), I32, I32, I32, C.c_double, C.c_double, P(Plan)]
+    for f in ("hs_predict_ttft_eq1",):
+        getattr(L, f).restype = C.c_double
+        getattr(L, f).argtypes = [C.c_double, C.c_double, I32, I32, P(C.c_double), P(C.c_double),
+                                  C.c_double, C.c_double]
+    L.hs_predict_tpot_eq2.restype = C.c_double
+    L.hs_predict_tpot_eq2.argtypes = [C.c_double, I32, I32, C.c_double]
+    L.hs_predict_ttft_eq5.restype = C.c_double
+    L.hs_predict_ttft_eq5.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, I32, I32,
+                                      P(C.c_double), P(C.c_double), C.c_double, C.c_double]
+    L.hs_group_create.argtypes = [P(ModelCfg), P(Plan), P(Image), P(Image), P(KvCfg), P(Comm), P(VP)]
+    L.hs_load_stage_async.argtypes = [VP, I32, U64]
+    L.hs_stage_load_stats.argtypes = [VP, I32, I32, P(LoadStats)]
+    L.hs_prefill.argtypes = [VP, I32, VP, VP, VP, VP, VP]
+    L.hs_decode_step.argtypes = [VP, I32, VP, VP, VP, VP]
+    L.hs_release_seq.argtypes = [VP, C.c_int64]
+    L.hs_consolidate.argtypes = [VP, I32, P(ConsolidateStats)]
+    L.hs_group_destroy.argtypes = [VP]
+    L.hs_group_info.argtypes = [VP, P(I32), P(I32)]
+    L.hs_debug_read_kv.argtypes = [VP, C.c_int64, I32, I32, I32, VP]
+    L.hs_debug_read_weights.argtypes = [VP, I32, U64, U64, VP]
+    L.hs_debug_poison_weights.argtypes = [VP, I32]
+    L.hs_debug_launch_count.argtypes = [VP, P(U64)]
+    L.hs_stage_timing_get.argtypes = [VP, I32, P(StageTiming)]
+    L.hs_profile_enable.argtypes = [VP, I32]
+    L.hs_profile_read.argtypes = [VP, P(ProfEntry), I32, P(I32), I32]
+    L.hs_debug_comm_selftest.argtypes = [P(Comm)]
+    L.hs_k_gemm.argtypes = [VP, I32, I32, VP, I32, I32, I32, VP, I32, VP, I32, VP, U64, VP]
+    L.hs_k_rmsnorm.argtypes = [VP, VP, VP, VP, I32, I32, C.c_float, VP]
+    L.hs_k_rope_kv.argtypes = [VP, VP, VP, VP, VP, VP, I32, I32, I32, VP]
+    L.hs_k_attention.argtypes = [VP, VP, VP, I32, I32, I32, VP, I32, VP, I32, I32, I32, VP, VP]
+    L.hs_k_argmax.argtypes = [VP, I32, I32, VP, VP]
+    L.hs_k_embed.argtypes = [VP, VP, VP, I32, I32, VP]
+    L.hs_k_span_copy.argtypes = [VP, VP, I32, U64, VP]
+    _lib = L
+    return L
+
+
+def check(code):
+    if code != 0:
+        raise HsError(code, lib().hs_last_error().decode())
+
+
+def model_cfg(cfg: dict) -> ModelCfg:
+    return ModelCfg(**{k: cfg[k] for k, _ in ModelCfg._fields_})
+
+
+def image_layout(cfg: dict) -> ImageHeader:
+    h = ImageHeader()
+    c = model_cfg(cfg)
+    check(lib().hs_image_layout(C.byref(c), C.byref(h)))
+    return h
+
+
+def plan_stages(cfg: dict, gpus, pp: int, full_memory_stages: int = 1, t_prefill_s: float = 0.0,
+                t_hop_s: float = 0.0) -> Plan:
+    arr = (Gpu * len(gpus))(*[Gpu(g["device"], g["h2d_gbps"], g.get("link_group", 0), g["free_bytes"]) for g in gpus])
+    out = Plan()
+    c = model_cfg(cfg)
+    check(lib().hs_plan_stages(C.byref(c), arr, len(gpus), pp, full_memory_stages, t_prefill_s, t_hop_s, C.byref(out)))
+    return out
+
+
+def predict_ttft_eq1(t_c, M, s, w, b, p, t_p, t_n):
+    D = C.c_double * s
+    return lib().hs_predict_ttft_eq1(t_c, M, s, w, D(*b), D(*p), t_p, t_n)
+
+
+def predict_tpot_eq2(t_d, s, w, t_n):
+    return lib().hs_predict_tpot_eq2(t_d, s, w, t_n)
+
+
+def predict_ttft_eq5(t_cc, t_cu, t_l, M, s, w, b, p, t_p, t_n):
+    D = C.c_double * s
+    return lib().hs_predict_ttft_eq5(t_cc, t_cu, t_l, M, s, w, D(*b), D(*p), t_p, t_n)
+
+
+class HostImage:
+    """A (slice of a) host weight image in pinned memory, filled by the caller's generator.
+    Holds a torch pinned tensor (torch = plumbing for host/device memory)."""
+
+    def __init__(self, header: ImageHeader, begin: int, end: int):
+        import torch
+        self.header = header
+        self.begin, self.end = begin, end
+        self.buf = torch.empty(end - begin, dtype=torch.uint8, pin_memory=True)
+
+    @property
+    def ptr(self) -> int:
+        return self.buf.data_ptr()
+
+    def c_image(self) -> Image:
+        return Image(C.pointer(self.header), C.c_void_p(self.ptr), self.begin, self.end - self.begin)
+
+
+class DistComm:
+    """hs_comm callbacks over torch.distributed (gloo sub-group for byte exchange)."""
+
+    def __init__(self):
+        import torch.distributed as dist
+        self.dist = dist
+        self.pg = dist.new_group(backend="gloo")
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+
+        def _ag(ctx, send, nbytes, recv):
+            try:
+                import torch
+                t = torch.frombuffer(bytearray(C.string_at(send, nbytes)), dtype=torch.uint8)
+                outs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(self.world)]
+                dist.all_gather(outs, t, group=self.pg)
+                cat = torch.cat(outs).numpy().tobytes()
+                C.memmove(recv, cat, len(cat))
+                return 0
+            except Exception:  # noqa
+                return 1
+
+        def _bar(ctx):
+            try:
+                dist.barrier(group=self.pg)
+                return 0
+            except Exception:  # noqa
+                return 1
+
+        self._ag, self._bar = ALLGATHER(_ag), BARRIER(_bar)
+        self.c = Comm(self.rank, self.world, None, self._ag, self._bar)
+
+
+def comm_selftest(comm: "DistComm"):
+    check(lib().hs_debug_comm_selftest(C.byref(comm.c)))
+
+
+class Group:
+    """A pipeline-parallel worker group (hs_group)."""
+
+    def __init__(self, cfg: dict, plan: Plan, image: HostImage | None = None, stage_images=None,
+                 num_blocks: int = 256, max_seqs: int = 16, max_tokens: int = 1024, comm: DistComm | None = None):
+        self.cfg = cfg
+        self.plan = plan
+        self._c = model_cfg(cfg)
+        self._img = image.c_image() if image is not None else None
+        self._keep = [image, stage_images]
+        self._stage_imgs = None
+        if stage_images is not None:
+            arr = (Image * plan.pp)(*[si.c_image() if si is not None else Image() for si in stage_images])
+            self._stage_imgs = arr
+        self._kv = KvCfg(16, num_blocks, max_seqs, max_tokens)
+        self._comm = comm
+        self.h = C.c_void_p()
+        check(lib().hs_group_create(C.byref(self._c), C.byref(plan), C.byref(self._img) if self._img else None,
+                                    self._stage_imgs, C.byref(self._kv), C.byref(comm.c) if comm else None,
+                                    C.byref(self.h)))
+
+    def load_stage_async(self, stage: int = -1, chunk_bytes: int = 0):
+        check(lib().hs_load_stage_async(self.h, stage, chunk_bytes))
+
+    def load_stats(self, stage: int, wait: bool = True) -> LoadStats:
+        s = LoadStats()
+        check(lib().hs_stage_load_stats(self.h, stage, 1 if wait else 0, C.byref(s)))
+        return s
+
+    def prefill(self, seq_ids, prompts, want_logits: bool = False):
+        n = len(seq_ids)
+        ids = np.asarray(seq_ids, dtype=np.int64)
+        lens = np.asarray([len(p) for p in prompts], dtype=np.int32)
+        toks = np.ascontiguousarray(np.concatenate([np.asarray(p, dtype=np.int32) for p in prompts]))
+        out = np.zeros(n, dtype=np.int32)
+        logits = np.zeros((n, self.cfg["vocab"]), dtype=np.float32) if want_logits else None
+        check(lib().hs_prefill(self.h, n, ids.ctypes.data, toks.ctypes.data, lens.ctypes.data, out.ctypes.data,
+                               logits.ctypes.data if logits is not None else None))
+        return out, logits
+
+    def decode_step(self, seq_ids, in_tokens=None, want_logits: bool = False):
+        n = len(seq_ids)
+        ids = np.asarray(seq_ids, dtype=np.int64)
+        tin = None if in_tokens is None else np.ascontiguousarray(np.asarray(in_tokens, dtype=np.int32))
+        out = np.zeros(n, dtype=np.int32)
+        logits = np.zeros((n, self.cfg["vocab"]), dtype=np.float32) if want_logits else None
+        check(lib().hs_decode_step(self.h, n, ids.ctypes.data, tin.ctypes.data if tin is not None else None,
+                                   out.ctypes.data, logits.ctypes.data if logits is not None else None))
+        return out, logits
+
+    def release_seq(self, seq_id: int):
+        check(lib().hs_release_seq(self.h, seq_id))
+
+    def consolidate(self, target: int = 0) -> ConsolidateStats:
+        s = ConsolidateStats()
+        check(lib().hs_consolidate(self.h, target, C.byref(s)))
+        return s
+
+    def info(self):
+        pp, owned = C.c_int32(), C.c_int32()
+        check(lib().hs_group_info(self.h, C.byref(pp), C.byref(owned)))
+        return pp.value, owned.value
+
+    def read_kv(self, seq_id: int, layer: int, pos0: int, n: int) -> np.ndarray:
+        out = np.zeros((n, 2, self.cfg["n_heads"], self.cfg["head_dim"]), dtype=np.uint16)
+        check(lib().hs_debug_read_kv(self.h, seq_id, layer, pos0, n, out.ctypes.data))
+        return out
+
+    def read_weights(self, stage: int, off: int, nbytes: int) -> np.ndarray:
+        out = np.empty(nbytes, dtype=np.uint8)
+        check(lib().hs_debug_read_weights(self.h, stage, off, nbytes, out.ctypes.data))
+        return out
+
+    def poison(self, stage: int):
+        check(lib().hs_debug_poison_weights(self.h, stage))
+
+    def timing(self, stage: int) -> StageTiming:
+        t = StageTiming()
+        check(lib().hs_stage_timing_get(self.h, stage, C.byref(t)))
+        return t
+
+    def profile(self, on: bool):
+        check(lib().hs_profile_enable(self.h, 1 if on else 0))
+
+    def profile_read(self, reset: bool = True) -> dict:
+        arr = (ProfEntry * 64)()
+        n = C.c_int32()
+        check(lib().hs_profile_read(self.h, arr, 64, C.byref(n), 1 if reset else 0))
+        return {arr[i].name.decode(): dict(count=arr[i].count, ms=arr[i].ms, bytes=arr[i].bytes, flops=arr[i].flops)
+                for i in range(min(n.value, 64))}
+
+    @staticmethod
+    def launch_count() -> int:
+        v = C.c_uint64()
+        check(lib().hs_debug_launch_count(None, C.byref(v)))
+        return v.value
+
+    def destroy(self):
+        if self.h:
+            check(lib().hs_group_destroy(self.h))
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:  # noqa
+            pass
+
+
+# ---------------------------------------------------------------- kernel entry points -------
+def _p(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    import torch
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def k_gemm(W, X, N, epi, out, resid=None, ws=None):
+    M, K = W.shape
+    ldo = out.shape[-1]
+    check(lib().hs_k_gemm(_p(W), M, K, _p(X), X.shape[0], N, epi, _p(out), ldo, _p(resid),
+                          resid.shape[-1] if resid is not None else 0, _p(ws),
+                          ws.numel() * ws.element_size() if ws is not None else 0, _stream()))
+
+
+def k_rmsnorm(x, w, y, eps, rows=None, T=None):
+    T = T if T is not None else (rows.numel() if rows is not None else x.shape[0])
+    check(lib().hs_k_rmsnorm(_p(x), _p(rows), _p(w), _p(y), T, x.shape[1], eps, _stream()))
+
+
+def k_rope_kv(qkv, pos, slot, tab, q_out, pool, n_heads, head_dim):
+    check(lib().hs_k_rope_kv(_p(qkv), _p(pos), _p(slot), _p(tab), _p(q_out), _p(pool), qkv.shape[0], n_heads,
+                             head_dim, _stream()))
+
+
+def k_attention(q, pool, seqs, max_nq, max_ctx, tables, o, n_heads, head_dim, decode, ws=None):
+    check(lib().hs_k_attention(_p(q), _p(pool), _p(seqs), seqs.shape[0], max_nq, max_ctx, _p(tables),
+                               tables.shape[1], _p(o), n_heads, head_dim, 1 if decode else 0, _p(ws), _stream()))
+
+
+def k_argmax(logits, tokens):
+    check(lib().hs_k_argmax(_p(logits), logits.shape[1], logits.shape[0], _p(tokens), _stream()))
+
+
+def k_embed(tok, E, x):
+    check(lib().hs_k_embed(_p(tok), _p(E), _p(x), tok.numel(), E.shape[1], _stream()))
+
+
+def k_span_copy(src, dst, span_bytes):
+    check(lib().hs_k_span_copy(_p(src), _p(dst), src.numel(), span_bytes, _stream()))

@@ -1,0 +1,87 @@
+"""CPU-side checks of the C-ABI library (no GPU needed): it loads, exports every symbol the
+headers declare, its image layout agrees with the input generator's, and its host-only
+planner / predictors agree with the oracle (integers bit-exact, predictions to 1e-12)."""
+import os
+import re
+
+import pytest
+
+import hsgen
+from oracle import plan as oplan
+from paper_2502_15524_b200 import hs
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    names = []
+    for h in ("hs.h", "hs_kernels.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        names += re.findall(r"^\s*(?:hs_status|double|const char\*)\s+(hs_\w+)\s*\(", src, re.M)
+    return names
+
+
+def test_library_exports_every_declared_symbol():
+    L = hs.lib()
+    decl = declared_symbols()
+    assert len(decl) >= 25
+    missing = [n for n in decl if not hasattr(L, n)]
+    assert not missing, missing
+    assert set(decl) == set(hs.SYMBOLS)
+
+
+@pytest.mark.parametrize("name", ["tiny", "llama2-7b", "llama2-13b"])
+def test_image_layout_matches_generator(name):
+    a = hs.image_layout(hsgen.CONFIGS[name])
+    b = hsgen.image_header(hsgen.CONFIGS[name])
+    assert bytes(a) == bytes(b)
+    assert a.param_bytes == sum(oplan.stage_param_bytes(hsgen.CONFIGS[name], 1))
+
+
+@pytest.mark.parametrize("name,pp", [("tiny", 1), ("tiny", 2), ("tiny", 3), ("tiny", 4), ("llama2-7b", 1),
+                                     ("llama2-7b", 2), ("llama2-7b", 4), ("llama2-7b", 8), ("llama2-13b", 4),
+                                     ("llama2-13b", 8), ("llama2-13b", 3)])
+def test_plan_matches_oracle(name, pp):
+    cfg = hsgen.CONFIGS[name]
+    gpus = [dict(device=i, h2d_gbps=55.6 - 0.01 * ((i * 5) % 8), link_group=i // 2, free_bytes=183 * 2**30)
+            for i in range(8)]
+    if name != "tiny":  # only two GPUs can hold the whole model: w=1 goes to the fastest of them
+        for g in gpus[2:]:
+            g["free_bytes"] = 20 * 2**30 if name == "llama2-7b" else 9 * 2**30
+    ours = hs.plan_stages(cfg, gpus, pp, 1, t_prefill_s=0.01, t_hop_s=1e-5).as_dict()
+    ref = oplan.plan(cfg, gpus, pp, 1, t_prefill_s=0.01, t_hop_s=1e-5)
+    assert ours["device"] == ref["device"]
+    assert ours["ranges"] == ref["ranges"]
+    assert ours["stage_bytes"] == ref["stage_bytes"]
+    assert ours["full_memory"] == ref["full_memory"]
+    assert ours["pred_ttft_s"] == pytest.approx(ref["pred_ttft_s"], rel=1e-12)
+    # slices are contiguous, cover [embed, end) and each holds at least the stage's bytes
+    h = hs.image_layout(cfg)
+    sl = ours["slices"]
+    assert sl[0][0] == h.embed_off and sl[-1][1] == h.total_bytes
+    assert all(sl[k][1] == sl[k + 1][0] for k in range(pp - 1))
+    assert all(e - b >= nb for (b, e), nb in zip(sl, ours["stage_bytes"]))
+
+
+def test_plan_errors():
+    cfg = hsgen.CONFIGS["llama2-7b"]
+    gpus = [dict(device=0, h2d_gbps=55.0, free_bytes=183 * 2**30)]
+    with pytest.raises(hs.HsError) as e:
+        hs.plan_stages(cfg, gpus, 2, 1)
+    assert e.value.code == 4  # HS_E_INFEASIBLE
+    with pytest.raises(hs.HsError) as e:
+        hs.plan_stages(cfg, gpus, 0, 1)
+    assert e.value.code == 1  # pp = 0 (SLO-driven choice) is not implemented yet
+    small = [dict(device=i, h2d_gbps=55.0, free_bytes=1 * 2**30) for i in range(8)]
+    with pytest.raises(hs.HsError):
+        hs.plan_stages(cfg, small, 8, 1)  # 1.9 GB stages do not fit 1 GiB
+
+
+def test_predictors_spec_values():
+    assert hs.predict_ttft_eq1(10, 100, 4, 0, [16] * 4, [128] * 4, 0.5, 0.01) == pytest.approx(13.7978125, abs=1e-12)
+    assert hs.predict_ttft_eq1(10, 100, 4, 4, [16] * 4, [128] * 4, 0.5, 0.01) == pytest.approx(12.2978125, abs=1e-12)
+    assert hs.predict_tpot_eq2(0.05, 4, 0, 0.01) == pytest.approx(0.24)
+    assert hs.predict_tpot_eq2(0.05, 4, 4, 0.01) == pytest.approx(0.09)
+    assert hs.predict_ttft_eq5(4, 2, 6, 100, 4, 0, [16] * 4, [128] * 4, 0.5, 0.01) == pytest.approx(14.04)
+    for args in [(3, 1, 2, 50, 2, 1, [10, 20], [30, 5], 0.2, 0.01), (0, 0, 0, 400, 4, 0, [16] * 4, [1000] * 4, 0, 0)]:
+        assert hs.predict_ttft_eq5(*args) == pytest.approx(oplan.eq5_ttft(*args), rel=1e-12)
