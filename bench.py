@@ -142,7 +142,8 @@ def run_ours(args):
     b, e = pd["slices"][rank if world > 1 else 0] if world > 1 else (hdr.embed_off, hdr.total_bytes)
     t_img = time.time()
     img = hs.HostImage(hdr, b, e)
-    hsgen.image_fill(hsgen.image_header(cfg), hsgen.WEIGHT_SEED, img.ptr, b, e)
+    hsgen.image_fill(hsgen.image_header(cfg), hsgen.WEIGHT_SEED, img.ptr, b, e,
+                     nthreads=max(1, cpu_cores() // max(1, world)))
     t_img = time.time() - t_img
     prompts = hsgen.prompts(n_seqs, plen, cfg["vocab"])
     ids = list(range(n_seqs))

@@ -309,6 +309,283 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
   }
 }
 
+// ------------------------------------------------------------------ stream-K (decode) -----
+// Persistent weight-streaming GEMM for small N (decode, N <= 64 tokens): the flattened space
+// of (tile, 64-wide K block) work is cut into G equal contiguous ranges, one per CTA
+// (G = #SMs), so every SM streams the same number of weight bytes whatever M and K are (no
+// wave quantisation, no idle SMs).  A CTA's range covers parts of one or more 128-row tiles;
+// each part's fp32 accumulator goes to a workspace slot; the CTA that completes a tile last
+// (per-tile arrival counter) sums the tile's parts in part order (deterministic) and applies
+// the epilogue, fused with the row-wide ops of decode:
+//   - FUSE_ROPE (QKV): bf16 rounding, RoPE of q and k, paged KV write;
+//   - FUSE_NORM (O-proj, down-proj): residual add, then the CTA that completes the last tile
+//     computes the RMSNorm of the whole row (grid-level arrival counter).
+// Counters are reset by their last arriver, so they are zero again for the next launch.
+// Warp roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer, warps 2-5 epilogue
+// (warp w drains TMEM lanes 32*(w%4)..); two TMEM accumulators so the MMA of part i+1
+// overlaps the drain of part i.
+struct SkParams {
+  int M, N, nkb, tiles, G, maxp;
+  float* ws;
+  unsigned* ctr;  // [tiles + 1]
+  int epi;
+  void* out;
+  int ldo;
+  const bf16* resid;
+  int ldr;
+  int fuse;
+  const bf16* norm_w;
+  bf16* norm_out;
+  float eps;
+  const int* pos;
+  const int* slot;
+  const float2* tab;
+  bf16* q_out;
+  bf16* pool;
+  int nh, hd;  // heads, head_dim
+};
+
+__device__ __forceinline__ int sk_begin(long long c, long long W, int G) { return (int)(c * W / G); }
+// CTA owning flattened k-block x: max c with floor(c W / G) <= x
+__device__ __host__ __forceinline__ int sk_owner(long long x, long long W, int G) {
+  return (int)(((x + 1) * G + W - 1) / W) - 1;
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// RMSNorm of one row with 128 threads (tid in [0,128)); fixed summation order.  Not inlined,
+// so the GEMM epilogue and the standalone decode row-norm run the very same code (PP = s
+// stays bitwise equal to PP = 1 across the stage boundary).
+__device__ __noinline__ void row_norm128(const bf16* __restrict__ h, int M, const bf16* __restrict__ w,
+                                         bf16* __restrict__ y, float eps, int tid, float* red, int bar_id) {
+  float ss = 0.f;
+  for (int m = tid; m < M; m += 128) {
+    const float v = __bfloat162float(h[m]);
+    ss = fmaf(v, v, ss);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((tid & 31) == 0) red[tid >> 5] = ss;
+  named_bar(bar_id, 128);
+  const float tot = (red[0] + red[1]) + (red[2] + red[3]);
+  const float rs = 1.0f / sqrtf(tot / (float)M + eps);
+  for (int m = tid; m < M; m += 128) y[m] = __float2bfloat16_rn(__bfloat162float(h[m]) * rs * __bfloat162float(w[m]));
+  named_bar(bar_id, 128);
+}
+
+template <int BN>
+struct SkCfg {
+  static constexpr int A_BYTES = 128 * 64 * 2;
+  static constexpr int B_BYTES = BN * 64 * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = BN >= 64 ? 6 : 8;
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int VALS_BYTES = 128 * BN * 4;  // tile values for the RoPE pairing
+  static constexpr int SMEM = STAGES * STAGE_BYTES + VALS_BYTES + 1024 + 512;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(192, 1)
+    gemm_sk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, SkParams p) {
+  using C = SkCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* vals = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + C::VALS_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  volatile int* flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
+  float* red = reinterpret_cast<float*>(tmem_slot + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long W = (long long)p.tiles * p.nkb;
+  const int beg = sk_begin(blockIdx.x, W, p.G), end = sk_begin(blockIdx.x + 1, W, p.G);
+
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"((uint32_t)C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer over every segment of the range
+      int i = 0;
+      for (int cur = beg; cur < end;) {
+        const int t = cur / p.nkb, kb_lo = cur % p.nkb, kb_hi = min(p.nkb, kb_lo + (end - cur));
+        for (int kb = kb_lo; kb < kb_hi; ++kb, ++i) {
+          const int s = i % C::STAGES;
+          mbar_wait(&empty[s], ((i / C::STAGES) & 1) ^ 1);
+          uint8_t* sa = smem + s * C::STAGE_BYTES;
+          mbar_expect_tx(&full[s], C::STAGE_BYTES);
+          tma_load_2d(&tmA, &full[s], sa, kb * 64, t * 128);
+          tma_load_2d(&tmB, &full[s], sa + C::A_BYTES, kb * 64, 0);
+        }
+        cur += kb_hi - kb_lo;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      constexpr uint32_t idesc = instr_desc<BN>();
+      int i = 0, seg = 0;
+      for (int cur = beg; cur < end; ++seg) {
+        const int kb_lo = cur % p.nkb, kb_hi = min(p.nkb, kb_lo + (end - cur));
+        const int buf = seg & 1;
+        mbar_wait(&tempty[buf], ((seg >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + buf * BN;
+        for (int kb = kb_lo; kb < kb_hi; ++kb, ++i) {
+          const int s = i % C::STAGES;
+          mbar_wait(&full[s], (i / C::STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint8_t* sa = smem + s * C::STAGE_BYTES;
+          const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + C::A_BYTES);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) umma_bf16(acc, da + 2 * k, db + 2 * k, idesc, (kb > kb_lo || k > 0) ? 1u : 0u);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[buf]);
+        cur += kb_hi - kb_lo;
+      }
+    }
+  } else {
+    // ---- epilogue warps 2..5 (et = 0..127 owns tile row ml = et)
+    const int quad = warp & 3;
+    const int ml = quad * 32 + lane;
+    const int et = ml;
+    int seg = 0;
+    for (int cur = beg; cur < end; ++seg) {
+      const int t = cur / p.nkb, kb_lo = cur % p.nkb, kb_hi = min(p.nkb, kb_lo + (end - cur));
+      const int buf = seg & 1;
+      mbar_wait(&tfull[buf], (seg >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int first = sk_owner((long long)t * p.nkb, W, p.G);
+      const int np = sk_owner((long long)(t + 1) * p.nkb - 1, W, p.G) - first + 1;
+      const int part = blockIdx.x - first;
+      float* tws = p.ws + (size_t)t * p.maxp * BN * 128;
+      {
+        float* dst = tws + (size_t)part * BN * 128 + ml;
+        const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + buf * BN;
+        constexpr int CH = BN < 32 ? 16 : 32;
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += CH) {
+          float v[32];
+          if constexpr (CH == 32) tmem_ld32(taddr + c0, v);
+          else tmem_ld16(taddr + c0, v);
+#pragma unroll
+          for (int j = 0; j < CH; ++j)
+            if (c0 + j < p.N) dst[(size_t)(c0 + j) * 128] = v[j];
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf])) : "memory");
+      cur += kb_hi - kb_lo;
+      // ---- arrival: the last CTA to finish a part of tile t applies its epilogue
+      __threadfence();
+      named_bar(1, 128);
+      if (et == 0) {
+        const unsigned old = atomicAdd(&p.ctr[t], 1u);
+        const int last = old == (unsigned)(np - 1);
+        if (last) p.ctr[t] = 0;
+        *flag = last;
+      }
+      named_bar(1, 128);
+      if (!*flag) continue;
+      __threadfence();
+      const int m = t * 128 + ml;
+      if (p.fuse == FUSE_ROPE) {
+        for (int n = 0; n < p.N; ++n) {
+          float a = 0.f;
+          for (int pt = 0; pt < np; ++pt) a += __ldcg(tws + (size_t)pt * BN * 128 + (size_t)n * 128 + ml);
+          vals[ml * BN + n] = __bfloat162float(__float2bfloat16_rn(a));
+        }
+        named_bar(1, 128);
+        const int H = p.nh * p.hd, half = p.hd >> 1;
+        const int region = (t * 128) / H, r0 = (t * 128) % H;  // 0 q, 1 k, 2 v
+        if (et < 64) {
+          const int hl = et / half, i = et % half;
+          const int ra = hl * p.hd + i, rb = ra + half;
+          const int head = (r0 + ra) / p.hd;
+          for (int n = 0; n < p.N; ++n) {
+            const float a = vals[ra * BN + n], b = vals[rb * BN + n];
+            const int sl = p.slot[n];
+            const size_t blk = (size_t)(sl >> 4), off = (size_t)(sl & 15);
+            if (region == 2) {
+              bf16* vd = p.pool + (((blk * 2 + 1) * p.nh + head) * 16 + off) * p.hd;
+              vd[i] = __float2bfloat16_rn(a);
+              vd[i + half] = __float2bfloat16_rn(b);
+            } else {
+              const float2 cs = p.tab[(size_t)p.pos[n] * half + i];
+              const bf16 x1 = __float2bfloat16_rn(a * cs.x - b * cs.y), x2 = __float2bfloat16_rn(b * cs.x + a * cs.y);
+              bf16* d = region == 0 ? p.q_out + (size_t)n * H + head * p.hd
+                                    : p.pool + (((blk * 2 + 0) * p.nh + head) * 16 + off) * p.hd;
+              d[i] = x1;
+              d[i + half] = x2;
+            }
+          }
+        }
+        named_bar(1, 128);
+        continue;
+      }
+      for (int n = 0; n < p.N; ++n) {
+        float a = 0.f;
+        for (int pt = 0; pt < np; ++pt) a += __ldcg(tws + (size_t)pt * BN * 128 + (size_t)n * 128 + ml);
+        if (p.epi == EPI_F32) {
+          reinterpret_cast<float*>(p.out)[(size_t)n * p.ldo + m] = a;
+        } else if (p.epi == EPI_BF16) {
+          reinterpret_cast<bf16*>(p.out)[(size_t)n * p.ldo + m] = __float2bfloat16_rn(a);
+        } else if (p.epi == EPI_RESID) {
+          reinterpret_cast<bf16*>(p.out)[(size_t)n * p.ldo + m] =
+              __float2bfloat16_rn(a + __bfloat162float(p.resid[(size_t)n * p.ldr + m]));
+        } else {  // silu-mul: lanes 0-15 gate rows, 16-31 their up rows
+          const float u = __shfl_xor_sync(0xffffffffu, a, 16);
+          if (lane < 16) reinterpret_cast<bf16*>(p.out)[(size_t)n * p.ldo + (m >> 5) * 16 + lane] = __float2bfloat16_rn(silu_f(a) * u);
+        }
+      }
+      if (p.fuse == FUSE_NORM) {  // grid-level arrival: the last tile's CTA normalises the rows
+        __threadfence();
+        named_bar(1, 128);
+        if (et == 0) {
+          const unsigned old = atomicAdd(&p.ctr[p.tiles], 1u);
+          const int last = old == (unsigned)(p.tiles - 1);
+          if (last) p.ctr[p.tiles] = 0;
+          *flag = last;
+        }
+        named_bar(1, 128);
+        if (*flag) {
+          __threadfence();
+          for (int n = 0; n < p.N; ++n)
+            row_norm128(reinterpret_cast<const bf16*>(p.out) + (size_t)n * p.ldo, p.M, p.norm_w,
+                        p.norm_out + (size_t)n * p.ldo, p.eps, et, red, 1);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)C::TMEM_COLS));
+}
+
+// Decode RMSNorm with the exact arithmetic of the fused epilogue (one 128-thread CTA per row).
+__global__ void __launch_bounds__(128) rownorm_kernel(const bf16* __restrict__ x, const bf16* __restrict__ w,
+                                                      bf16* __restrict__ y, int H, float eps) {
+  __shared__ float red[4];
+  row_norm128(x + (size_t)blockIdx.x * H, H, w, y + (size_t)blockIdx.x * H, eps, threadIdx.x, red, 1);
+}
+
 // ------------------------------------------------------------------ host side -----------
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                     const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -399,7 +676,19 @@ static void warm_one() {
   cudaFuncGetAttributes(&at, gemm_kernel<BN>);
 }
 
+template <int BN>
+static void warm_sk() {
+  cudaFuncAttributes at;
+  cudaFuncSetAttribute(gemm_sk_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SkCfg<BN>::SMEM);
+  cudaFuncGetAttributes(&at, gemm_sk_kernel<BN>);
+}
+
 void warm_gemm_kernels() {
+  warm_sk<16>();
+  warm_sk<32>();
+  warm_sk<64>();
+  cudaFuncAttributes at0;
+  cudaFuncGetAttributes(&at0, rownorm_kernel);
   warm_one<16>();
   warm_one<32>();
   warm_one<64>();
@@ -409,9 +698,58 @@ void warm_gemm_kernels() {
   cudaFuncGetAttributes(&at, splitk_reduce_kernel);
 }
 
+template <int BN>
+static hs_status launch_sk(const GemmArgs& a, cudaStream_t st, bool* done) {
+  using C = SkCfg<BN>;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int G = num_sms(dev);
+  const int tiles = a.M / 128, nkb = a.K / 64;
+  const long long W = (long long)tiles * nkb;
+  const int per = (int)(W / G);
+  if (per < 2) return HS_OK;  // too little work per SM: use the tiled kernel
+  const int maxp = (nkb + per - 1) / per + 1;
+  const uint64_t ctr_bytes = align_up((uint64_t)(tiles + 1) * 4, 256);
+  if (ctr_bytes + (uint64_t)tiles * maxp * BN * 128 * 4 > a.workspace_bytes || !a.counters) return HS_OK;
+  const GemmFusion& f = a.fuse;
+  if (f.kind == FUSE_ROPE && (a.epi != EPI_BF16 || (f.head_dim != 64 && f.head_dim != 128))) return HS_OK;
+  static bool attr_set[64] = {};
+  if (dev < 64 && !attr_set[dev]) {
+    HS_CUDA(cudaFuncSetAttribute(gemm_sk_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set[dev] = true;
+  }
+  int bi = 0;
+  while (kBN[bi] != BN) ++bi;
+  SkParams p{};
+  p.M = a.M; p.N = a.N; p.nkb = nkb; p.tiles = tiles; p.G = G; p.maxp = maxp;
+  p.ws = a.workspace; p.ctr = a.counters;
+  p.epi = a.epi; p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr;
+  p.fuse = f.kind; p.norm_w = f.norm_w; p.norm_out = f.norm_out; p.eps = f.eps;
+  p.pos = f.pos; p.slot = f.slot; p.tab = f.rope_tab; p.q_out = f.q_out; p.pool = f.pool;
+  p.nh = f.n_heads; p.hd = f.head_dim;
+  if (p.fuse == FUSE_NORM && a.epi != EPI_RESID) p.fuse = FUSE_NONE;
+  gemm_sk_kernel<BN><<<G, 192, C::SMEM, st>>>(a.A->map, a.B[bi].map, p);
+  count_launch();
+  HS_CUDA(cudaGetLastError());
+  if (f.applied && p.fuse != FUSE_NONE) *f.applied = true;
+  *done = true;
+  return HS_OK;
+}
+
+void launch_rownorm_decode(const bf16* x, const bf16* w, bf16* y, int T, int H, float eps, cudaStream_t st) {
+  rownorm_kernel<<<T, 128, 0, st>>>(x, w, y, H, eps);
+  count_launch();
+}
+
 hs_status gemm(const GemmArgs& a, cudaStream_t st) {
   if (a.M % 128 || a.K % 64 || a.N <= 0) HS_FAIL(HS_E_INVAL, "gemm shape M=%d N=%d K=%d", a.M, a.N, a.K);
+  if (a.fuse.applied) *a.fuse.applied = false;
   const int BN = gemm_bn(a.N);
+  if (BN <= 64 && a.workspace) {  // weight-streaming decode GEMM: stream-K over all SMs
+    bool done = false;
+    hs_status r = BN == 16 ? launch_sk<16>(a, st, &done) : BN == 32 ? launch_sk<32>(a, st, &done) : launch_sk<64>(a, st, &done);
+    if (r != HS_OK || done) return r;
+  }
   const int tiles = (a.M / 128) * (int)cdiv(a.N, BN);
   const int nkb = a.K / 64;
   int dev = 0;

@@ -27,6 +27,26 @@ struct TmaMat {
 // Encodes a 128B-swizzled K-major tile map (box = 64 cols x box_rows rows).
 hs_status make_tma(TmaMat* t, const void* ptr, int64_t rows, int64_t cols, int box_rows);
 
+// Decode-path fusions applied by the stream-K reduction (the whole output row of a token is
+// available there):
+//   FUSE_NORM : out = bf16(acc + resid) (as EPI_RESID) and norm_out = RMSNorm(out) * norm_w
+//   FUSE_ROPE : (QKV GEMM, EPI_BF16) q, k, v = bf16(acc); q' / k' rotated (RoPE table), q' to
+//               q_out, k' and v written into the paged KV pool at slot[n]
+enum GemmFuse : int { FUSE_NONE = 0, FUSE_NORM = 1, FUSE_ROPE = 2 };
+struct GemmFusion {
+  int kind = FUSE_NONE;
+  const bf16* norm_w = nullptr;
+  bf16* norm_out = nullptr;
+  float eps = 0.f;
+  const int* pos = nullptr;
+  const int* slot = nullptr;
+  const float2* rope_tab = nullptr;
+  bf16* q_out = nullptr;
+  bf16* pool = nullptr;
+  int n_heads = 0, head_dim = 0;
+  bool* applied = nullptr;  // set to true when the fusion ran (else the caller runs the op)
+};
+
 struct GemmArgs {
   const TmaMat* A;   // weights [M, K]  (box_rows must be 128)
   const TmaMat* B;   // activations [>=N, K] (box_rows must equal the chosen BN; see gemm_bn)
@@ -36,8 +56,10 @@ struct GemmArgs {
   int ldo;           // elements
   const bf16* resid; // EPI_RESID: resid[n * ldr + m]
   int ldr;
-  float* workspace;  // split-K partials (may be null => no split)
+  float* workspace;  // split-K / stream-K partials (may be null => no split)
   uint64_t workspace_bytes;
+  unsigned* counters;  // stream-K arrival counters: >= M/128 + 1 zeroed words (null => no stream-K)
+  GemmFusion fuse;
 };
 
 // Tile width (tokens) the launcher will use for N tokens; activation maps must be encoded
@@ -48,5 +70,10 @@ int gemm_bn_count();
 int gemm_bn_value(int i);
 
 hs_status gemm(const GemmArgs& a, cudaStream_t stream);
+
+// RMSNorm of T rows with exactly the arithmetic of the FUSE_NORM epilogue (decode path: a
+// stage's first layer normalises its input like the previous layer's fused epilogue would,
+// so PP = s stays bitwise equal to PP = 1).  H <= 8192.
+void launch_rownorm_decode(const bf16* x, const bf16* w, bf16* y, int T, int H, float eps, cudaStream_t st);
 
 }  // namespace hs

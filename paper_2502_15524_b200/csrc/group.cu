@@ -37,6 +37,7 @@ static constexpr int kBlock = 16;
 static constexpr uint64_t kDefaultChunk = 32ull << 20;
 static constexpr uint64_t kWorkspace = 64ull << 20;
 static constexpr int kSendCtas = 64;
+static constexpr uint64_t kCounters = 1 << 16;
 
 // Comm block of a stage (one allocation, shared with peers): flags + token / hidden inputs.
 struct CommLayout {
@@ -79,6 +80,7 @@ struct Stage {
   bf16 *xa = nullptr, *xb = nullptr, *nrm = nullptr, *qkv = nullptr, *q = nullptr, *o = nullptr,
        *act = nullptr, *fin = nullptr;
   float *logits = nullptr, *ws = nullptr, *attn_ws = nullptr;
+  unsigned* ctr = nullptr;  // stream-K / attention arrival counters (zeroed; self-resetting)
   float2* rope = nullptr;
   uint8_t* d_meta = nullptr;
   uint8_t* h_meta = nullptr;  // pinned staging
@@ -204,7 +206,7 @@ static void free_stage(Stage& s) {
   auto F = [](void* p) { if (p) cudaFree(p); };
   if (s.owned) {
     F(s.arena); F(s.kv_mem); F(s.comm); F(s.xa); F(s.xb); F(s.nrm); F(s.qkv); F(s.q); F(s.o);
-    F(s.act); F(s.fin); F(s.logits); F(s.ws); F(s.attn_ws); F(s.rope); F(s.d_meta); F(s.d_tok_out);
+    F(s.act); F(s.fin); F(s.logits); F(s.ws); F(s.attn_ws); F(s.ctr); F(s.rope); F(s.d_meta); F(s.d_tok_out);
     if (s.h_meta) cudaFreeHost(s.h_meta);
     if (s.h_out) cudaFreeHost(s.h_out);
     for (auto e : s.ev_layer) if (e) cudaEventDestroy(e);
@@ -270,7 +272,9 @@ static hs_status setup_owned_stage(hs_group* g, int k) {
   HS_ALLOC(s.fin, (size_t)std::max(S, 16) * H * 2);
   HS_ALLOC(s.logits, (size_t)S * c.vocab * 4);
   HS_ALLOC(s.ws, kWorkspace);
-  HS_ALLOC(s.attn_ws, (size_t)S * c.n_heads * 16 * (c.head_dim + 2) * 4);
+  HS_ALLOC(s.ctr, kCounters * 4);
+  HS_CUDA(cudaMemset(s.ctr, 0, kCounters * 4));
+  HS_ALLOC(s.attn_ws, (size_t)S * c.n_heads * attn_decode_splits(c.max_seq) * (c.head_dim + 2) * 4);
   HS_ALLOC(s.d_tok_out, (size_t)align_up(S * 4, 16) + 16);
   // RoPE table (fp32 cos/sin of angle = p * theta^(-2i/d), computed in double), DESIGN.md
   {
@@ -500,7 +504,11 @@ static void layout_meta(CallMeta& m, int max_blocks) {
   m.bytes = o;
 }
 
-static hs_status run_layer(hs_group* g, Stage& s, int l, bf16*& x, const CallMeta& m) {
+// One decoder layer (a6-a12) on a stage.  `normed` says s.nrm already holds RMSNorm(x) with
+// this layer's attn_norm (fused into the previous layer's down-projection epilogue in decode);
+// on return it says whether s.nrm holds the next consumer's norm (next layer's attn_norm, or
+// the final norm into s.fin for the model's last layer).
+static hs_status run_layer(hs_group* g, Stage& s, int l, bf16*& x, const CallMeta& m, bool& normed, bool& fin_done) {
   const hs_model_cfg& c = g->cfg;
   const int H = c.hidden, T = m.T;
   LayerDev& L = s.layers[l];
@@ -513,26 +521,45 @@ static hs_status run_layer(hs_group* g, Stage& s, int l, bf16*& x, const CallMet
   bf16* hbuf = (x == s.xb) ? s.xa : s.xb;
   const bool dec = m.decode;
   const double TH2 = 2.0 * T * H, F = c.ffn;
-  { ProfScope ps(g, s, PK_RMSNORM, dec, 2 * TH2 + 2.0 * H, 0);
-    launch_rmsnorm(x, nullptr, L.attn_norm, s.nrm, T, H, c.rms_eps, st); }
+  if (!normed) {
+    ProfScope ps(g, s, PK_RMSNORM, dec, 2 * TH2 + 2.0 * H, 0);
+    if (dec && H <= 8192) launch_rownorm_decode(x, L.attn_norm, s.nrm, T, H, c.rms_eps, st);
+    else launch_rmsnorm(x, nullptr, L.attn_norm, s.nrm, T, H, c.rms_eps, st);
+  }
+  bool applied = false;
   GemmArgs a{};
-  a.N = T; a.K = H; a.workspace = s.ws; a.workspace_bytes = kWorkspace;
+  a.N = T; a.K = H; a.workspace = s.ws; a.workspace_bytes = kWorkspace; a.counters = s.ctr;
   a.A = &L.wqkv; a.B = s.b_nrm; a.M = 3 * H; a.epi = EPI_BF16; a.out = s.qkv; a.ldo = 3 * H;
+  if (dec) {  // fused bf16 rounding + RoPE + paged KV write in the stream-K reduction
+    a.fuse.kind = FUSE_ROPE; a.fuse.pos = pos; a.fuse.slot = slot; a.fuse.rope_tab = s.rope; a.fuse.q_out = s.q;
+    a.fuse.pool = pool; a.fuse.n_heads = c.n_heads; a.fuse.head_dim = c.head_dim; a.fuse.applied = &applied;
+  }
   { ProfScope ps(g, s, PK_GEMM_QKV, dec, gemm_bytes(3.0 * H, T, H, 3.0 * H, false), 2.0 * 3 * H * T * H);
     HS_TRY(gemm(a, st)); }
-  { ProfScope ps(g, s, PK_ROPE_KV, dec, 3 * TH2 + 3 * TH2, 0);
-    launch_rope_kv(s.qkv, pos, slot, s.rope, s.q, pool, T, c.n_heads, c.head_dim, st); }
+  if (!applied) {
+    ProfScope ps(g, s, PK_ROPE_KV, dec, 3 * TH2 + 3 * TH2, 0);
+    launch_rope_kv(s.qkv, pos, slot, s.rope, s.q, pool, T, c.n_heads, c.head_dim, st);
+  }
   { ProfScope ps(g, s, PK_ATTN, dec, 2 * TH2 + 2.0 * 2 * H * m.kv_tokens, 4.0 * H * m.attn_pairs);
     if (m.decode)
       launch_attn_decode(s.q, pool, sd, m.n, m.max_ctx, tab, g->max_blocks, s.o, c.n_heads, c.head_dim,
-                         s.attn_ws, attn_decode_splits(m.max_ctx), st);
+                         s.attn_ws, attn_decode_splits(m.max_ctx), s.ctr + kCounters / 2, st);
     else
       launch_attn_prefill(s.q, pool, sd, m.n, m.max_nq, tab, g->max_blocks, s.o, c.n_heads, c.head_dim, st); }
+  a.fuse = GemmFusion{};
+  applied = false;
   a.A = &L.wo; a.B = s.b_o; a.M = H; a.K = H; a.epi = EPI_RESID; a.out = hbuf; a.ldo = H; a.resid = x; a.ldr = H;
+  if (dec) {  // fused residual + RMSNorm(ffn_norm)
+    a.fuse.kind = FUSE_NORM; a.fuse.norm_w = L.ffn_norm; a.fuse.norm_out = s.nrm; a.fuse.eps = c.rms_eps;
+    a.fuse.applied = &applied;
+  }
   { ProfScope ps(g, s, PK_GEMM_O, dec, gemm_bytes(H, T, H, H, true), 2.0 * H * T * H);
     HS_TRY(gemm(a, st)); }
-  { ProfScope ps(g, s, PK_RMSNORM, dec, 2 * TH2 + 2.0 * H, 0);
-    launch_rmsnorm(hbuf, nullptr, L.ffn_norm, s.nrm, T, H, c.rms_eps, st); }
+  if (!applied) {
+    ProfScope ps(g, s, PK_RMSNORM, dec, 2 * TH2 + 2.0 * H, 0);
+    launch_rmsnorm(hbuf, nullptr, L.ffn_norm, s.nrm, T, H, c.rms_eps, st);
+  }
+  a.fuse = GemmFusion{};
   a.A = &L.wgu; a.B = s.b_nrm; a.M = 2 * c.ffn; a.K = H; a.epi = EPI_SILU_MUL; a.out = s.act; a.ldo = c.ffn;
   a.resid = nullptr;
   { ProfScope ps(g, s, PK_GEMM_GU, dec, gemm_bytes(2 * F, T, H, F, false), 2.0 * 2 * F * T * H);
@@ -540,8 +567,25 @@ static hs_status run_layer(hs_group* g, Stage& s, int l, bf16*& x, const CallMet
   bf16* xout = (hbuf == s.xa) ? s.xb : s.xa;
   a.A = &L.wd; a.B = s.b_act; a.M = H; a.K = c.ffn; a.epi = EPI_RESID; a.out = xout; a.ldo = H; a.resid = hbuf;
   a.ldr = H;
+  applied = false;
+  const bool next_here = l + 1 < s.le;
+  const bool model_last = l + 1 == c.n_layers;
+  if (dec && (next_here || model_last)) {  // fused residual + next consumer's RMSNorm
+    a.fuse.kind = FUSE_NORM;
+    a.fuse.eps = c.rms_eps;
+    a.fuse.applied = &applied;
+    if (next_here) {
+      a.fuse.norm_w = s.layers[l + 1].attn_norm;
+      a.fuse.norm_out = s.nrm;
+    } else {  // decode: every row is a sequence's last position -> final norm into s.fin
+      a.fuse.norm_w = reinterpret_cast<const bf16*>(s.wptr(g->hdr.final_off + g->hdr.t_final_norm));
+      a.fuse.norm_out = s.fin;
+    }
+  }
   { ProfScope ps(g, s, PK_GEMM_DOWN, dec, gemm_bytes(H, T, F, H, true), 2.0 * H * T * F);
     HS_TRY(gemm(a, st)); }
+  normed = applied && next_here;
+  fin_done = applied && model_last;
   x = xout;
   return HS_OK;
 }
@@ -614,9 +658,11 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
       launch_wait(s.flag_x(), ep, s.err(), st);
       x = reinterpret_cast<bf16*>(s.comm + g->cl.x_in);
     }
+    bool normed = false, fin_done = false;
     for (int l = s.lb; l < s.le; ++l) {
       HS_CUDA(cudaStreamWaitEvent(st, s.ev_layer[l], 0));
-      HS_TRY(run_layer(g, s, l, x, m));
+      if (l + 1 == c.n_layers && s.le == c.n_layers) HS_CUDA(cudaStreamWaitEvent(st, s.ev_final, 0));
+      HS_TRY(run_layer(g, s, l, x, m, normed, fin_done));
     }
     if (k != last) {
       Stage& nx = g->st[g->active[ai + 1]];
@@ -625,14 +671,14 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
     } else {
       if (s.le == c.n_layers) HS_CUDA(cudaStreamWaitEvent(st, s.ev_final, 0));
       const int* d_last = reinterpret_cast<const int*>(s.d_meta + m.o_last);
-      {
+      if (!fin_done) {
         ProfScope ps(g, s, PK_RMSNORM, dec, 4.0 * m.n * c.hidden, 0);
         launch_rmsnorm(x, d_last, reinterpret_cast<const bf16*>(s.wptr(g->hdr.final_off + g->hdr.t_final_norm)),
                        s.fin, m.n, c.hidden, c.rms_eps, st);
       }
       GemmArgs a{};
       a.A = &s.lm; a.B = s.b_fin; a.M = c.vocab; a.N = m.n; a.K = c.hidden; a.epi = EPI_F32; a.out = s.logits;
-      a.ldo = c.vocab; a.workspace = s.ws; a.workspace_bytes = kWorkspace;
+      a.ldo = c.vocab; a.workspace = s.ws; a.workspace_bytes = kWorkspace; a.counters = s.ctr;
       {
         ProfScope ps(g, s, PK_LM_HEAD, dec, 2.0 * c.vocab * c.hidden + 2.0 * m.n * c.hidden + 4.0 * m.n * c.vocab,
                      2.0 * c.vocab * m.n * c.hidden);
@@ -817,51 +863,49 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
     cudaSetDevice(T.device);
     // the target must have its own slice resident before it takes over
     HS_CUDA(cudaStreamSynchronize(T.copy));
-    cudaStream_t s1 = T.copy, s2 = T.comp;
+    cudaStream_t s2 = T.comp;
     cudaEvent_t e0, e1, e2;
     HS_CUDA(cudaEventCreate(&e0));
     HS_CUDA(cudaEventCreate(&e1));
     HS_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
-    HS_CUDA(cudaEventRecord(e0, s1));
-    HS_CUDA(cudaStreamWaitEvent(s2, e0, 0));
-    // 2. KV blocks of every live sequence for the layers the target lacks: block-table driven
-    //    gather, pulled over NVLink by the target's SMs ("collect these blocks from all
-    //    workers with a gather operation")
-    std::vector<uint64_t> src, dst;
+    // 2. one copy list, pulled over NVLink by the target's SMs (16-byte loads, many in flight):
+    //    (a) the weight regions the target lacks (each owner's stage slice), (b) the used KV
+    //    blocks of every live sequence for those layers, placed at the same block ids ("collect
+    //    these blocks from all workers with a gather operation ... placed at different layers,
+    //    according to which worker it comes from")
+    const uint64_t piece = 64ull << 10;
+    std::vector<CopyDesc> list;
+    auto add = [&](uint64_t src, uint64_t dst, uint64_t bytes) {
+      for (uint64_t o = 0; o < bytes; o += piece) list.push_back({src + o, dst + o, std::min(piece, bytes - o)});
+    };
     for (int k : g->active) {
       if (k == tgt) continue;
       Stage& S = g->st[k];
       HS_TRY(open_peer_memory(g, S));
-      for (int l = S.lb; l < S.le; ++l)
-        for (auto& kvp : g->seqs)
-          for (int b : kvp.second.blocks) {
-            src.push_back(reinterpret_cast<uint64_t>(S.kv_pool(l, g->kv_layer_bytes)) + (uint64_t)b * g->kv_block_bytes);
-            dst.push_back(reinterpret_cast<uint64_t>(T.kv_pool(l, g->kv_layer_bytes)) + (uint64_t)b * g->kv_block_bytes);
-          }
+      add(reinterpret_cast<uint64_t>(S.arena + (S.slice_begin - S.arena_off0)), reinterpret_cast<uint64_t>(T.wptr(S.slice_begin)),
+          S.slice_end - S.slice_begin);
+      stats.weight_bytes += g->plan.stage_bytes[k];
     }
-    uint64_t* d_ptrs = nullptr;
-    if (!src.empty()) {
-      HS_CUDA(cudaMalloc(&d_ptrs, src.size() * 16));
-      HS_CUDA(cudaMemcpy(d_ptrs, src.data(), src.size() * 8, cudaMemcpyHostToDevice));
-      HS_CUDA(cudaMemcpy(d_ptrs + src.size(), dst.data(), dst.size() * 8, cudaMemcpyHostToDevice));
-      launch_span_copy(d_ptrs, d_ptrs + src.size(), (int)src.size(), g->kv_block_bytes, s2);
-    }
-    stats.kv_bytes = (uint64_t)src.size() * g->kv_block_bytes;
-    // 3. weight regions the target lacks: copy-engine pull from each owner's arena
     for (int k : g->active) {
       if (k == tgt) continue;
       Stage& S = g->st[k];
-      const uint64_t b = S.slice_begin, e = S.slice_end;
-      const uint64_t chunk = 256ull << 20;
-      for (uint64_t o = b; o < e; o += chunk) {
-        const uint64_t n = std::min(chunk, e - o);
-        HS_CUDA(cudaMemcpyAsync(T.wptr(o), S.arena + (o - S.arena_off0), n, cudaMemcpyDefault, s1));
-      }
-      stats.weight_bytes += g->plan.stage_bytes[k];
+      for (int l = S.lb; l < S.le; ++l)
+        for (auto& kvp : g->seqs)
+          for (int b : kvp.second.blocks) {
+            add(reinterpret_cast<uint64_t>(S.kv_pool(l, g->kv_layer_bytes)) + (uint64_t)b * g->kv_block_bytes,
+                reinterpret_cast<uint64_t>(T.kv_pool(l, g->kv_layer_bytes)) + (uint64_t)b * g->kv_block_bytes,
+                g->kv_block_bytes);
+            stats.kv_bytes += g->kv_block_bytes;
+          }
     }
-    HS_CUDA(cudaEventRecord(e2, s2));
-    HS_CUDA(cudaStreamWaitEvent(s1, e2, 0));
-    HS_CUDA(cudaEventRecord(e1, s1));
+    CopyDesc* d_list = nullptr;
+    if (!list.empty()) {
+      HS_CUDA(cudaMalloc(&d_list, list.size() * sizeof(CopyDesc)));
+      HS_CUDA(cudaMemcpy(d_list, list.data(), list.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+    }
+    HS_CUDA(cudaEventRecord(e0, s2));
+    launch_copy_list(d_list, (int)list.size(), 8 * num_sms(T.device), s2);
+    HS_CUDA(cudaEventRecord(e1, s2));
     HS_CUDA(cudaEventSynchronize(e1));
     float ms = 0;
     HS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
@@ -869,7 +913,7 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaEventDestroy(e2);
-    if (d_ptrs) cudaFree(d_ptrs);
+    if (d_list) cudaFree(d_list);
     // 4. rebind the target to every layer (maps already exist for a full-memory arena)
     T.lb = 0;
     T.le = c.n_layers;

@@ -22,8 +22,18 @@ extern "C" hs_status hs_k_gemm(const void* W, int32_t M, int32_t K, const void* 
   GemmArgs g{};
   g.A = &a; g.B = b; g.M = M; g.N = N; g.K = K; g.epi = epi; g.out = out; g.ldo = ldo;
   g.resid = reinterpret_cast<const bf16*>(resid); g.ldr = ldr;
-  g.workspace = reinterpret_cast<float*>(ws); g.workspace_bytes = ws ? ws_bytes : 0;
-  return gemm(g, reinterpret_cast<cudaStream_t>(stream));
+  // the first 64 KiB of the workspace hold the stream-K arrival counters (zeroed here)
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  if (ws && ws_bytes > (1u << 20)) {
+    HS_CUDA(cudaMemsetAsync(ws, 0, 65536, st));
+    g.counters = reinterpret_cast<unsigned*>(ws);
+    g.workspace = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + 65536);
+    g.workspace_bytes = ws_bytes - 65536;
+  } else {
+    g.workspace = reinterpret_cast<float*>(ws);
+    g.workspace_bytes = ws ? ws_bytes : 0;
+  }
+  return gemm(g, st);
 }
 
 extern "C" hs_status hs_k_rmsnorm(const void* x, const int32_t* rows, const void* w, void* y, int32_t T, int32_t H,
@@ -52,10 +62,20 @@ extern "C" hs_status hs_k_attention(const void* q, const void* pool, const int32
   static_assert(sizeof(SeqDesc) == 16, "SeqDesc layout");
   auto st = reinterpret_cast<cudaStream_t>(stream);
   const SeqDesc* sd = reinterpret_cast<const SeqDesc*>(seqs);
-  if (decode)
+  if (decode) {
+    // per-device zeroed arrival counters for the split merge (self-resetting)
+    static unsigned* ctr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!ctr[dev]) {
+      HS_CUDA(cudaMalloc(&ctr[dev], 1 << 20));
+      HS_CUDA(cudaMemset(ctr[dev], 0, 1 << 20));
+    }
+    if ((size_t)n * nh * 4 > (1u << 20)) HS_FAIL(HS_E_INVAL, "too many (seq, head) pairs");
     launch_attn_decode(reinterpret_cast<const bf16*>(q), reinterpret_cast<const bf16*>(pool), sd, n, max_ctx, tables,
                        max_blocks, reinterpret_cast<bf16*>(o), nh, d, reinterpret_cast<float*>(ws),
-                       attn_decode_splits(max_ctx), st);
+                       attn_decode_splits(max_ctx), ctr[dev], st);
+  }
   else
     launch_attn_prefill(reinterpret_cast<const bf16*>(q), reinterpret_cast<const bf16*>(pool), sd, n, max_nq, tables,
                         max_blocks, reinterpret_cast<bf16*>(o), nh, d, st);

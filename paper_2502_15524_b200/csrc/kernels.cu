@@ -254,134 +254,151 @@ void launch_attn_prefill(const bf16* q, const bf16* pool, const SeqDesc* seqs, i
   else attn_prefill_kernel<64><<<grid, 128, 0, st>>>(q, pool, seqs, tables, max_blocks, o, nh);
 }
 
-// Decode: CTA = (head, seq, split); warp w takes keys start + w, start + w + 4, ...
+// Decode: CTA = (head, seq, split of DEC_KC = 64 keys).  The split's 4 block ids are read
+// first, then every K/V row of the split is issued as 16-byte loads into registers at once
+// (memory-level parallelism, no dependent per-key chain) and staged in shared memory;
+// scores with 2 threads per key, block softmax, P.V with one thread per output dimension.
+// The CTA that finishes a (seq, head) last merges the splits in split order (deterministic).
+constexpr int DEC_KC = 64;
+
 template <int D>
 __global__ void __launch_bounds__(128) attn_decode_kernel(
     const bf16* __restrict__ q, const bf16* __restrict__ pool, const SeqDesc* __restrict__ seqs,
     const int* __restrict__ tables, int max_blocks, bf16* __restrict__ o, int nh, float* __restrict__ ws,
-    int splits, int chunk) {
-  constexpr int E = D / 32;
-  __shared__ float sm_m[4], sm_l[4];
-  __shared__ float sm_acc[4][D];
+    int splits, unsigned* __restrict__ ctr) {
+  __shared__ __align__(16) bf16 Ks[DEC_KC][D];
+  __shared__ __align__(16) bf16 Vs[DEC_KC][D];
+  __shared__ float qs[D];
+  __shared__ float ps[DEC_KC];
+  __shared__ float red[8];
+  __shared__ float part[128];
+  __shared__ int blk[DEC_KC / 16];
+  __shared__ int is_last;
   const int head = blockIdx.x, si = blockIdx.y, sp = blockIdx.z;
   const SeqDesc s = seqs[si];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tid = threadIdx.x;
   const int H = nh * D;
   const int n_keys = s.pos0 + 1;
-  const int k0 = sp * chunk, k1 = min(n_keys, k0 + chunk);
-  const float scale = 1.4426950408889634f / sqrtf((float)D);
-  float qv[E], acc[E], m = -INFINITY, l = 0.f;
-  load_lane<D>(q + (size_t)s.q_start * H + head * D + lane * E, qv);
+  const int k0 = sp * DEC_KC;
+  const int nk = min(DEC_KC, n_keys - k0);
+  float* w = ws + (((size_t)si * nh + head) * splits + sp) * (D + 2);
+  float mx = -INFINITY, sum = 0.f, ov = 0.f;
+  if (nk > 0) {
+    const int* tab = tables + (size_t)s.table * max_blocks;
+    if (tid < DEC_KC / 16) blk[tid] = (k0 + tid * 16 < n_keys) ? tab[(k0 >> 4) + tid] : 0;
+    const float scale = 1.4426950408889634f / sqrtf((float)D);
+    for (int e = tid; e < D; e += 128) qs[e] = __bfloat162float(q[(size_t)s.q_start * H + head * D + e]) * scale;
+    __syncthreads();
+    constexpr int RU4 = D / 8;                    // 16-byte units per row
+    constexpr int PER = DEC_KC * RU4 / 128;       // units per thread per matrix
+    const size_t vstride = (size_t)nh * 16 * D;
+    uint4 kr[PER], vr[PER];
 #pragma unroll
-  for (int e = 0; e < E; ++e) { qv[e] *= scale; acc[e] = 0.f; }
-  const int* tab = tables + (size_t)s.table * max_blocks;
-  const size_t vstride = (size_t)nh * 16 * D;
-  int j = k0 + warp;
-  // two keys per iteration to keep two K/V row loads in flight per warp
-  for (; j + 4 < k1; j += 8) {
-    const size_t b0 = ((((size_t)tab[j >> 4] * 2) * nh + head) * 16 + (j & 15)) * D + lane * E;
-    const int j2 = j + 4;
-    const size_t b1 = ((((size_t)tab[j2 >> 4] * 2) * nh + head) * 16 + (j2 & 15)) * D + lane * E;
-    float ka[E], va[E], kb[E], vb[E];
-    load_lane<D>(pool + b0, ka);
-    load_lane<D>(pool + b0 + vstride, va);
-    load_lane<D>(pool + b1, kb);
-    load_lane<D>(pool + b1 + vstride, vb);
-    float pa = 0.f, pb = 0.f;
-#pragma unroll
-    for (int e = 0; e < E; ++e) { pa += qv[e] * ka[e]; pb += qv[e] * kb[e]; }
-    pa = warp_sum(pa);
-    pb = warp_sum(pb);
-    const float mn = fmaxf(m, fmaxf(pa, pb));
-    const float corr = exp2f(m - mn), ea = exp2f(pa - mn), eb = exp2f(pb - mn);
-    l = l * corr + ea + eb;
-#pragma unroll
-    for (int e = 0; e < E; ++e) acc[e] = acc[e] * corr + ea * va[e] + eb * vb[e];
-    m = mn;
-  }
-  for (; j < k1; j += 4) {
-    const size_t b0 = ((((size_t)tab[j >> 4] * 2) * nh + head) * 16 + (j & 15)) * D + lane * E;
-    float ka[E], va[E];
-    load_lane<D>(pool + b0, ka);
-    load_lane<D>(pool + b0 + vstride, va);
-    float pa = 0.f;
-#pragma unroll
-    for (int e = 0; e < E; ++e) pa += qv[e] * ka[e];
-    pa = warp_sum(pa);
-    const float mn = fmaxf(m, pa);
-    const float corr = exp2f(m - mn), ea = exp2f(pa - mn);
-    l = l * corr + ea;
-#pragma unroll
-    for (int e = 0; e < E; ++e) acc[e] = acc[e] * corr + ea * va[e];
-    m = mn;
-  }
-  // combine the 4 warps (fixed order)
-  if (lane == 0) { sm_m[warp] = m; sm_l[warp] = l; }
-#pragma unroll
-  for (int e = 0; e < E; ++e) sm_acc[warp][lane * E + e] = acc[e];
-  __syncthreads();
-  if (warp == 0) {
-    float M = fmaxf(fmaxf(sm_m[0], sm_m[1]), fmaxf(sm_m[2], sm_m[3]));
-    float L = 0.f, A[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) A[e] = 0.f;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const float f = sm_m[w] == -INFINITY ? 0.f : exp2f(sm_m[w] - M);
-      L += sm_l[w] * f;
-#pragma unroll
-      for (int e = 0; e < E; ++e) A[e] += sm_acc[w][lane * E + e] * f;
+    for (int r = 0; r < PER; ++r) {
+      const int idx = tid + r * 128, jj = idx / RU4, u = idx % RU4;
+      if (jj < nk) {
+        const size_t base = ((((size_t)blk[jj >> 4] * 2) * nh + head) * 16 + (jj & 15)) * D;
+        kr[r] = __ldcs(reinterpret_cast<const uint4*>(pool + base) + u);
+        vr[r] = __ldcs(reinterpret_cast<const uint4*>(pool + base + vstride) + u);
+      }
     }
-    if (splits == 1) {
-      float r[E];
 #pragma unroll
-      for (int e = 0; e < E; ++e) r[e] = A[e] / L;
-      store_lane<D>(o + (size_t)s.q_start * H + head * D + lane * E, r);
+    for (int r = 0; r < PER; ++r) {
+      const int idx = tid + r * 128, jj = idx / RU4, u = idx % RU4;
+      if (jj < nk) {
+        reinterpret_cast<uint4*>(&Ks[jj][0])[u] = kr[r];
+        reinterpret_cast<uint4*>(&Vs[jj][0])[u] = vr[r];
+      }
+    }
+    __syncthreads();
+    {  // scores: thread pair per key
+      const int jj = tid >> 1, hf = tid & 1;
+      float acc = 0.f;
+      if (jj < nk) {
+        const __nv_bfloat162* kk2 = reinterpret_cast<const __nv_bfloat162*>(&Ks[jj][hf * (D / 2)]);
+#pragma unroll 8
+        for (int e = 0; e < D / 4; ++e) {
+          const float2 kk = __bfloat1622float2(kk2[e]);
+          acc += qs[hf * (D / 2) + 2 * e] * kk.x + qs[hf * (D / 2) + 2 * e + 1] * kk.y;
+        }
+      }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      if (hf == 0) ps[jj] = jj < nk ? acc : -INFINITY;
+    }
+    __syncthreads();
+    {
+      const float v0 = tid < DEC_KC ? ps[tid] : -INFINITY;
+      float m = v0;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+      if ((tid & 31) == 0) red[tid >> 5] = m;
+      __syncthreads();
+      mx = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+      const float pr = tid < nk ? exp2f(v0 - mx) : 0.f;
+      __syncthreads();
+      if (tid < DEC_KC) ps[tid] = pr;
+      float t = pr;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+      if ((tid & 31) == 0) red[4 + (tid >> 5)] = t;
+      __syncthreads();
+      sum = (red[4] + red[5]) + (red[6] + red[7]);
+    }
+    if constexpr (D == 128) {
+#pragma unroll 8
+      for (int jj = 0; jj < nk; ++jj) ov += ps[jj] * __bfloat162float(Vs[jj][tid]);
     } else {
-      float* w = ws + (((size_t)si * nh + head) * splits + sp) * (D + 2);
-      if (lane == 0) { w[0] = M; w[1] = L; }
-#pragma unroll
-      for (int e = 0; e < E; ++e) w[2 + lane * E + e] = A[e];
+      const int e = tid & (D - 1), hl = tid / D;
+      float a = 0.f;
+      for (int jj = hl; jj < nk; jj += 2) a += ps[jj] * __bfloat162float(Vs[jj][e]);
+      part[tid] = a;
+      __syncthreads();
+      ov = tid < D ? part[tid] + part[tid + D] : 0.f;
     }
   }
-}
-
-template <int D>
-__global__ void attn_decode_combine(const float* __restrict__ ws, const SeqDesc* __restrict__ seqs,
-                                    bf16* __restrict__ o, int nh, int splits) {
-  const int head = blockIdx.x, si = blockIdx.y;
-  const int e = threadIdx.x;  // D threads
-  const float* w = ws + ((size_t)si * nh + head) * splits * (D + 2);
-  float M = -INFINITY;
-  for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, w[sp * (D + 2)]);
-  float L = 0.f, A = 0.f;
-  for (int sp = 0; sp < splits; ++sp) {
-    const float ms = w[sp * (D + 2)];
-    const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
-    L += w[sp * (D + 2) + 1] * f;
-    A += w[sp * (D + 2) + 2 + e] * f;
+  if (splits == 1) {
+    if (tid < D) o[(size_t)s.q_start * H + head * D + tid] = __float2bfloat16_rn(ov / sum);
+    return;
   }
-  o[(size_t)seqs[si].q_start * nh * D + head * D + e] = __float2bfloat16_rn(A / L);
+  if (tid < D) {
+    if (tid == 0) { w[0] = mx; w[1] = sum; }
+    w[2 + tid] = ov;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    unsigned* c = ctr + (size_t)si * nh + head;
+    const unsigned old = atomicAdd(c, 1u);
+    is_last = old == (unsigned)(splits - 1);
+    if (is_last) *c = 0;
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  if (tid < D) {  // merge the splits in split order
+    const float* w0 = ws + ((size_t)si * nh + head) * splits * (D + 2);
+    float M = -INFINITY;
+    for (int k = 0; k < splits; ++k) M = fmaxf(M, __ldcg(w0 + k * (D + 2)));
+    float L = 0.f, A = 0.f;
+    for (int k = 0; k < splits; ++k) {
+      const float ms = __ldcg(w0 + k * (D + 2));
+      const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
+      L += __ldcg(w0 + k * (D + 2) + 1) * f;
+      A += __ldcg(w0 + k * (D + 2) + 2 + tid) * f;
+    }
+    o[(size_t)s.q_start * H + head * D + tid] = __float2bfloat16_rn(A / L);
+  }
 }
 
-int attn_decode_splits(int max_ctx) {
-  int s = (max_ctx + 127) / 128;
-  return s < 1 ? 1 : (s > 16 ? 16 : s);
-}
+int attn_decode_splits(int max_ctx) { return (max_ctx + DEC_KC - 1) / DEC_KC; }
 
 void launch_attn_decode(const bf16* q, const bf16* pool, const SeqDesc* seqs, int n_seqs, int max_ctx,
                         const int* tables, int max_blocks, bf16* o, int nh, int d, float* ws, int splits,
-                        cudaStream_t st) {
-  count_launch(splits > 1 ? 2 : 1);
-  const int chunk = (max_ctx + splits - 1) / splits;
+                        unsigned* ctr, cudaStream_t st) {
+  count_launch();
   dim3 grid(nh, n_seqs, splits);
-  if (d == 128) {
-    attn_decode_kernel<128><<<grid, 128, 0, st>>>(q, pool, seqs, tables, max_blocks, o, nh, ws, splits, chunk);
-    if (splits > 1) attn_decode_combine<128><<<dim3(nh, n_seqs), 128, 0, st>>>(ws, seqs, o, nh, splits);
-  } else {
-    attn_decode_kernel<64><<<grid, 128, 0, st>>>(q, pool, seqs, tables, max_blocks, o, nh, ws, splits, chunk);
-    if (splits > 1) attn_decode_combine<64><<<dim3(nh, n_seqs), 64, 0, st>>>(ws, seqs, o, nh, splits);
-  }
+  if (d == 128) attn_decode_kernel<128><<<grid, 128, 0, st>>>(q, pool, seqs, tables, max_blocks, o, nh, ws, splits, ctr);
+  else attn_decode_kernel<64><<<grid, 128, 0, st>>>(q, pool, seqs, tables, max_blocks, o, nh, ws, splits, ctr);
 }
 
 // ------------------------------------------------------------------ argmax (a15) ---------
@@ -488,6 +505,28 @@ __global__ void __launch_bounds__(256) span_copy_kernel(const uint64_t* __restri
   for (; i < e; i += 256) d[i] = s[i];
 }
 
+// Copy list: descriptors {src, dst, bytes} (bytes % 16 == 0, <= 64 KiB each), persistent
+// grid-stride over descriptors; 4 x 16-byte loads in flight per thread before the stores.
+__global__ void __launch_bounds__(256) copy_list_kernel(const CopyDesc* __restrict__ d, int n) {
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const uint4* s = reinterpret_cast<const uint4*>(d[i].src);
+    uint4* o = reinterpret_cast<uint4*>(d[i].dst);
+    const int n16 = (int)(d[i].bytes >> 4);
+    int j = threadIdx.x;
+    for (; j + 768 < n16; j += 1024) {
+      uint4 a = s[j], b = s[j + 256], c = s[j + 512], e = s[j + 768];
+      o[j] = a; o[j + 256] = b; o[j + 512] = c; o[j + 768] = e;
+    }
+    for (; j < n16; j += 256) o[j] = s[j];
+  }
+}
+
+void launch_copy_list(const CopyDesc* d, int n, int ctas, cudaStream_t st) {
+  if (n <= 0) return;
+  count_launch();
+  copy_list_kernel<<<ctas < n ? ctas : n, 256, 0, st>>>(d, n);
+}
+
 void launch_span_copy(const uint64_t* src, const uint64_t* dst, int n, uint64_t span_bytes, cudaStream_t st) {
   if (n <= 0) return;
   count_launch();
@@ -509,12 +548,11 @@ void warm_kernels() {
   cudaFuncGetAttributes(&a, attn_prefill_kernel<128>);
   cudaFuncGetAttributes(&a, attn_decode_kernel<64>);
   cudaFuncGetAttributes(&a, attn_decode_kernel<128>);
-  cudaFuncGetAttributes(&a, attn_decode_combine<64>);
-  cudaFuncGetAttributes(&a, attn_decode_combine<128>);
   cudaFuncGetAttributes(&a, argmax_kernel);
   cudaFuncGetAttributes(&a, send_kernel);
   cudaFuncGetAttributes(&a, wait_kernel);
   cudaFuncGetAttributes(&a, span_copy_kernel);
+  cudaFuncGetAttributes(&a, copy_list_kernel);
 }
 
 }  // namespace hs

@@ -30,11 +30,12 @@ void launch_attn_prefill(const bf16* q, const bf16* pool, const SeqDesc* seqs, i
                          int max_nq, const int* tables, int max_blocks, bf16* o, int n_heads,
                          int head_dim, cudaStream_t st);
 
-// Decode attention (one query per sequence) with deterministic split-KV.
-// ws: n_seqs * n_heads * kv_splits * (head_dim + 2) floats.
+// Decode attention (one query per sequence) with deterministic split-KV (64 keys per split).
+// ws: n_seqs * n_heads * kv_splits * (head_dim + 2) floats; ctr: n_seqs * n_heads zeroed
+// arrival counters (self-resetting).
 void launch_attn_decode(const bf16* q, const bf16* pool, const SeqDesc* seqs, int n_seqs,
                         int max_ctx, const int* tables, int max_blocks, bf16* o, int n_heads,
-                        int head_dim, float* ws, int kv_splits, cudaStream_t st);
+                        int head_dim, float* ws, int kv_splits, unsigned* ctr, cudaStream_t st);
 int attn_decode_splits(int max_ctx);
 
 // tokens[i] = argmax_v logits[i][v], ties -> lowest id (a15)
@@ -52,5 +53,11 @@ void launch_wait(const unsigned* flag, unsigned epoch, int* err, cudaStream_t st
 // be peer mappings).  Bit-exact byte copy with 16-byte accesses.
 void launch_span_copy(const uint64_t* src, const uint64_t* dst, int n, uint64_t span_bytes,
                       cudaStream_t st);
+
+// Consolidation copy list (weights + KV blocks in one launch), pulled by the launching GPU.
+struct CopyDesc {
+  uint64_t src, dst, bytes;
+};
+void launch_copy_list(const CopyDesc* d, int n, int ctas, cudaStream_t st);
 
 }  // namespace hs

@@ -49,6 +49,7 @@ def check_bf16(gpu_bits, ref_vals, max_frac=0.02, scale=None):
 GEMM_CASES = [  # (M, K, N)
     (256, 256, 1), (256, 256, 16), (384, 256, 37), (256, 512, 64), (512, 256, 130),
     (768, 256, 300), (256, 768, 1100), (128, 64, 5),
+    (2048, 4096, 7), (1536, 2048, 64), (4096, 11008, 3),  # stream-K (decode) path when ws is given
 ]
 
 
@@ -180,7 +181,7 @@ def test_attention_paged(nh, d, decode):
         t0 += n
     q = np.concatenate(qs).reshape(t0, nh * d)
     o = torch.empty((t0, nh * d), dtype=torch.bfloat16, device="cuda")
-    ws = torch.empty(len(lens) * nh * 16 * (d + 2), dtype=torch.float32, device="cuda")
+    ws = torch.empty(len(lens) * nh * 64 * (d + 2), dtype=torch.float32, device="cuda")
     hs.k_attention(dev_bf16(q), dev_bf16(pool), torch.tensor(seqs, dtype=torch.int32, device="cuda"),
                    max(lens), max(ctxs), torch.from_numpy(tables).cuda(), o, nh, d, decode, ws)
     torch.cuda.synchronize()
