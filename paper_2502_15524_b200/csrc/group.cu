@@ -290,8 +290,11 @@ static hs_status setup_owned_stage(hs_group* g, int k) {
   }
   s.meta_bytes = (size_t)T * 12 + (size_t)S * (8 + sizeof(SeqDesc) + (size_t)g->max_blocks * 4) + 1024;
   HS_ALLOC(s.d_meta, s.meta_bytes);
-  HS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.h_meta), s.meta_bytes, cudaHostAllocDefault));
-  HS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.h_out), (size_t)S * 4 + 64, cudaHostAllocDefault));
+  // mapped pinned staging: the SMs read call metadata / write tokens directly (see
+  // launch_small_copy), so nothing small queues behind the weight stream on the copy engines
+  HS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.h_meta), s.meta_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  HS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s.h_out), align_up((size_t)S * 4 + 64, 16),
+                        cudaHostAllocMapped | cudaHostAllocPortable));
   int lo = 0, hi = 0;
   HS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   s.owns_streams = true;
@@ -638,7 +641,7 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
       sd[i].table = i;
     }
     HS_CUDA(cudaEventRecord(s.ev_c0, st));
-    HS_CUDA(cudaMemcpyAsync(s.d_meta, hm, m.bytes, cudaMemcpyHostToDevice, st));
+    launch_small_copy(hm, s.d_meta, m.bytes, st);
     const int* d_tok = reinterpret_cast<const int*>(s.d_meta + m.o_tok);
     const bool dec = m.decode;
     bf16* x = nullptr;
@@ -661,7 +664,7 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
     bool normed = false, fin_done = false;
     for (int l = s.lb; l < s.le; ++l) {
       HS_CUDA(cudaStreamWaitEvent(st, s.ev_layer[l], 0));
-      if (l + 1 == c.n_layers && s.le == c.n_layers) HS_CUDA(cudaStreamWaitEvent(st, s.ev_final, 0));
+      if (m.decode && l + 1 == c.n_layers) HS_CUDA(cudaStreamWaitEvent(st, s.ev_final, 0));  // fused final norm
       HS_TRY(run_layer(g, s, l, x, m, normed, fin_done));
     }
     if (k != last) {
@@ -696,15 +699,15 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
         Stage& d = g->st[kk];
         launch_send(s.d_tok_out, d.comm + g->cl.tok_in, tb, s.done(), d.flag_tok(), ep, 1, st);
       }
-      HS_CUDA(cudaMemcpyAsync(s.h_out, s.d_tok_out, (size_t)m.n * 4, cudaMemcpyDeviceToHost, st));
+      launch_small_copy(s.d_tok_out, s.h_out, align_up((uint64_t)m.n * 4, 16), st);
       if (out_logits)
         HS_CUDA(cudaMemcpyAsync(out_logits, s.logits, (size_t)m.n * c.vocab * 4, cudaMemcpyDeviceToHost, st));
     }
     if (k != last && g->spmd) {  // non-last SPMD ranks read the broadcast tokens
       launch_wait(s.flag_tok(), ep, s.err(), st);
-      HS_CUDA(cudaMemcpyAsync(s.h_out, s.comm + g->cl.tok_in, (size_t)m.n * 4, cudaMemcpyDeviceToHost, st));
+      launch_small_copy(s.comm + g->cl.tok_in, s.h_out, align_up((uint64_t)m.n * 4, 16), st);
     }
-    HS_CUDA(cudaMemcpyAsync(s.h_out + m.n, s.err(), 4, cudaMemcpyDeviceToHost, st));
+    launch_small_copy(s.comm, s.h_out + align_up((uint64_t)m.n, 4), 16, st);  // flags + err word
     HS_CUDA(cudaEventRecord(s.ev_c1, st));
     s.called = true;
   }
@@ -720,7 +723,7 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
       g->dead = true;
       HS_FAIL(HS_E_CUDA, "stage %d: %s", k, cudaGetErrorString(e));
     }
-    err |= s.h_out[m.n];
+    err |= s.h_out[align_up((uint64_t)m.n, 4) + CommLayout::ERR / 4];
     if (k == last || (g->spmd && !got)) {
       memcpy(out_tokens, s.h_out, (size_t)m.n * 4);
       got = true;

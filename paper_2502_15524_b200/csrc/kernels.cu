@@ -527,6 +527,23 @@ void launch_copy_list(const CopyDesc* d, int n, int ctas, cudaStream_t st) {
   copy_list_kernel<<<ctas < n ? ctas : n, 256, 0, st>>>(d, n);
 }
 
+// Small copies between mapped pinned host memory and device memory done by SMs, so they never
+// queue behind the multi-GB weight stream on the copy engines (a DMA H2D of call metadata on
+// the compute stream would wait for the whole load and serialise prefill after it).
+__global__ void __launch_bounds__(256) small_copy_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                         int n16) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += gridDim.x * blockDim.x) dst[i] = src[i];
+  __threadfence_system();
+}
+
+void launch_small_copy(const void* src, void* dst, uint64_t bytes, cudaStream_t st) {
+  const int n16 = (int)((bytes + 15) / 16);
+  if (n16 <= 0) return;
+  count_launch();
+  const int ctas = n16 > 4096 ? 16 : 1;
+  small_copy_kernel<<<ctas, 256, 0, st>>>(reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst), n16);
+}
+
 void launch_span_copy(const uint64_t* src, const uint64_t* dst, int n, uint64_t span_bytes, cudaStream_t st) {
   if (n <= 0) return;
   count_launch();
@@ -553,6 +570,7 @@ void warm_kernels() {
   cudaFuncGetAttributes(&a, wait_kernel);
   cudaFuncGetAttributes(&a, span_copy_kernel);
   cudaFuncGetAttributes(&a, copy_list_kernel);
+  cudaFuncGetAttributes(&a, small_copy_kernel);
 }
 
 }  // namespace hs

@@ -54,6 +54,10 @@ void launch_wait(const unsigned* flag, unsigned epoch, int* err, cudaStream_t st
 void launch_span_copy(const uint64_t* src, const uint64_t* dst, int n, uint64_t span_bytes,
                       cudaStream_t st);
 
+// 16-byte-granular copy by SMs (src / dst may be mapped pinned host memory): call metadata
+// in, tokens out, without touching the copy engines that stream the weights.
+void launch_small_copy(const void* src, void* dst, uint64_t bytes, cudaStream_t st);
+
 // Consolidation copy list (weights + KV blocks in one launch), pulled by the launching GPU.
 struct CopyDesc {
   uint64_t src, dst, bytes;
