@@ -31,7 +31,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "cold-start TTFT (s) and decode tok/s at PP=1/2/4/8; consolidation GB/s vs NVLink"
 PCIE_H2D_GBS = 55.6        # measured per GPU in isolation (profiles/r01_links_measured.json)
-PCIE_H2D_AGG_CAP = 115.5   # measured 4-GPU concurrent aggregate (host-side cap)
+# (a first probe that read ONE shared pinned buffer from 4 GPUs saw 115 GB/s in total; with a
+# buffer per GPU, as here, PP=4 loads reach 209 GB/s: links are independent, so the
+# aggregate peak is N x the isolated per-link figure)
 NVLINK_GBS = 900.0         # nominal per direction per GPU (north star); measured P2P 770
 
 
@@ -272,7 +274,7 @@ def run_ours(args):
     pre_gemm = [v for k, v in prof.items() if k.startswith("gemm_") and k.endswith(".prefill")]
     out = None
     if rank == 0:
-        agg_link = PCIE_H2D_GBS * pp if pp <= 2 else min(PCIE_H2D_GBS * pp, PCIE_H2D_AGG_CAP * (pp / 4))
+        agg_link = PCIE_H2D_GBS * pp
         load_gbs = loaded / (load_ms / 1e3) / 1e9
         out = {
             "metric": METRIC, "value": round(ttft_dev, 5), "unit": "s", "n_gpus": world, "steps": args.steps,
@@ -292,9 +294,7 @@ def run_ours(args):
             "load": {"bytes_per_stage_max": max(pd["stage_bytes"]), "bytes_total": int(loaded),
                      "stage_load_ms_max": round(load_ms, 2), "achieved_gbs": round(load_gbs, 2),
                      "peak_gbs_isolated_sum": round(PCIE_H2D_GBS * pp, 1),
-                     "peak_gbs_measured_concurrent": round(agg_link, 1),
-                     "frac_of_isolated_sum": round(load_gbs / (PCIE_H2D_GBS * pp), 4),
-                     "frac_of_measured_concurrent": round(load_gbs / agg_link, 4)},
+                     "frac_of_isolated_sum": round(load_gbs / agg_link, 4)},
             "decode": {"tok_s_device": round(n_seqs * dsteps / dec_dev, 2), "tok_s_host": round(n_seqs * dsteps / dec_host, 2),
                        "hbm_roofline_tok_s": None},
             "roofline": roof,

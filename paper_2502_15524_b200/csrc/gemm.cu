@@ -358,10 +358,28 @@ __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.syn
 // stays bitwise equal to PP = 1 across the stage boundary).
 __device__ __noinline__ void row_norm128(const bf16* __restrict__ h, int M, const bf16* __restrict__ w,
                                          bf16* __restrict__ y, float eps, int tid, float* red, int bar_id) {
+  // 16-byte loads (8 values), all issued before use; fixed per-thread summation order
+  const int n8 = M >> 3;
+  const uint4* h4 = reinterpret_cast<const uint4*>(h);
+  constexpr int U = 8;  // up to 8 x 1024 values per thread-iteration batch
   float ss = 0.f;
-  for (int m = tid; m < M; m += 128) {
-    const float v = __bfloat162float(h[m]);
-    ss = fmaf(v, v, ss);
+  for (int c0 = 0; c0 < n8; c0 += U * 128) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + u * 128 + tid;
+      v[u] = c < n8 ? __ldcg(h4 + c) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(p2[k]);
+        ss = fmaf(f.x, f.x, ss);
+        ss = fmaf(f.y, f.y, ss);
+      }
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
@@ -369,7 +387,21 @@ __device__ __noinline__ void row_norm128(const bf16* __restrict__ h, int M, cons
   named_bar(bar_id, 128);
   const float tot = (red[0] + red[1]) + (red[2] + red[3]);
   const float rs = 1.0f / sqrtf(tot / (float)M + eps);
-  for (int m = tid; m < M; m += 128) y[m] = __float2bfloat16_rn(__bfloat162float(h[m]) * rs * __bfloat162float(w[m]));
+  const uint4* w4 = reinterpret_cast<const uint4*>(w);
+  uint4* y4 = reinterpret_cast<uint4*>(y);
+  for (int c = tid; c < n8; c += 128) {
+    const uint4 hv = __ldcg(h4 + c), wv = w4[c];
+    uint4 o;
+    const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&hv);
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&wv);
+    __nv_bfloat162* r = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 x = __bfloat1622float2(a[k]), g = __bfloat1622float2(b[k]);
+      r[k] = __floats2bfloat162_rn(x.x * rs * g.x, x.y * rs * g.y);
+    }
+    y4[c] = o;
+  }
   named_bar(bar_id, 128);
 }
 

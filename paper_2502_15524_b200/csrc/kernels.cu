@@ -164,85 +164,193 @@ __device__ __forceinline__ void store_lane(bf16* p, const float* v) {
   }
 }
 
-constexpr int PF_Q = 16;    // queries per CTA (4 warps x 4)
-constexpr int PF_KC = 64;   // keys staged per chunk
+// Prefill: flash-attention with bf16 tensor-core MMAs (m16n8k16, fp32 accumulation).
+// CTA = (64-query tile, head, sequence), 4 warps x 16 query rows.  Per 64-key chunk the K and V
+// rows are gathered from the paged pool into XOR-swizzled shared memory (conflict-free
+// ldmatrix), S = Q K^T and O += P V run on the tensor cores, the online softmax in fp32 with
+// exp2 (scores pre-scaled by log2(e)/sqrt(d)).  P is fed to the P.V MMA as a bf16 pair
+// P = P_hi + P_lo (two MMAs sharing the V fragments), so the probabilities keep ~16 bits
+// (the oracle's contract is fp32 probabilities; a single bf16 P would add 2^-9 relative error).
+constexpr int PF_Q = 64;
+constexpr int PF_KC = 64;
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ void mma_bf16_16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
 
 template <int D>
 __global__ void __launch_bounds__(128) attn_prefill_kernel(
     const bf16* __restrict__ q, const bf16* __restrict__ pool, const SeqDesc* __restrict__ seqs,
     const int* __restrict__ tables, int max_blocks, bf16* __restrict__ o, int nh) {
-  constexpr int E = D / 32;
-  __shared__ __align__(16) bf16 Ks[PF_KC][D];
-  __shared__ __align__(16) bf16 Vs[PF_KC][D];
+  constexpr int CH = D / 8;  // 16-byte chunks per row
+  constexpr int KS = D / 16; // k-steps over head_dim
+  __shared__ __align__(128) uint4 Ks[PF_KC * CH];
+  __shared__ __align__(128) uint4 Vs[PF_KC * CH];
   const SeqDesc s = seqs[blockIdx.z];
   const int head = blockIdx.y;
   const int qt0 = blockIdx.x * PF_Q;
   if (qt0 >= s.n_q) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tig = lane & 3;
   const int H = nh * D;
-  const float scale = 1.4426950408889634f / sqrtf((float)D);
-  float qv[4][E], acc[4][E], m[4], l[4];
-  int qpos[4];
+  const float sl2 = 1.4426950408889634f / sqrtf((float)D);
+  // Q fragments of this warp's 16 rows (rows beyond n_q read row n_q-1: results discarded)
+  const int r0 = qt0 + warp * 16 + g, r1 = r0 + 8;
+  const int qa = min(r0, s.n_q - 1), qb = min(r1, s.n_q - 1);
+  const uint32_t* q0p = reinterpret_cast<const uint32_t*>(q + (size_t)(s.q_start + qa) * H + head * D);
+  const uint32_t* q1p = reinterpret_cast<const uint32_t*>(q + (size_t)(s.q_start + qb) * H + head * D);
+  uint32_t qf[KS][4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int qi = qt0 + warp * 4 + j;
-    qpos[j] = qi < s.n_q ? s.pos0 + qi : -1;
-    if (qi < s.n_q) load_lane<D>(q + (size_t)(s.q_start + qi) * H + head * D + lane * E, qv[j]);
-    else
-#pragma unroll
-      for (int e = 0; e < E; ++e) qv[j][e] = 0.f;
-#pragma unroll
-    for (int e = 0; e < E; ++e) { qv[j][e] *= scale; acc[j][e] = 0.f; }
-    m[j] = -INFINITY;
-    l[j] = 0.f;
+  for (int ks = 0; ks < KS; ++ks) {
+    qf[ks][0] = q0p[ks * 8 + tig];
+    qf[ks][1] = q1p[ks * 8 + tig];
+    qf[ks][2] = q0p[ks * 8 + 4 + tig];
+    qf[ks][3] = q1p[ks * 8 + 4 + tig];
   }
+  const int pos_a = s.pos0 + r0, pos_b = s.pos0 + r1;
+  float acc[D / 8][4];
+#pragma unroll
+  for (int j = 0; j < D / 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+  float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
   const int n_keys = s.pos0 + min(qt0 + PF_Q, s.n_q);
   const int* tab = tables + (size_t)s.table * max_blocks;
-  constexpr int RU4 = D / 8;  // uint4 per row
+  const uint32_t ks_base = static_cast<uint32_t>(__cvta_generic_to_shared(Ks));
+  const uint32_t vs_base = static_cast<uint32_t>(__cvta_generic_to_shared(Vs));
+  const int warp_max_pos = s.pos0 + min(qt0 + warp * 16 + 15, s.n_q - 1);
   for (int kc = 0; kc < n_keys; kc += PF_KC) {
     __syncthreads();
     const int nk = min(PF_KC, n_keys - kc);
-    for (int idx = threadIdx.x; idx < nk * RU4; idx += 128) {
-      const int jj = idx / RU4, u = idx % RU4;
-      const int j = kc + jj;
-      const size_t blk = (size_t)tab[j >> 4];
-      const size_t base = (((blk * 2) * nh + head) * 16 + (j & 15)) * D;
-      reinterpret_cast<uint4*>(&Ks[jj][0])[u] = reinterpret_cast<const uint4*>(pool + base)[u];
-      reinterpret_cast<uint4*>(&Vs[jj][0])[u] =
-          reinterpret_cast<const uint4*>(pool + base + (size_t)nh * 16 * D)[u];
+    // gather K, V rows (256 B / 128 B each) into swizzled smem: chunk c of row r at c ^ (r & 7)
+    for (int idx = threadIdx.x; idx < PF_KC * CH; idx += 128) {
+      const int r = idx / CH, c = idx % CH;
+      uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
+      if (r < nk) {
+        const int j = kc + r;
+        const size_t base = ((((size_t)tab[j >> 4] * 2) * nh + head) * 16 + (j & 15)) * D;
+        kv = reinterpret_cast<const uint4*>(pool + base)[c];
+        vv = reinterpret_cast<const uint4*>(pool + base + (size_t)nh * 16 * D)[c];
+      }
+      Ks[r * CH + (c ^ (r & 7))] = kv;
+      Vs[r * CH + (c ^ (r & 7))] = vv;
     }
     __syncthreads();
-    for (int jj = 0; jj < nk; ++jj) {
-      const int j = kc + jj;
-      float kf[E], vf[E];
-      load_lane<D>(&Ks[jj][lane * E], kf);
-      load_lane<D>(&Vs[jj][lane * E], vf);
+    if (kc > warp_max_pos) continue;  // whole chunk in this warp's causal future
+    // S = Q K^T : 16 x 64 per warp (8 n-tiles of 8 keys)
+    float sc[8][4];
 #pragma unroll
-      for (int qq = 0; qq < 4; ++qq) {
-        if (j > qpos[qq]) continue;  // causal mask (warp-uniform)
-        float part = 0.f;
+    for (int j = 0; j < 8; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
 #pragma unroll
-        for (int e = 0; e < E; ++e) part += qv[qq][e] * kf[e];
-        const float sc = warp_sum(part);
-        const float mn = fmaxf(m[qq], sc);
-        const float corr = exp2f(m[qq] - mn), pr = exp2f(sc - mn);
-        l[qq] = l[qq] * corr + pr;
+    for (int j = 0; j < 8; ++j) {
+      const int row = j * 8 + (lane & 7);
 #pragma unroll
-        for (int e = 0; e < E; ++e) acc[qq][e] = acc[qq][e] * corr + pr * vf[e];
-        m[qq] = mn;
+      for (int ks = 0; ks < KS; ks += 2) {
+        const int c = 2 * ks + (lane >> 3);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(ks_base + (uint32_t)((row * CH + (c ^ (row & 7))) * 16), b0, b1, b2, b3);
+        mma_bf16_16816(sc[j], qf[ks], b0, b1);
+        mma_bf16_16816(sc[j], qf[ks + 1], b2, b3);
+      }
+    }
+    // causal mask, scaling, online softmax (rows g and g+8 of the warp tile)
+    float mx_a = m_a, mx_b = m_b;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int k0 = kc + j * 8 + 2 * tig;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int kp = k0 + e;
+        sc[j][e] = (kp <= pos_a && kp < kc + nk) ? sc[j][e] * sl2 : -INFINITY;
+        sc[j][2 + e] = (kp <= pos_b && kp < kc + nk) ? sc[j][2 + e] * sl2 : -INFINITY;
+        mx_a = fmaxf(mx_a, sc[j][e]);
+        mx_b = fmaxf(mx_b, sc[j][2 + e]);
+      }
+    }
+    mx_a = fmaxf(mx_a, __shfl_xor_sync(0xffffffffu, mx_a, 1));
+    mx_a = fmaxf(mx_a, __shfl_xor_sync(0xffffffffu, mx_a, 2));
+    mx_b = fmaxf(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, 1));
+    mx_b = fmaxf(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, 2));
+    const float ca = mx_a == -INFINITY ? 1.f : exp2f(m_a - mx_a);
+    const float cb = mx_b == -INFINITY ? 1.f : exp2f(m_b - mx_b);
+    m_a = mx_a;
+    m_b = mx_b;
+    float sa = 0.f, sb = 0.f;
+    uint32_t pf[4][4], pl[4][4];  // P (hi, lo) as A fragments: k-step kk covers n-tiles 2kk, 2kk+1
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float p0 = mx_a == -INFINITY ? 0.f : exp2f(sc[j][0] - mx_a);
+      const float p1 = mx_a == -INFINITY ? 0.f : exp2f(sc[j][1] - mx_a);
+      const float p2 = mx_b == -INFINITY ? 0.f : exp2f(sc[j][2] - mx_b);
+      const float p3 = mx_b == -INFINITY ? 0.f : exp2f(sc[j][3] - mx_b);
+      sa += p0 + p1;
+      sb += p2 + p3;
+      const __nv_bfloat162 h01 = __floats2bfloat162_rn(p0, p1), h23 = __floats2bfloat162_rn(p2, p3);
+      const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
+      pf[j >> 1][(j & 1) * 2 + 0] = *reinterpret_cast<const uint32_t*>(&h01);
+      pf[j >> 1][(j & 1) * 2 + 1] = *reinterpret_cast<const uint32_t*>(&h23);
+      pl[j >> 1][(j & 1) * 2 + 0] = pack_bf16(p0 - f01.x, p1 - f01.y);
+      pl[j >> 1][(j & 1) * 2 + 1] = pack_bf16(p2 - f23.x, p3 - f23.y);
+    }
+    l_a = l_a * ca + sa;
+    l_b = l_b * cb + sb;
+#pragma unroll
+    for (int j = 0; j < D / 8; ++j) {
+      acc[j][0] *= ca;
+      acc[j][1] *= ca;
+      acc[j][2] *= cb;
+      acc[j][3] *= cb;
+    }
+    // O += P V : V rows are keys (k), columns head dims (n) -> transposed ldmatrix
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int vrow = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+      for (int dd = 0; dd < D / 8; dd += 2) {
+        const int c = dd + (lane >> 4);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(vs_base + (uint32_t)((vrow * CH + (c ^ (vrow & 7))) * 16), b0, b1, b2, b3);
+        mma_bf16_16816(acc[dd], pf[kk], b0, b1);
+        mma_bf16_16816(acc[dd + 1], pf[kk], b2, b3);
+        mma_bf16_16816(acc[dd], pl[kk], b0, b1);
+        mma_bf16_16816(acc[dd + 1], pl[kk], b2, b3);
       }
     }
   }
+  // finalize: quad-reduce the row sums, normalise, store bf16
+  l_a += __shfl_xor_sync(0xffffffffu, l_a, 1);
+  l_a += __shfl_xor_sync(0xffffffffu, l_a, 2);
+  l_b += __shfl_xor_sync(0xffffffffu, l_b, 1);
+  l_b += __shfl_xor_sync(0xffffffffu, l_b, 2);
+  const float ia = 1.f / l_a, ib = 1.f / l_b;
+  if (r0 < s.n_q) {
+    uint32_t* oa = reinterpret_cast<uint32_t*>(o + (size_t)(s.q_start + r0) * H + head * D);
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int qi = qt0 + warp * 4 + j;
-    if (qi < s.n_q) {
-      float r[E];
-      const float inv = 1.0f / l[j];
+    for (int j = 0; j < D / 8; ++j) oa[j * 4 + tig] = pack_bf16(acc[j][0] * ia, acc[j][1] * ia);
+  }
+  if (r1 < s.n_q) {
+    uint32_t* ob = reinterpret_cast<uint32_t*>(o + (size_t)(s.q_start + r1) * H + head * D);
 #pragma unroll
-      for (int e = 0; e < E; ++e) r[e] = acc[j][e] * inv;
-      store_lane<D>(o + (size_t)(s.q_start + qi) * H + head * D + lane * E, r);
-    }
+    for (int j = 0; j < D / 8; ++j) ob[j * 4 + tig] = pack_bf16(acc[j][2] * ib, acc[j][3] * ib);
   }
 }
 

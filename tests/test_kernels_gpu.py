@@ -35,12 +35,13 @@ def ulp_diff(a_bits, b_bits):
     return np.abs(key(a_bits) - key(b_bits))
 
 
-def check_bf16(gpu_bits, ref_vals, max_frac=0.02, scale=None):
+def check_bf16(gpu_bits, ref_vals, max_frac=0.02, scale=None, rel=2.0 ** -20):
     """<= 1 bf16 ulp from the exactly rounded fp64 value, except where cancellation makes the
-    result tiny: there |gpu - ref| <= 2^-20 * scale (fp32 accumulation error of the terms)."""
+    result tiny: there |gpu - ref| <= rel * scale (accumulation error of the terms; 2^-20 for
+    an fp32 sum, 2^-16 for tensor-core attention with P split into two bf16 halves)."""
     d = ulp_diff(gpu_bits, bf16_bits(ref_vals))
     if scale is not None:
-        close = np.abs(bf16_value(gpu_bits) - ref_vals) <= 2.0 ** -20 * scale
+        close = np.abs(bf16_value(gpu_bits) - ref_vals) <= rel * scale
         d = np.where(close, np.minimum(d, 1), d)
     assert d.max() <= 1, f"max ulp diff {d.max()}"
     assert (d > 0).mean() <= max_frac, f"{(d > 0).mean():.4f} of elements differ by 1 ulp"
@@ -144,15 +145,18 @@ def test_rope_kv_write(nh, d):
         assert np.array_equal(P[blk, 1, :, off, :], qkv.reshape(T, 3, nh, d)[t, 2])
 
 
-def attention_ref(q, K, V, pos):
-    """Causal softmax attention (float64): q [n, nh, d] at positions pos over K, V [ctx, nh, d]."""
+def attention_ref(q, K, V, pos, want_scale=False):
+    """Causal softmax attention (float64): q [n, nh, d] at positions pos over K, V [ctx, nh, d].
+    With want_scale also returns sum_j p_j |v_j| (the magnitude of the terms)."""
     d = q.shape[-1]
     out = np.empty_like(q)
+    scale = np.empty_like(q)
     for i, p in enumerate(pos):
         sc = np.einsum("hd,khd->hk", q[i], K[: p + 1]) / np.sqrt(d)
         e = np.exp(sc - sc.max(-1, keepdims=True))
         out[i] = np.einsum("hk,khd->hd", e, V[: p + 1]) / e.sum(-1)[:, None]
-    return out
+        scale[i] = np.einsum("hk,khd->hd", e, np.abs(V[: p + 1])) / e.sum(-1)[:, None]
+    return (out, scale) if want_scale else out
 
 
 @pytest.mark.parametrize("nh,d", [(4, 64), (8, 128)])
@@ -175,7 +179,7 @@ def test_attention_paged(nh, d, decode):
             pool[tab[p // 16], 1, :, p % 16] = V[p]
         q = rand_bf16(rng, (n, nh, d))
         pos = np.arange(ctx - n, ctx)
-        outs_ref.append(attention_ref(bf16_value(q), bf16_value(K), bf16_value(V), pos))
+        outs_ref.append(attention_ref(bf16_value(q), bf16_value(K), bf16_value(V), pos, want_scale=True))
         qs.append(q)
         seqs.append([t0, n, ctx - n, i])
         t0 += n
@@ -185,7 +189,9 @@ def test_attention_paged(nh, d, decode):
     hs.k_attention(dev_bf16(q), dev_bf16(pool), torch.tensor(seqs, dtype=torch.int32, device="cuda"),
                    max(lens), max(ctxs), torch.from_numpy(tables).cuda(), o, nh, d, decode, ws)
     torch.cuda.synchronize()
-    check_bf16(host_bits(o), np.concatenate(outs_ref).reshape(t0, nh * d), max_frac=0.05)
+    ref = np.concatenate([r[0] for r in outs_ref]).reshape(t0, nh * d)
+    sc = np.concatenate([r[1] for r in outs_ref]).reshape(t0, nh * d)
+    check_bf16(host_bits(o), ref, max_frac=0.05, scale=sc, rel=2.0 ** -16)
 
 
 def test_argmax_ties_lowest_id():
