@@ -35,6 +35,7 @@ PCIE_H2D_GBS = 55.6        # measured per GPU in isolation (profiles/r01_links_m
 # buffer per GPU, as here, PP=4 loads reach 209 GB/s: links are independent, so the
 # aggregate peak is N x the isolated per-link figure)
 NVLINK_GBS = 900.0         # nominal per direction per GPU (north star); measured P2P 770
+PROFILE_STEPS = 8          # decode steps per timed step run under the per-kernel event profile
 
 
 def env_int(k, d):
@@ -180,7 +181,6 @@ def run_ours(args):
         r["ttft_dev"] = g.timing(stage).since_load_ms / 1e3
         r["load_ms"] = g.timing(stage).load_ms
         r["loaded_bytes"] = g.load_stats(stage).bytes
-        g.profile(profile)
         dev = 0.0
         t2 = time.perf_counter()
         for _ in range(dsteps):
@@ -188,15 +188,18 @@ def run_ours(args):
             dev += g.timing(stage).call_ms
         r["decode_host"] = time.perf_counter() - t2
         r["decode_dev"] = dev / 1e3
-        if consolidate:
+        if profile:  # per-kernel event profile on extra decode steps (events break PDL overlap)
+            g.profile(True)
+            for _ in range(PROFILE_STEPS):
+                g.decode_step(ids)
             g.profile(False)
+        if consolidate:
             st = g.consolidate(0)
             r["cons_s"] = st.seconds
             r["cons_pause"] = st.pause_seconds
             r["cons_bytes"] = st.weight_bytes + st.kv_bytes
             r["cons_w"], r["cons_kv"] = st.weight_bytes, st.kv_bytes
             if rank == 0:
-                g.profile(profile)
                 dev2 = 0.0
                 t3 = time.perf_counter()
                 for _ in range(dsteps):
@@ -205,7 +208,6 @@ def run_ours(args):
                 r["decode2_host"] = time.perf_counter() - t3
                 r["decode2_dev"] = dev2 / 1e3
         r["prof"] = g.profile_read(reset=True) if profile else {}
-        g.profile(False)
         if consolidate:
             barrier()
             g.destroy()

@@ -7,6 +7,7 @@
 
 #include <cstdio>
 #include <string>
+#include <utility>
 
 #include "../../include/hs.h"
 
@@ -57,6 +58,30 @@ uint64_t launch_total();
 // Forces module loading of every kernel on the current device (no lazy-load cost at T0).
 void warm_gemm_kernels();
 void warm_kernels();
+
+// Programmatic dependent launch: every kernel of the library is launched with
+// programmaticStreamSerialization, calls griddepcontrol.launch_dependents at entry (so the
+// next kernel's CTAs are scheduled while this one runs) and griddepcontrol.wait before its
+// first access to memory written by earlier kernels (weights may be prefetched before).
+// HS_PDL=0 in the environment disables it (A/B measurements).
+#define PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+#define PDL_LAUNCH() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launchk(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 struct DeviceGuard {
   int prev = -1;

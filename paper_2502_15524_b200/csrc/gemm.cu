@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 
 namespace hs {
@@ -163,6 +164,7 @@ __global__ void __launch_bounds__(128, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 KParams p) {
   using C = Cfg<BN>;
+  PDL_LAUNCH();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
@@ -194,8 +196,16 @@ __global__ void __launch_bounds__(128, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0 && lane == 0) {
-    // ---- TMA producer
-    for (int i = 0; i < nk; ++i) {
+    // ---- TMA producer: weights of the first stages before the grid dependency resolves
+    const int pre = min(nk, C::STAGES);
+    for (int i = 0; i < pre; ++i) {
+      mbar_expect_tx(&full[i], C::STAGE_BYTES);
+      tma_load_2d(&tmA, &full[i], smem + i * C::STAGE_BYTES, (kb0 + i) * 64, m0);
+    }
+    PDL_WAIT();
+    for (int i = 0; i < pre; ++i)
+      tma_load_2d(&tmB, &full[i], smem + i * C::STAGE_BYTES + C::A_BYTES, (kb0 + i) * 64, n0);
+    for (int i = pre; i < nk; ++i) {
       const int s = i % C::STAGES;
       const uint32_t ph = (i / C::STAGES) & 1;
       mbar_wait(&empty[s], ph ^ 1);
@@ -225,6 +235,7 @@ __global__ void __launch_bounds__(128, 1)
     umma_commit(accf);
   }
   __syncwarp();
+  PDL_WAIT();
 
   // ---- epilogue: all 4 warps
   mbar_wait(accf, 0);
@@ -286,6 +297,8 @@ __global__ void __launch_bounds__(128, 1)
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N,
                                      int epi, void* out, int ldo, const bf16* __restrict__ resid,
                                      int ldr) {
+  PDL_LAUNCH();
+  PDL_WAIT();
   const int n = blockIdx.y;
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= M) return;
@@ -420,6 +433,7 @@ template <int BN>
 __global__ void __launch_bounds__(192, 1)
     gemm_sk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, SkParams p) {
   using C = SkCfg<BN>;
+  PDL_LAUNCH();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* vals = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES);
@@ -452,19 +466,25 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer over every segment of the range
-      int i = 0;
-      for (int cur = beg; cur < end;) {
-        const int t = cur / p.nkb, kb_lo = cur % p.nkb, kb_hi = min(p.nkb, kb_lo + (end - cur));
-        for (int kb = kb_lo; kb < kb_hi; ++kb, ++i) {
-          const int s = i % C::STAGES;
-          mbar_wait(&empty[s], ((i / C::STAGES) & 1) ^ 1);
-          uint8_t* sa = smem + s * C::STAGE_BYTES;
-          mbar_expect_tx(&full[s], C::STAGE_BYTES);
-          tma_load_2d(&tmA, &full[s], sa, kb * 64, t * 128);
-          tma_load_2d(&tmB, &full[s], sa + C::A_BYTES, kb * 64, 0);
-        }
-        cur += kb_hi - kb_lo;
+    if (lane == 0) {  // ---- TMA producer over the CTA's k-block range [beg, end)
+      // weights of the first stages are requested before the grid dependency resolves
+      const int pre = min(end - beg, C::STAGES);
+      for (int i = 0; i < pre; ++i) {
+        const int x = beg + i;
+        mbar_expect_tx(&full[i], C::STAGE_BYTES);
+        tma_load_2d(&tmA, &full[i], smem + i * C::STAGE_BYTES, (x % p.nkb) * 64, (x / p.nkb) * 128);
+      }
+      PDL_WAIT();
+      for (int i = 0; i < pre; ++i)
+        tma_load_2d(&tmB, &full[i], smem + i * C::STAGE_BYTES + C::A_BYTES, ((beg + i) % p.nkb) * 64, 0);
+      for (int i = pre; beg + i < end; ++i) {
+        const int x = beg + i;
+        const int s = i % C::STAGES;
+        mbar_wait(&empty[s], ((i / C::STAGES) & 1) ^ 1);
+        uint8_t* sa = smem + s * C::STAGE_BYTES;
+        mbar_expect_tx(&full[s], C::STAGE_BYTES);
+        tma_load_2d(&tmA, &full[s], sa, (x % p.nkb) * 64, (x / p.nkb) * 128);
+        tma_load_2d(&tmB, &full[s], sa + C::A_BYTES, (x % p.nkb) * 64, 0);
       }
     }
   } else if (warp == 1) {
@@ -493,6 +513,7 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     // ---- epilogue warps 2..5 (et = 0..127 owns tile row ml = et)
+    PDL_WAIT();
     const int quad = warp & 3;
     const int ml = quad * 32 + lane;
     const int et = ml;
@@ -611,9 +632,173 @@ __global__ void __launch_bounds__(192, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)C::TMEM_COLS));
 }
 
+// ------------------------------------------------------------------ persistent tiled (prefill)
+// Tensor-bound GEMM for many tokens.  Persistent CTAs (one per SM) walk a static tile
+// schedule (tile = blockIdx.x + i * gridDim.x, consecutive tiles share the weight tile so the
+// second read hits L2); warp 0 TMA producer, warp 1 MMA issuer, warps 2-5 epilogue; two TMEM
+// accumulators so the epilogue of tile i overlaps the MMAs of tile i+1.
+struct TpParams {
+  int M, N, nkb, m_tiles, n_tiles;
+  int epi;
+  void* out;
+  int ldo;
+  const bf16* resid;
+  int ldr;
+};
+
+template <int BN>
+struct TpCfg {
+  static constexpr int A_BYTES = 128 * 64 * 2;
+  static constexpr int B_BYTES = BN * 64 * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = BN >= 256 ? 4 : 6;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(192, 1)
+    gemm_tp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TpParams p) {
+  using C = TpCfg<BN>;
+  PDL_LAUNCH();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles = p.m_tiles * p.n_tiles;
+
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"((uint32_t)C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // weights of the first stages before the grid dependency resolves
+      const int my_tiles = blockIdx.x < tiles ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+      const int pre = min(my_tiles * p.nkb, C::STAGES);
+      for (int i = 0; i < pre; ++i) {
+        const int t = blockIdx.x + (i / p.nkb) * gridDim.x;
+        mbar_expect_tx(&full[i], C::STAGE_BYTES);
+        tma_load_2d(&tmA, &full[i], smem + i * C::STAGE_BYTES, (i % p.nkb) * 64, (t / p.n_tiles) * 128);
+      }
+      PDL_WAIT();
+      for (int i = 0; i < pre; ++i) {
+        const int t = blockIdx.x + (i / p.nkb) * gridDim.x;
+        tma_load_2d(&tmB, &full[i], smem + i * C::STAGE_BYTES + C::A_BYTES, (i % p.nkb) * 64, (t % p.n_tiles) * BN);
+      }
+      int i = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m0 = (t / p.n_tiles) * 128, n0 = (t % p.n_tiles) * BN;
+        for (int kb = 0; kb < p.nkb; ++kb, ++i) {
+          if (i < pre) continue;
+          const int s = i % C::STAGES;
+          mbar_wait(&empty[s], ((i / C::STAGES) & 1) ^ 1);
+          uint8_t* sa = smem + s * C::STAGE_BYTES;
+          mbar_expect_tx(&full[s], C::STAGE_BYTES);
+          tma_load_2d(&tmA, &full[s], sa, kb * 64, m0);
+          tma_load_2d(&tmB, &full[s], sa + C::A_BYTES, kb * 64, n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = instr_desc<BN>();
+      int i = 0, lt = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
+        const int buf = lt & 1;
+        mbar_wait(&tempty[buf], ((lt >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + buf * BN;
+        for (int kb = 0; kb < p.nkb; ++kb, ++i) {
+          const int s = i % C::STAGES;
+          mbar_wait(&full[s], (i / C::STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint8_t* sa = smem + s * C::STAGE_BYTES;
+          const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + C::A_BYTES);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) umma_bf16(acc, da + 2 * k, db + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[buf]);
+      }
+    }
+  } else {
+    PDL_WAIT();
+    const int quad = warp & 3;
+    int lt = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
+      const int buf = lt & 1;
+      const int m0 = (t / p.n_tiles) * 128, n0 = (t % p.n_tiles) * BN;
+      mbar_wait(&tfull[buf], (lt >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int m = m0 + quad * 32 + lane;
+      const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16) + buf * BN;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(trow + c0, v);
+        if (n0 + c0 < p.N) {
+          const int ncol = min(32, p.N - n0 - c0);
+          if (p.epi == EPI_F32) {
+            float* o = reinterpret_cast<float*>(p.out) + (size_t)(n0 + c0) * p.ldo;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < ncol) o[(size_t)j * p.ldo + m] = v[j];
+          } else if (p.epi == EPI_BF16) {
+            bf16* o = reinterpret_cast<bf16*>(p.out) + (size_t)(n0 + c0) * p.ldo;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < ncol) o[(size_t)j * p.ldo + m] = __float2bfloat16_rn(v[j]);
+          } else if (p.epi == EPI_RESID) {
+            bf16* o = reinterpret_cast<bf16*>(p.out) + (size_t)(n0 + c0) * p.ldo;
+            const bf16* r = p.resid + (size_t)(n0 + c0) * p.ldr;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < ncol) o[(size_t)j * p.ldo + m] = __float2bfloat16_rn(v[j] + __bfloat162float(r[(size_t)j * p.ldr + m]));
+          } else {
+            bf16* o = reinterpret_cast<bf16*>(p.out) + (size_t)(n0 + c0) * p.ldo;
+            const int f = (m0 + quad * 32) / 2 + lane;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float u = __shfl_xor_sync(0xffffffffu, v[j], 16);
+              if (lane < 16 && j < ncol) o[(size_t)j * p.ldo + f] = __float2bfloat16_rn(silu_f(v[j]) * u);
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf])) : "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)C::TMEM_COLS));
+}
+
 // Decode RMSNorm with the exact arithmetic of the fused epilogue (one 128-thread CTA per row).
 __global__ void __launch_bounds__(128) rownorm_kernel(const bf16* __restrict__ x, const bf16* __restrict__ w,
                                                       bf16* __restrict__ y, int H, float eps) {
+  PDL_LAUNCH();
+  PDL_WAIT();
   __shared__ float red[4];
   row_norm128(x + (size_t)blockIdx.x * H, H, w, y + (size_t)blockIdx.x * H, eps, threadIdx.x, red, 1);
 }
@@ -657,6 +842,14 @@ hs_status make_tma(TmaMat* t, const void* ptr, int64_t rows, int64_t cols, int b
   return HS_OK;
 }
 
+bool pdl_enabled() {
+  static int on = [] {
+    const char* e = getenv("HS_PDL");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return on != 0;
+}
+
 static const int kBN[] = {16, 32, 64, 128, 256};
 int gemm_bn_count() { return 5; }
 int gemm_bn_value(int i) { return kBN[i]; }
@@ -689,12 +882,12 @@ static hs_status launch(const GemmArgs& a, int splits, int kbps, cudaStream_t st
   p.epi = splits > 1 ? -1 : a.epi;
   p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr; p.ws = a.workspace;
   dim3 grid(cdiv(a.M, 128), cdiv(a.N, BN), splits);
-  gemm_kernel<BN><<<grid, 128, C::SMEM, st>>>(a.A->map, tb.map, p);
+  launchk(gemm_kernel<BN>, grid, 128, C::SMEM, st, a.A->map, tb.map, p);
   count_launch();
   HS_CUDA(cudaGetLastError());
   if (splits > 1) {
     dim3 g2(cdiv(a.M, 256), a.N);
-    splitk_reduce_kernel<<<g2, 256, 0, st>>>(a.workspace, splits, a.M, a.N, a.epi, a.out, a.ldo, a.resid, a.ldr);
+    launchk(splitk_reduce_kernel, g2, 256, 0, st, (const float*)a.workspace, splits, a.M, a.N, a.epi, a.out, a.ldo, a.resid, a.ldr);
     count_launch();
     HS_CUDA(cudaGetLastError());
   }
@@ -715,7 +908,16 @@ static void warm_sk() {
   cudaFuncGetAttributes(&at, gemm_sk_kernel<BN>);
 }
 
+template <int BN>
+static void warm_tp() {
+  cudaFuncAttributes at;
+  cudaFuncSetAttribute(gemm_tp_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, TpCfg<BN>::SMEM);
+  cudaFuncGetAttributes(&at, gemm_tp_kernel<BN>);
+}
+
 void warm_gemm_kernels() {
+  warm_tp<128>();
+  warm_tp<256>();
   warm_sk<16>();
   warm_sk<32>();
   warm_sk<64>();
@@ -760,7 +962,7 @@ static hs_status launch_sk(const GemmArgs& a, cudaStream_t st, bool* done) {
   p.pos = f.pos; p.slot = f.slot; p.tab = f.rope_tab; p.q_out = f.q_out; p.pool = f.pool;
   p.nh = f.n_heads; p.hd = f.head_dim;
   if (p.fuse == FUSE_NORM && a.epi != EPI_RESID) p.fuse = FUSE_NONE;
-  gemm_sk_kernel<BN><<<G, 192, C::SMEM, st>>>(a.A->map, a.B[bi].map, p);
+  launchk(gemm_sk_kernel<BN>, G, 192, C::SMEM, st, a.A->map, a.B[bi].map, p);
   count_launch();
   HS_CUDA(cudaGetLastError());
   if (f.applied && p.fuse != FUSE_NONE) *f.applied = true;
@@ -768,8 +970,32 @@ static hs_status launch_sk(const GemmArgs& a, cudaStream_t st, bool* done) {
   return HS_OK;
 }
 
+template <int BN>
+static hs_status launch_tp(const GemmArgs& a, cudaStream_t st) {
+  using C = TpCfg<BN>;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static bool attr_set[64] = {};
+  if (dev < 64 && !attr_set[dev]) {
+    HS_CUDA(cudaFuncSetAttribute(gemm_tp_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set[dev] = true;
+  }
+  int bi = 0;
+  while (kBN[bi] != BN) ++bi;
+  if (a.B[bi].box_rows != BN) HS_FAIL(HS_E_INVAL, "TMA box mismatch");
+  TpParams p{};
+  p.M = a.M; p.N = a.N; p.nkb = a.K / 64; p.m_tiles = a.M / 128; p.n_tiles = (int)cdiv(a.N, BN);
+  p.epi = a.epi; p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr;
+  const int tiles = p.m_tiles * p.n_tiles;
+  const int grid = std::min(tiles, num_sms(dev));
+  launchk(gemm_tp_kernel<BN>, grid, 192, C::SMEM, st, a.A->map, a.B[bi].map, p);
+  count_launch();
+  HS_CUDA(cudaGetLastError());
+  return HS_OK;
+}
+
 void launch_rownorm_decode(const bf16* x, const bf16* w, bf16* y, int T, int H, float eps, cudaStream_t st) {
-  rownorm_kernel<<<T, 128, 0, st>>>(x, w, y, H, eps);
+  launchk(rownorm_kernel, T, 128, 0, st, x, w, y, H, eps);
   count_launch();
 }
 
@@ -781,6 +1007,14 @@ hs_status gemm(const GemmArgs& a, cudaStream_t st) {
     bool done = false;
     hs_status r = BN == 16 ? launch_sk<16>(a, st, &done) : BN == 32 ? launch_sk<32>(a, st, &done) : launch_sk<64>(a, st, &done);
     if (r != HS_OK || done) return r;
+  }
+  if (a.N > 64) {  // tensor-bound: persistent tiles; BN minimising (waves x tile cost)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int G = num_sms(dev), mt = a.M / 128;
+    const long long c128 = cdiv((long long)mt * cdiv(a.N, 128), G) * 128;
+    const long long c256 = cdiv((long long)mt * cdiv(a.N, 256), G) * 256;
+    return c256 < c128 ? launch_tp<256>(a, st) : launch_tp<128>(a, st);
   }
   const int tiles = (a.M / 128) * (int)cdiv(a.N, BN);
   const int nkb = a.K / 64;

@@ -10,6 +10,8 @@ namespace hs {
 // ------------------------------------------------------------------ embedding (a5) -------
 __global__ void embed_kernel(const int* __restrict__ tok, const uint4* __restrict__ E,
                              uint4* __restrict__ x, int H8) {
+  PDL_LAUNCH();
+  PDL_WAIT();
   const int t = blockIdx.x;
   const uint4* src = E + (size_t)tok[t] * H8;
   uint4* dst = x + (size_t)t * H8;
@@ -19,8 +21,8 @@ __global__ void embed_kernel(const int* __restrict__ tok, const uint4* __restric
 void launch_embed(const int* tok, const bf16* E, bf16* x, int T, int H, cudaStream_t st) {
   count_launch();
   const int H8 = H / 8;
-  embed_kernel<<<T, H8 < 512 ? H8 : 512, 0, st>>>(tok, reinterpret_cast<const uint4*>(E),
-                                                   reinterpret_cast<uint4*>(x), H8);
+  launchk(embed_kernel, T, H8 < 512 ? H8 : 512, 0, st, tok, reinterpret_cast<const uint4*>(E),
+          reinterpret_cast<uint4*>(x), H8);
 }
 
 // ------------------------------------------------------------------ RMSNorm (a6) ---------
@@ -34,6 +36,8 @@ template <int MAXV>
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const uint4* __restrict__ x, const int* __restrict__ rows,
                                                       const uint4* __restrict__ w, uint4* __restrict__ y,
                                                       int H8, float inv_h, float eps) {
+  PDL_LAUNCH();
+  PDL_WAIT();
   __shared__ float red[8];
   const int i = blockIdx.x;
   const int r = rows ? rows[i] : i;
@@ -85,16 +89,18 @@ void launch_rmsnorm(const bf16* x, const int* rows, const bf16* w, bf16* y, int 
   auto X = reinterpret_cast<const uint4*>(x);
   auto W = reinterpret_cast<const uint4*>(w);
   auto Y = reinterpret_cast<uint4*>(y);
-  if (H8 <= 256) rmsnorm_kernel<1><<<T, 256, 0, st>>>(X, rows, W, Y, H8, 1.0f / H, eps);
-  else if (H8 <= 512) rmsnorm_kernel<2><<<T, 256, 0, st>>>(X, rows, W, Y, H8, 1.0f / H, eps);
-  else if (H8 <= 1024) rmsnorm_kernel<4><<<T, 256, 0, st>>>(X, rows, W, Y, H8, 1.0f / H, eps);
-  else rmsnorm_kernel<8><<<T, 256, 0, st>>>(X, rows, W, Y, H8, 1.0f / H, eps);
+  if (H8 <= 256) launchk(rmsnorm_kernel<1>, T, 256, 0, st, X, rows, W, Y, H8, 1.0f / H, eps);
+  else if (H8 <= 512) launchk(rmsnorm_kernel<2>, T, 256, 0, st, X, rows, W, Y, H8, 1.0f / H, eps);
+  else if (H8 <= 1024) launchk(rmsnorm_kernel<4>, T, 256, 0, st, X, rows, W, Y, H8, 1.0f / H, eps);
+  else launchk(rmsnorm_kernel<8>, T, 256, 0, st, X, rows, W, Y, H8, 1.0f / H, eps);
 }
 
 // ------------------------------------------------------------------ RoPE + KV write (a8) -
 __global__ void rope_kv_kernel(const bf16* __restrict__ qkv, const int* __restrict__ pos,
                                const int* __restrict__ slot, const float2* __restrict__ tab,
                                bf16* __restrict__ q_out, bf16* __restrict__ pool, int nh, int d) {
+  PDL_LAUNCH();
+  PDL_WAIT();
   const int t = blockIdx.x;
   const int H = nh * d, hd = d / 2;
   const bf16* row = qkv + (size_t)t * 3 * H;
@@ -125,7 +131,7 @@ __global__ void rope_kv_kernel(const bf16* __restrict__ qkv, const int* __restri
 void launch_rope_kv(const bf16* qkv, const int* pos, const int* slot, const float2* tab, bf16* q_out,
                     bf16* pool, int T, int nh, int d, cudaStream_t st) {
   count_launch();
-  rope_kv_kernel<<<T, 256, 0, st>>>(qkv, pos, slot, tab, q_out, pool, nh, d);
+  launchk(rope_kv_kernel, T, 256, 0, st, qkv, pos, slot, tab, q_out, pool, nh, d);
 }
 
 // ------------------------------------------------------------------ attention (a9) -------
@@ -203,6 +209,8 @@ template <int D>
 __global__ void __launch_bounds__(128) attn_prefill_kernel(
     const bf16* __restrict__ q, const bf16* __restrict__ pool, const SeqDesc* __restrict__ seqs,
     const int* __restrict__ tables, int max_blocks, bf16* __restrict__ o, int nh) {
+  PDL_LAUNCH();
+  PDL_WAIT();
   constexpr int CH = D / 8;  // 16-byte chunks per row
   constexpr int KS = D / 16; // k-steps over head_dim
   __shared__ __align__(128) uint4 Ks[PF_KC * CH];
@@ -358,8 +366,8 @@ void launch_attn_prefill(const bf16* q, const bf16* pool, const SeqDesc* seqs, i
                          const int* tables, int max_blocks, bf16* o, int nh, int d, cudaStream_t st) {
   count_launch();
   dim3 grid((max_nq + PF_Q - 1) / PF_Q, nh, n_seqs);
-  if (d == 128) attn_prefill_kernel<128><<<grid, 128, 0, st>>>(q, pool, seqs, tables, max_blocks, o, nh);
-  else attn_prefill_kernel<64><<<grid, 128, 0, st>>>(q, pool, seqs, tables, max_blocks, o, nh);
+  if (d == 128) launchk(attn_prefill_kernel<128>, grid, 128, 0, st, q, pool, seqs, tables, max_blocks, o, nh);
+  else launchk(attn_prefill_kernel<64>, grid, 128, 0, st, q, pool, seqs, tables, max_blocks, o, nh);
 }
 
 // Decode: CTA = (head, seq, split of DEC_KC = 64 keys).  The split's 4 block ids are read
@@ -374,6 +382,8 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
     const bf16* __restrict__ q, const bf16* __restrict__ pool, const SeqDesc* __restrict__ seqs,
     const int* __restrict__ tables, int max_blocks, bf16* __restrict__ o, int nh, float* __restrict__ ws,
     int splits, unsigned* __restrict__ ctr) {
+  PDL_LAUNCH();
+  PDL_WAIT();
   __shared__ __align__(16) bf16 Ks[DEC_KC][D];
   __shared__ __align__(16) bf16 Vs[DEC_KC][D];
   __shared__ float qs[D];
@@ -505,13 +515,15 @@ void launch_attn_decode(const bf16* q, const bf16* pool, const SeqDesc* seqs, in
                         unsigned* ctr, cudaStream_t st) {
   count_launch();
   dim3 grid(nh, n_seqs, splits);
-  if (d == 128) attn_decode_kernel<128><<<grid, 128, 0, st>>>(q, pool, seqs, tables, max_blocks, o, nh, ws, splits, ctr);
-  else attn_decode_kernel<64><<<grid, 128, 0, st>>>(q, pool, seqs, tables, max_blocks, o, nh, ws, splits, ctr);
+  if (d == 128) launchk(attn_decode_kernel<128>, grid, 128, 0, st, q, pool, seqs, tables, max_blocks, o, nh, ws, splits, ctr);
+  else launchk(attn_decode_kernel<64>, grid, 128, 0, st, q, pool, seqs, tables, max_blocks, o, nh, ws, splits, ctr);
 }
 
 // ------------------------------------------------------------------ argmax (a15) ---------
 __global__ void __launch_bounds__(1024) argmax_kernel(const float* __restrict__ logits, int V,
                                                       int* __restrict__ out) {
+  PDL_LAUNCH();
+  PDL_WAIT();
   __shared__ float bv[32];
   __shared__ int bi[32];
   const float* row = logits + (size_t)blockIdx.x * V;
@@ -541,13 +553,15 @@ __global__ void __launch_bounds__(1024) argmax_kernel(const float* __restrict__ 
 
 void launch_argmax(const float* logits, int V, int n, int* tokens, cudaStream_t st) {
   count_launch();
-  argmax_kernel<<<n, 1024, 0, st>>>(logits, V, tokens);
+  launchk(argmax_kernel, n, 1024, 0, st, logits, V, tokens);
 }
 
 // ------------------------------------------------------------------ hand-off (a13) -------
 __global__ void __launch_bounds__(256) send_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
                                                    uint64_t n16, unsigned* done_ctr, unsigned* flag,
                                                    unsigned epoch) {
+  PDL_LAUNCH();
+  PDL_WAIT();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (; i + 3 * stride < n16; i += 4 * stride) {
@@ -570,11 +584,13 @@ __global__ void __launch_bounds__(256) send_kernel(const uint4* __restrict__ src
 void launch_send(const void* src, void* dst, uint64_t bytes, unsigned* done_ctr, unsigned* flag,
                  unsigned epoch, int ctas, cudaStream_t st) {
   count_launch();
-  send_kernel<<<ctas, 256, 0, st>>>(reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst),
-                                    bytes / 16, done_ctr, flag, epoch);
+  launchk(send_kernel, ctas, 256, 0, st, reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst),
+          (uint64_t)(bytes / 16), done_ctr, flag, epoch);
 }
 
 __global__ void wait_kernel(const unsigned* flag, unsigned epoch, int* err) {
+  PDL_LAUNCH();
+  PDL_WAIT();
   uint64_t t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (;;) {
@@ -593,13 +609,15 @@ __global__ void wait_kernel(const unsigned* flag, unsigned epoch, int* err) {
 
 void launch_wait(const unsigned* flag, unsigned epoch, int* err, cudaStream_t st) {
   count_launch();
-  wait_kernel<<<1, 1, 0, st>>>(flag, epoch, err);
+  launchk(wait_kernel, 1, 1, 0, st, flag, epoch, err);
 }
 
 // ------------------------------------------------------------------ span copy (a17) ------
 __global__ void __launch_bounds__(256) span_copy_kernel(const uint64_t* __restrict__ src,
                                                         const uint64_t* __restrict__ dst, uint64_t n16,
                                                         int parts) {
+  PDL_LAUNCH();
+  PDL_WAIT();
   const int span = blockIdx.x / parts, part = blockIdx.x % parts;
   const uint4* s = reinterpret_cast<const uint4*>(src[span]);
   uint4* d = reinterpret_cast<uint4*>(dst[span]);
@@ -616,6 +634,8 @@ __global__ void __launch_bounds__(256) span_copy_kernel(const uint64_t* __restri
 // Copy list: descriptors {src, dst, bytes} (bytes % 16 == 0, <= 64 KiB each), persistent
 // grid-stride over descriptors; 4 x 16-byte loads in flight per thread before the stores.
 __global__ void __launch_bounds__(256) copy_list_kernel(const CopyDesc* __restrict__ d, int n) {
+  PDL_LAUNCH();
+  PDL_WAIT();
   for (int i = blockIdx.x; i < n; i += gridDim.x) {
     const uint4* s = reinterpret_cast<const uint4*>(d[i].src);
     uint4* o = reinterpret_cast<uint4*>(d[i].dst);
@@ -632,7 +652,7 @@ __global__ void __launch_bounds__(256) copy_list_kernel(const CopyDesc* __restri
 void launch_copy_list(const CopyDesc* d, int n, int ctas, cudaStream_t st) {
   if (n <= 0) return;
   count_launch();
-  copy_list_kernel<<<ctas < n ? ctas : n, 256, 0, st>>>(d, n);
+  launchk(copy_list_kernel, ctas < n ? ctas : n, 256, 0, st, d, n);
 }
 
 // Small copies between mapped pinned host memory and device memory done by SMs, so they never
@@ -640,6 +660,8 @@ void launch_copy_list(const CopyDesc* d, int n, int ctas, cudaStream_t st) {
 // the compute stream would wait for the whole load and serialise prefill after it).
 __global__ void __launch_bounds__(256) small_copy_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
                                                          int n16) {
+  PDL_LAUNCH();
+  PDL_WAIT();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += gridDim.x * blockDim.x) dst[i] = src[i];
   __threadfence_system();
 }
@@ -649,7 +671,7 @@ void launch_small_copy(const void* src, void* dst, uint64_t bytes, cudaStream_t 
   if (n16 <= 0) return;
   count_launch();
   const int ctas = n16 > 4096 ? 16 : 1;
-  small_copy_kernel<<<ctas, 256, 0, st>>>(reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst), n16);
+  launchk(small_copy_kernel, ctas, 256, 0, st, reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst), n16);
 }
 
 void launch_span_copy(const uint64_t* src, const uint64_t* dst, int n, uint64_t span_bytes, cudaStream_t st) {
@@ -658,7 +680,7 @@ void launch_span_copy(const uint64_t* src, const uint64_t* dst, int n, uint64_t 
   const uint64_t n16 = span_bytes / 16;
   int parts = (int)((span_bytes + 65535) / 65536);
   if (parts < 1) parts = 1;
-  span_copy_kernel<<<n * parts, 256, 0, st>>>(src, dst, n16, parts);
+  launchk(span_copy_kernel, n * parts, 256, 0, st, src, dst, n16, parts);
 }
 
 void warm_kernels() {
