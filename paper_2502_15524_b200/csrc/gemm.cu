@@ -423,7 +423,9 @@ struct SkCfg {
   static constexpr int A_BYTES = 128 * 64 * 2;
   static constexpr int B_BYTES = BN * 64 * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN >= 64 ? 6 : 8;
+  // BN <= 32: 5 stages (~100 KB) so two CTAs fit an SM: the next kernel's CTA (PDL) becomes
+  // resident and prefetches its weights while this one drains
+  static constexpr int STAGES = BN >= 64 ? 6 : 5;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
   static constexpr int VALS_BYTES = 128 * BN * 4;  // tile values for the RoPE pairing
   static constexpr int SMEM = STAGES * STAGE_BYTES + VALS_BYTES + 1024 + 512;
