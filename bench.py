@@ -265,7 +265,7 @@ def run_ours(args):
     g_bytes = sum(v["bytes"] for v in dec_gemm)
     g_count = sum(v["count"] for v in dec_gemm)
     achieved = (g_bytes / (g_ms / 1e3) / 1e9) if g_ms > 0 else 0.0
-    roof = {"kernel": "gemm_kernel (tcgen05 swap-AB decode GEMM, qkv/o/gate_up/down, + split-K reduce)",
+    roof = {"kernel": "gemm_sk_kernel<16> (tcgen05 stream-K weight-streaming decode GEMM: qkv/o/gate_up/down, fused epilogues)",
             "bound": "hbm", "achieved": round(agg_max(achieved) if False else achieved, 1),
             "peak": pk.get("hbm_gbs"), "unit": "GB/s",
             "frac": round(achieved / pk.get("hbm_gbs", 6650.0), 4), "traffic": None,

@@ -37,6 +37,12 @@ hs_status hs_k_embed(const int32_t* tok, const void* E, void* x, int32_t T, int3
 hs_status hs_k_span_copy(const uint64_t* src, const uint64_t* dst, int32_t n, uint64_t span_bytes,
                          void* stream);
 
+/* Test-only instrumentation: enable != 0 makes the stream-K decode GEMM record per-CTA phase
+ * timestamps (%globaltimer ns: start, weights requested, grid dependency resolved, first
+ * stage full, last MMA issued, epilogue done, CTA end; 8 slots per CTA) of its latest launch;
+ * host_out (optional) receives n_ctas * 8 uint64.  enable == 0 frees the buffer. */
+hs_status hs_debug_gemm_trace(int32_t enable, void* host_out, int32_t n_ctas);
+
 #ifdef __cplusplus
 }
 #endif

@@ -356,7 +356,14 @@ struct SkParams {
   bf16* q_out;
   bf16* pool;
   int nh, hd;  // heads, head_dim
+  unsigned long long* trace;  // optional per-CTA phase timestamps (globaltimer ns), 8 per CTA
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ int sk_begin(long long c, long long W, int G) { return (int)(c * W / G); }
 // CTA owning flattened k-block x: max c with floor(c W / G) <= x
@@ -449,13 +456,22 @@ __global__ void __launch_bounds__(192, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long W = (long long)p.tiles * p.nkb;
   const int beg = sk_begin(blockIdx.x, W, p.G), end = sk_begin(blockIdx.x + 1, W, p.G);
+  unsigned long long* tr = p.trace ? p.trace + blockIdx.x * 8 : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = gtimer();
+  const int pre = min(end - beg, C::STAGES);
 
   if (threadIdx.x == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // the producer (this thread) requests the first weight tiles before anything else:
+    // they do not depend on the previous kernel (PDL) nor on TMEM
+    for (int i = 0; i < pre; ++i) {
+      const int x = beg + i;
+      mbar_expect_tx(&full[i], C::STAGE_BYTES);
+      tma_load_2d(&tmA, &full[i], smem + i * C::STAGE_BYTES, (x % p.nkb) * 64, (x / p.nkb) * 128);
+    }
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -469,14 +485,10 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer over the CTA's k-block range [beg, end)
-      // weights of the first stages are requested before the grid dependency resolves
-      const int pre = min(end - beg, C::STAGES);
-      for (int i = 0; i < pre; ++i) {
-        const int x = beg + i;
-        mbar_expect_tx(&full[i], C::STAGE_BYTES);
-        tma_load_2d(&tmA, &full[i], smem + i * C::STAGE_BYTES, (x % p.nkb) * 64, (x / p.nkb) * 128);
-      }
+      // (the first `pre` weight tiles were requested during setup, before the dependency)
+      if (tr) tr[1] = gtimer();
       PDL_WAIT();
+      if (tr) tr[2] = gtimer();
       for (int i = 0; i < pre; ++i)
         tma_load_2d(&tmB, &full[i], smem + i * C::STAGE_BYTES + C::A_BYTES, ((beg + i) % p.nkb) * 64, 0);
       for (int i = pre; beg + i < end; ++i) {
@@ -502,6 +514,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int kb = kb_lo; kb < kb_hi; ++kb, ++i) {
           const int s = i % C::STAGES;
           mbar_wait(&full[s], (i / C::STAGES) & 1);
+          if (tr && i == 0) tr[3] = gtimer();
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint8_t* sa = smem + s * C::STAGE_BYTES;
           const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + C::A_BYTES);
@@ -512,6 +525,7 @@ __global__ void __launch_bounds__(192, 1)
         umma_commit(&tfull[buf]);
         cur += kb_hi - kb_lo;
       }
+      if (tr) tr[4] = gtimer();
     }
   } else {
     // ---- epilogue warps 2..5 (et = 0..127 owns tile row ml = et)
@@ -548,17 +562,18 @@ __global__ void __launch_bounds__(192, 1)
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf])) : "memory");
       cur += kb_hi - kb_lo;
       // ---- arrival: the last CTA to finish a part of tile t applies its epilogue
-      __threadfence();
+      // (CTA barrier, then one gpu-scope fence + atomic by one thread: cumulative release)
       named_bar(1, 128);
       if (et == 0) {
+        __threadfence();
         const unsigned old = atomicAdd(&p.ctr[t], 1u);
         const int last = old == (unsigned)(np - 1);
         if (last) p.ctr[t] = 0;
         *flag = last;
       }
+      if (et == 0 && *flag) __threadfence();  // acquire side
       named_bar(1, 128);
       if (!*flag) continue;
-      __threadfence();
       const int m = t * 128 + ml;
       if (p.fuse == FUSE_ROPE) {
         for (int n = 0; n < p.N; ++n) {
@@ -610,17 +625,19 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
       if (p.fuse == FUSE_NORM) {  // grid-level arrival: the last tile's CTA normalises the rows
-        __threadfence();
         named_bar(1, 128);
         if (et == 0) {
+          __threadfence();
           const unsigned old = atomicAdd(&p.ctr[p.tiles], 1u);
           const int last = old == (unsigned)(p.tiles - 1);
-          if (last) p.ctr[p.tiles] = 0;
+          if (last) {
+            p.ctr[p.tiles] = 0;
+            __threadfence();
+          }
           *flag = last;
         }
         named_bar(1, 128);
         if (*flag) {
-          __threadfence();
           for (int n = 0; n < p.N; ++n)
             row_norm128(reinterpret_cast<const bf16*>(p.out) + (size_t)n * p.ldo, p.M, p.norm_w,
                         p.norm_out + (size_t)n * p.ldo, p.eps, et, red, 1);
@@ -628,8 +645,10 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   }
+  if (tr && threadIdx.x == 64) tr[5] = gtimer();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (tr && threadIdx.x == 0) tr[6] = gtimer();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)C::TMEM_COLS));
 }
@@ -934,6 +953,9 @@ void warm_gemm_kernels() {
   cudaFuncGetAttributes(&at, splitk_reduce_kernel);
 }
 
+// HS_TRACE=1: the stream-K GEMM records per-CTA phase timestamps (hs_debug_gemm_trace)
+static unsigned long long* g_sk_trace = nullptr;
+
 template <int BN>
 static hs_status launch_sk(const GemmArgs& a, cudaStream_t st, bool* done) {
   using C = SkCfg<BN>;
@@ -963,6 +985,7 @@ static hs_status launch_sk(const GemmArgs& a, cudaStream_t st, bool* done) {
   p.fuse = f.kind; p.norm_w = f.norm_w; p.norm_out = f.norm_out; p.eps = f.eps;
   p.pos = f.pos; p.slot = f.slot; p.tab = f.rope_tab; p.q_out = f.q_out; p.pool = f.pool;
   p.nh = f.n_heads; p.hd = f.head_dim;
+  p.trace = g_sk_trace;
   if (p.fuse == FUSE_NORM && a.epi != EPI_RESID) p.fuse = FUSE_NONE;
   launchk(gemm_sk_kernel<BN>, G, 192, C::SMEM, st, a.A->map, a.B[bi].map, p);
   count_launch();
@@ -1048,3 +1071,20 @@ hs_status gemm(const GemmArgs& a, cudaStream_t st) {
 }
 
 }  // namespace hs
+
+extern "C" hs_status hs_debug_gemm_trace(int32_t enable, void* host_out, int32_t n_ctas) {
+  using namespace hs;
+  if (enable && !g_sk_trace) {
+    HS_CUDA(cudaMalloc(&g_sk_trace, 4096 * 8 * 8));
+    HS_CUDA(cudaMemset(g_sk_trace, 0, 4096 * 8 * 8));
+  }
+  if (host_out && g_sk_trace) {
+    HS_CUDA(cudaDeviceSynchronize());
+    HS_CUDA(cudaMemcpy(host_out, g_sk_trace, (size_t)n_ctas * 8 * 8, cudaMemcpyDeviceToHost));
+  }
+  if (!enable && g_sk_trace) {
+    cudaFree(g_sk_trace);
+    g_sk_trace = nullptr;
+  }
+  return HS_OK;
+}

@@ -110,7 +110,7 @@ SYMBOLS = ["hs_image_layout", "hs_plan_stages", "hs_predict_ttft_eq1", "hs_predi
            "hs_debug_poison_weights", "hs_debug_launch_count", "hs_stage_timing_get", "hs_profile_enable",
            "hs_profile_read", "hs_debug_comm_selftest",
            "hs_k_gemm", "hs_k_rmsnorm", "hs_k_rope_kv", "hs_k_attention", "hs_k_argmax", "hs_k_embed",
-           "hs_k_span_copy"]
+           "hs_k_span_copy", "hs_debug_gemm_trace"]
 
 _lib = None
 
@@ -160,6 +160,7 @@ def lib():
     L.hs_k_argmax.argtypes = [VP, I32, I32, VP, VP]
     L.hs_k_embed.argtypes = [VP, VP, VP, I32, I32, VP]
     L.hs_k_span_copy.argtypes = [VP, VP, I32, U64, VP]
+    L.hs_debug_gemm_trace.argtypes = [I32, VP, I32]
     _lib = L
     return L
 
@@ -409,3 +410,9 @@ def k_embed(tok, E, x):
 
 def k_span_copy(src, dst, span_bytes):
     check(lib().hs_k_span_copy(_p(src), _p(dst), src.numel(), span_bytes, _stream()))
+
+
+def gemm_trace(enable: bool, n_ctas: int = 0):
+    out = np.zeros((max(n_ctas, 1), 8), dtype=np.uint64)
+    check(lib().hs_debug_gemm_trace(1 if enable else 0, out.ctypes.data if n_ctas else None, n_ctas))
+    return out[:n_ctas]

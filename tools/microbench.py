@@ -47,6 +47,26 @@ def gemm_cases(iters):
         del Ws
 
 
+def overhead_cases(iters):
+    """Fixed cost of the decode GEMM: time vs bytes at constant M (one tile row per SM)."""
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    for M, K in [(18944, 128), (18944, 256), (18944, 1024), (18944, 2048), (18944, 4096), (4096, 4096), (8192, 4096)]:
+        nrot = max(1, int(400e6 // (M * K * 2)) + 1)
+        Ws = [torch.randn(M, K, device="cuda").to(torch.bfloat16) for _ in range(nrot)]
+        X = torch.randn(16, K, device="cuda").to(torch.bfloat16)
+        out = torch.empty(1, M, device="cuda", dtype=torch.bfloat16)
+        us = timeit(lambda i: hs.k_gemm(Ws[i % nrot], X, 1, 0, out, ws=ws), iters)
+        print(json.dumps({"case": "overhead", "M": M, "K": K, "MB": round(M * K * 2 / 1e6, 2), "us": round(us, 2)}), flush=True)
+        del Ws
+    # the same GEMMs without the counter memset of hs_k_gemm (ws=None -> tiled split path) for reference
+    a = torch.zeros(1, 16, device="cuda", dtype=torch.float32)
+    t = torch.zeros(1, device="cuda", dtype=torch.int32)
+    us = timeit(lambda i: hs.k_argmax(a, t), iters)
+    print(json.dumps({"case": "tiny kernel (argmax 16)", "us": round(us, 2)}), flush=True)
+    us = timeit(lambda i: ws[:65536].zero_(), iters)
+    print(json.dumps({"case": "64KB memset", "us": round(us, 2)}), flush=True)
+
+
 def attn_cases(iters):
     for nh, d, ctx, B in [(32, 128, 544, 1), (40, 128, 576, 16), (32, 128, 4000, 1)]:
         nblk = B * ((ctx + 15) // 16) + 4
@@ -80,3 +100,5 @@ if __name__ == "__main__":
         gemm_cases(iters)
     if what in ("attn", "all"):
         attn_cases(iters)
+    if what in ("overhead", "all"):
+        overhead_cases(iters)
