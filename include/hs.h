@@ -117,8 +117,9 @@ hs_status hs_image_layout(const hs_model_cfg* cfg, hs_image_header* out);
 typedef struct {
   int32_t device;     /* CUDA ordinal (as seen by the process that will own the stage) */
   double h2d_gbps;    /* p_i: host->device bandwidth of this GPU's link, GB/s (10^9 B/s) */
-  int32_t link_group; /* GPUs sharing one host uplink share a group id (contention, NEXT) */
+  int32_t link_group; /* GPUs sharing one host uplink share a group id (hs_links_*) */
   uint64_t free_bytes;/* free HBM */
+  int32_t n_workers;  /* workers already running on this GPU (Alg. 1's "GPU sharing") */
 } hs_gpu;
 
 typedef struct {
@@ -144,6 +145,37 @@ typedef struct {
 hs_status hs_plan_stages(const hs_model_cfg* cfg, const hs_gpu* gpus, int32_t n_gpus,
                          int32_t pp, int32_t full_memory_stages, double t_prefill_s,
                          double t_hop_s, hs_plan* out);
+
+/* SLO-driven choice of s and w (Algorithm 1) on one box: for s = 1..max_pp
+ * and w = 0..s the GPUs are chosen by hs_plan_stages' selection rule, TTFT is Eq. 5 specialised
+ * (R9) and TPOT is Eq. 2 (t_d, t_n); among the SLO-feasible choices the one whose
+ * GPUs already host the fewest workers wins (ties: smaller s, then larger w).  If none is
+ * feasible, out = (1, 1, best full-capable GPU) and HS_E_INFEASIBLE is returned (the paper's
+ * "use single worker if no solution").  sharing (optional) = workers already on the chosen
+ * GPUs. */
+typedef struct {
+  double t_prefill_s, t_decode_s, t_hop_s; /* t_p, t_d, t_n (historical measurements) */
+  double slo_ttft_s, slo_tpot_s;
+  int32_t max_pp;                          /* paper: 4; north star: up to 8 */
+} hs_slo;
+hs_status hs_plan_auto(const hs_model_cfg* cfg, const hs_gpu* gpus, int32_t n_gpus,
+                       const hs_slo* slo, hs_plan* out, int32_t* sharing);
+
+/* Contention-aware admission of simultaneous cold starts sharing a host link group
+ * (§4.2, Eq. 3, Eq. 4; R17: the paper's per-server
+ * network bandwidth B becomes the bandwidth of a group of GPUs behind one host uplink).
+ * Units: bytes and seconds.  admit settles the group to `now` first, then accepts iff
+ * S_i <= B/(N+1) (D_i - now) for every listed worker and the candidate; settle applies
+ * S_i' = S_i - B/N (now - T') and drops workers with S_i' < 0. */
+typedef struct hs_links hs_links;
+hs_status hs_links_create(int32_t n_groups, const double* group_bytes_per_s, hs_links** out);
+hs_status hs_links_admit(hs_links* l, int32_t group, double pending_bytes, double deadline_s,
+                         double now_s, int32_t* accepted, int64_t* worker_id);
+hs_status hs_links_settle(hs_links* l, int32_t group, double now_s);
+hs_status hs_links_complete(hs_links* l, int32_t group, int64_t worker_id, double now_s);
+hs_status hs_links_pending(hs_links* l, int32_t group, int32_t max_n, int32_t* n,
+                           double* pending, int64_t* ids);
+hs_status hs_links_destroy(hs_links* l);
 
 /* Paper's predictors, exposed for the planner's tests (PAPER.md:398 Eq. 1, :417 Eq. 2,
  * :579-584 Eq. 5).  Bandwidth arrays have s entries; M in the same unit as b,p numerators. */

@@ -32,10 +32,10 @@ def eq5_ttft(t_cc, t_cu, t_l, M, s, w, b, p, t_p, t_n):
 
 
 def select_servers(full_capable, low_capable, s, w):
-    """full_capable / low_capable: lists of (server_id, ratio).  Returns s server ids:
-    the w smallest-ratio full-capable, then the s-w smallest-ratio of the merged rest;
-    ties broken by server id."""
-    key = lambda t: (t[1], t[0])  # noqa: E731
+    """full_capable / low_capable: lists of (server_id, ratio[, n_workers]).  Returns s server
+    ids: the w smallest-ratio full-capable, then the s-w smallest-ratio of the merged rest;
+    ratio ties broken by fewer running workers (R18), then server id."""
+    key = lambda t: (t[1], t[2] if len(t) > 2 else 0, t[0])  # noqa: E731
     fc = sorted(full_capable, key=key)
     if len(fc) < w:
         raise ValueError("infeasible")
@@ -65,14 +65,74 @@ def plan(cfg: dict, gpus, pp: int, full_memory_stages: int = 1, t_prefill_s=0.0,
     w = full_memory_stages stages reserve the whole model (stage 0 first), chosen by the
     selection rule with ratio 1/p; returns dict(pp, device, ranges, stage_bytes,
     full_memory, pred_ttft_s)."""
+    if pp > cfg["n_layers"]:
+        raise ValueError("infeasible")
     sb = stage_param_bytes(cfg, pp)
     model_bytes = embed_param_bytes(cfg) + final_param_bytes(cfg) + cfg["n_layers"] * layer_param_bytes(cfg)
     w = min(full_memory_stages, pp)
-    full = [(g["device"], 1.0 / g["h2d_gbps"]) for g in gpus if g["free_bytes"] >= model_bytes]
-    low = [(g["device"], 1.0 / g["h2d_gbps"]) for g in gpus
+    full = [(g["device"], 1.0 / g["h2d_gbps"], g.get("n_workers", 0)) for g in gpus if g["free_bytes"] >= model_bytes]
+    low = [(g["device"], 1.0 / g["h2d_gbps"], g.get("n_workers", 0)) for g in gpus
            if max(sb) <= g["free_bytes"] < model_bytes]
     devs = select_servers(full, low, pp, w)
     p = {g["device"]: g["h2d_gbps"] for g in gpus}
     pred = max(sb[k] / (p[devs[k]] * 1e9) for k in range(pp)) + t_prefill_s * (pp - w + w / pp) + t_hop_s * pp
     return dict(pp=pp, device=devs, ranges=split_layers(cfg["n_layers"], pp), stage_bytes=sb,
                 full_memory=[1 if k < w else 0 for k in range(pp)], pred_ttft_s=pred)
+
+
+def alg1(cfg: dict, gpus, t_p, t_d, t_n, slo_ttft, slo_tpot, max_pp=4):
+    """Algorithm 1 by exhaustive enumeration on one box: every (s, w) whose
+    selected GPUs exist and whose predicted TTFT (Eq. 5 specialised, R9) and TPOT (Eq. 2) meet
+    the SLOs is feasible; return the feasible choice with minimal GPU sharing (workers already
+    on the chosen GPUs), ties -> smaller s, then larger w; else the single-worker fallback.
+    Returns (plan, sharing, feasible)."""
+    best = None
+    for s in range(1, min(max_pp, cfg["n_layers"]) + 1):
+        for w in range(0, s + 1):
+            try:
+                p = plan(cfg, gpus, s, w, t_p, t_n)
+            except ValueError:
+                continue
+            if p["pred_ttft_s"] > slo_ttft or eq2_tpot(t_d, s, w, t_n) > slo_tpot:
+                continue
+            nw = {g["device"]: g.get("n_workers", 0) for g in gpus}
+            share = sum(nw[d] for d in p["device"])
+            key = (share, s, -w)
+            if best is None or key < best[0]:
+                best = (key, p, share)
+    if best is None:
+        p = plan(cfg, gpus, 1, 1, t_p, t_n)
+        nw = {g["device"]: g.get("n_workers", 0) for g in gpus}
+        return p, nw[p["device"][0]], False
+    return best[1], best[2], True
+
+
+class ContentionRegistry:
+    """Eq. 3 / Eq. 4 for one server (here: one host-link group), exactly as
+    written: admit iff S_i <= B/(N+1) (D_i - T) for all workers incl. the candidate; on each
+    change S_i' = S_i - B/N (T - T'), deleting workers with S_i' < 0."""
+
+    def __init__(self, B):
+        self.B, self.last, self.ws, self.next = B, 0.0, {}, 1
+
+    def settle(self, now):
+        assert now >= self.last
+        if self.ws:
+            dec = self.B / len(self.ws) * (now - self.last)
+            self.ws = {i: (S - dec, D) for i, (S, D) in self.ws.items() if S - dec >= 0}
+        self.last = now
+
+    def admit(self, S, D, now):
+        self.settle(now)
+        share = self.B / (len(self.ws) + 1)
+        ok = S <= share * (D - now) and all(Si <= share * (Di - now) for Si, Di in self.ws.values())
+        if not ok:
+            return False, 0
+        wid = self.next
+        self.next += 1
+        self.ws[wid] = (S, D)
+        return True, wid
+
+    def complete(self, wid, now):
+        self.settle(now)
+        self.ws.pop(wid, None)

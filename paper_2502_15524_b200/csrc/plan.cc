@@ -126,15 +126,19 @@ extern "C" hs_status hs_plan_stages(const hs_model_cfg* cfg, const hs_gpu* gpus,
   }
   // Selection rule with ratio 1/p_i (remote fetch absent: 1/b_i = 0).
   const int w = std::max(0, std::min<int>(full_memory_stages, pp));
-  struct Cand { double r; int dev; };
+  // ties in 1/p_i -> GPUs with fewer running workers first ("prioritizes free GPUs",
+  // PAPER.md:421; R18), then device id
+  struct Cand { double r; int nw; int dev; };
   std::vector<Cand> full, low;
   for (int i = 0; i < n_gpus; ++i) {
     if (gpus[i].h2d_gbps <= 0) { set_error("hs_plan_stages: h2d_gbps must be > 0"); return HS_E_INVAL; }
     const double r = 1.0 / gpus[i].h2d_gbps;
-    if (gpus[i].free_bytes >= model) full.push_back({r, gpus[i].device});
-    else if (gpus[i].free_bytes >= maxb) low.push_back({r, gpus[i].device});
+    if (gpus[i].free_bytes >= model) full.push_back({r, gpus[i].n_workers, gpus[i].device});
+    else if (gpus[i].free_bytes >= maxb) low.push_back({r, gpus[i].n_workers, gpus[i].device});
   }
-  auto less = [](const Cand& a, const Cand& b) { return a.r < b.r || (a.r == b.r && a.dev < b.dev); };
+  auto less = [](const Cand& a, const Cand& b) {
+    return a.r < b.r || (a.r == b.r && (a.nw < b.nw || (a.nw == b.nw && a.dev < b.dev)));
+  };
   std::stable_sort(full.begin(), full.end(), less);
   if ((int)full.size() < w) { set_error("hs_plan_stages: not enough full-memory GPUs"); return HS_E_INFEASIBLE; }
   std::vector<Cand> rest(full.begin() + w, full.end());

@@ -50,7 +50,12 @@ class Image(C.Structure):
 
 class Gpu(C.Structure):
     _fields_ = [("device", C.c_int32), ("h2d_gbps", C.c_double), ("link_group", C.c_int32),
-                ("free_bytes", C.c_uint64)]
+                ("free_bytes", C.c_uint64), ("n_workers", C.c_int32)]
+
+
+class Slo(C.Structure):
+    _fields_ = [("t_prefill_s", C.c_double), ("t_decode_s", C.c_double), ("t_hop_s", C.c_double),
+                ("slo_ttft_s", C.c_double), ("slo_tpot_s", C.c_double), ("max_pp", C.c_int32)]
 
 
 class Plan(C.Structure):
@@ -110,7 +115,8 @@ SYMBOLS = ["hs_image_layout", "hs_plan_stages", "hs_predict_ttft_eq1", "hs_predi
            "hs_debug_poison_weights", "hs_debug_launch_count", "hs_stage_timing_get", "hs_profile_enable",
            "hs_profile_read", "hs_debug_comm_selftest",
            "hs_k_gemm", "hs_k_rmsnorm", "hs_k_rope_kv", "hs_k_attention", "hs_k_argmax", "hs_k_embed",
-           "hs_k_span_copy", "hs_debug_gemm_trace"]
+           "hs_k_span_copy", "hs_debug_gemm_trace", "hs_plan_auto", "hs_links_create", "hs_links_admit",
+           "hs_links_settle", "hs_links_complete", "hs_links_pending", "hs_links_destroy"]
 
 _lib = None
 
@@ -161,6 +167,13 @@ def lib():
     L.hs_k_embed.argtypes = [VP, VP, VP, I32, I32, VP]
     L.hs_k_span_copy.argtypes = [VP, VP, I32, U64, VP]
     L.hs_debug_gemm_trace.argtypes = [I32, VP, I32]
+    L.hs_plan_auto.argtypes = [P(ModelCfg), P(Gpu), I32, P(Slo), P(Plan), P(I32)]
+    L.hs_links_create.argtypes = [I32, P(C.c_double), P(VP)]
+    L.hs_links_admit.argtypes = [VP, I32, C.c_double, C.c_double, C.c_double, P(I32), P(C.c_int64)]
+    L.hs_links_settle.argtypes = [VP, I32, C.c_double]
+    L.hs_links_complete.argtypes = [VP, I32, C.c_int64, C.c_double]
+    L.hs_links_pending.argtypes = [VP, I32, I32, P(I32), P(C.c_double), P(C.c_int64)]
+    L.hs_links_destroy.argtypes = [VP]
     _lib = L
     return L
 
@@ -181,9 +194,59 @@ def image_layout(cfg: dict) -> ImageHeader:
     return h
 
 
+def _gpus(gpus):
+    return (Gpu * len(gpus))(*[Gpu(g["device"], g["h2d_gbps"], g.get("link_group", 0), g["free_bytes"],
+                                   g.get("n_workers", 0)) for g in gpus])
+
+
+def plan_auto(cfg: dict, gpus, t_prefill_s, t_decode_s, t_hop_s, slo_ttft_s, slo_tpot_s, max_pp=4):
+    """Algorithm 1: returns (plan, sharing, feasible)."""
+    out, sh = Plan(), C.c_int32()
+    c = model_cfg(cfg)
+    slo = Slo(t_prefill_s, t_decode_s, t_hop_s, slo_ttft_s, slo_tpot_s, max_pp)
+    r = lib().hs_plan_auto(C.byref(c), _gpus(gpus), len(gpus), C.byref(slo), C.byref(out), C.byref(sh))
+    if r not in (0, 4):
+        check(r)
+    return out, sh.value, r == 0
+
+
+class Links:
+    """Eq. 3 / Eq. 4 contention registry over host-link groups (hs_links_*)."""
+
+    def __init__(self, group_bytes_per_s):
+        arr = (C.c_double * len(group_bytes_per_s))(*group_bytes_per_s)
+        self.h = C.c_void_p()
+        check(lib().hs_links_create(len(group_bytes_per_s), arr, C.byref(self.h)))
+
+    def admit(self, group, pending, deadline, now):
+        acc, wid = C.c_int32(), C.c_int64()
+        check(lib().hs_links_admit(self.h, group, pending, deadline, now, C.byref(acc), C.byref(wid)))
+        return bool(acc.value), wid.value
+
+    def settle(self, group, now):
+        check(lib().hs_links_settle(self.h, group, now))
+
+    def complete(self, group, wid, now):
+        check(lib().hs_links_complete(self.h, group, wid, now))
+
+    def pending(self, group):
+        n = C.c_int32()
+        check(lib().hs_links_pending(self.h, group, 0, C.byref(n), None, None))
+        pend = (C.c_double * max(n.value, 1))()
+        ids = (C.c_int64 * max(n.value, 1))()
+        check(lib().hs_links_pending(self.h, group, n.value, C.byref(n), pend, ids))
+        return {ids[i]: pend[i] for i in range(n.value)}
+
+    def __del__(self):
+        try:
+            lib().hs_links_destroy(self.h)
+        except Exception:  # noqa
+            pass
+
+
 def plan_stages(cfg: dict, gpus, pp: int, full_memory_stages: int = 1, t_prefill_s: float = 0.0,
                 t_hop_s: float = 0.0) -> Plan:
-    arr = (Gpu * len(gpus))(*[Gpu(g["device"], g["h2d_gbps"], g.get("link_group", 0), g["free_bytes"]) for g in gpus])
+    arr = _gpus(gpus)
     out = Plan()
     c = model_cfg(cfg)
     check(lib().hs_plan_stages(C.byref(c), arr, len(gpus), pp, full_memory_stages, t_prefill_s, t_hop_s, C.byref(out)))
