@@ -256,11 +256,21 @@ hs_status hs_decode_step(hs_group* g, int32_t n_seqs, const int64_t* seq_ids,
 hs_status hs_release_seq(hs_group* g, int64_t seq_id);
 
 typedef struct {
-  uint64_t weight_bytes; /* weight bytes migrated into the target */
+  uint64_t weight_bytes; /* weight bytes migrated into the target over NVLink */
   uint64_t kv_bytes;     /* KV bytes migrated into the target */
   double seconds;        /* device time of the migration (first copy start .. last end) */
   double pause_seconds;  /* host time from call entry to return (drain + migrate + rebind) */
+  uint64_t weight_bytes_host; /* weight bytes that arrived by the background host load */
 } hs_consolidate_stats;
+
+/* Paper-faithful background load ("the
+ * parameter manager loads the second part of model in background ... in low-priority CUDA
+ * streams"): the full-memory target stage streams the weight regions it lacks from its own
+ * host image over its own PCIe link, queued behind its critical load, while the group keeps
+ * serving pipelined.  A later hs_consolidate waits for it and then moves only the KV blocks
+ * (and any region not covered) over NVLink.  The target's image must cover the whole model.
+ * Errors: HS_E_INVAL (target not full-memory / not owned / image too small), HS_E_STATE. */
+hs_status hs_load_background_async(hs_group* g, int32_t target_stage, uint64_t chunk_bytes);
 
 /* Scale-down consolidation: drain in-flight work, copy the
  * weight regions the target lacks and gather the used KV blocks of every live sequence

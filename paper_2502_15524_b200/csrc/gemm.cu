@@ -356,6 +356,7 @@ struct SkParams {
   bf16* q_out;
   bf16* pool;
   int nh, hd;  // heads, head_dim
+  int nslots;
   unsigned long long* trace;  // optional per-CTA phase timestamps (globaltimer ns), 8 per CTA
 };
 
@@ -591,6 +592,7 @@ __global__ void __launch_bounds__(192, 1)
           for (int n = 0; n < p.N; ++n) {
             const float a = vals[ra * BN + n], b = vals[rb * BN + n];
             const int sl = p.slot[n];
+            if (sl < 0 || sl >= p.nslots) continue;  // never dereference an out-of-range slot
             const size_t blk = (size_t)(sl >> 4), off = (size_t)(sl & 15);
             if (region == 2) {
               bf16* vd = p.pool + (((blk * 2 + 1) * p.nh + head) * 16 + off) * p.hd;
@@ -984,7 +986,7 @@ static hs_status launch_sk(const GemmArgs& a, cudaStream_t st, bool* done) {
   p.epi = a.epi; p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr;
   p.fuse = f.kind; p.norm_w = f.norm_w; p.norm_out = f.norm_out; p.eps = f.eps;
   p.pos = f.pos; p.slot = f.slot; p.tab = f.rope_tab; p.q_out = f.q_out; p.pool = f.pool;
-  p.nh = f.n_heads; p.hd = f.head_dim;
+  p.nh = f.n_heads; p.hd = f.head_dim; p.nslots = f.nslots;
   p.trace = g_sk_trace;
   if (p.fuse == FUSE_NORM && a.epi != EPI_RESID) p.fuse = FUSE_NONE;
   launchk(gemm_sk_kernel<BN>, G, 192, C::SMEM, st, a.A->map, a.B[bi].map, p);

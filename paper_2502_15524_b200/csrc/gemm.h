@@ -44,6 +44,7 @@ struct GemmFusion {
   bf16* q_out = nullptr;
   bf16* pool = nullptr;
   int n_heads = 0, head_dim = 0;
+  int nslots = 1 << 30;     // KV slots in the pool (range check of slot[n])
   bool* applied = nullptr;  // set to true when the fusion ran (else the caller runs the op)
 };
 

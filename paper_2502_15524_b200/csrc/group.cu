@@ -90,6 +90,9 @@ struct Stage {
   cudaStream_t comp = nullptr, copy = nullptr;
   cudaEvent_t ev_embed = nullptr, ev_final = nullptr, ev_l0 = nullptr, ev_l1 = nullptr;
   cudaEvent_t ev_c0 = nullptr, ev_c1 = nullptr;  // start / end of the last call on comp
+  cudaEvent_t ev_bg0 = nullptr, ev_bg = nullptr; // background (host path) load start / end
+  bool bg_issued = false;
+  uint64_t bg_bytes = 0;
   bool called = false;
   std::vector<cudaEvent_t> ev_layer;
   bool load_issued = false;
@@ -210,7 +213,7 @@ static void free_stage(Stage& s) {
     if (s.h_meta) cudaFreeHost(s.h_meta);
     if (s.h_out) cudaFreeHost(s.h_out);
     for (auto e : s.ev_layer) if (e) cudaEventDestroy(e);
-    for (auto e : {s.ev_embed, s.ev_final, s.ev_l0, s.ev_l1, s.ev_c0, s.ev_c1}) if (e) cudaEventDestroy(e);
+    for (auto e : {s.ev_embed, s.ev_final, s.ev_l0, s.ev_l1, s.ev_c0, s.ev_c1, s.ev_bg0, s.ev_bg}) if (e) cudaEventDestroy(e);
     if (s.owns_streams && s.comp) cudaStreamDestroy(s.comp);
     if (s.owns_streams && s.copy) cudaStreamDestroy(s.copy);
   } else {
@@ -315,6 +318,8 @@ static hs_status setup_owned_stage(hs_group* g, int k) {
   HS_CUDA(cudaEventCreate(&s.ev_l1));
   HS_CUDA(cudaEventCreate(&s.ev_c0));
   HS_CUDA(cudaEventCreate(&s.ev_c1));
+  HS_CUDA(cudaEventCreate(&s.ev_bg0));
+  HS_CUDA(cudaEventCreate(&s.ev_bg));
   s.ev_layer.assign(c.n_layers, nullptr);
   for (int l = 0; l < c.n_layers; ++l) HS_CUDA(cudaEventCreateWithFlags(&s.ev_layer[l], cudaEventDisableTiming));
   // TMA descriptors: weights of every layer the arena holds, activation operands
@@ -487,6 +492,35 @@ static hs_status load_stage(hs_group* g, int k, uint64_t chunk) {
   return HS_OK;
 }
 
+// Background host-path load of the regions a full-memory target lacks.
+static hs_status load_background(hs_group* g, int tgt, uint64_t chunk) {
+  if (tgt < 0 || tgt >= (int)g->st.size()) HS_FAIL(HS_E_INVAL, "bad stage %d", tgt);
+  Stage& T = g->st[tgt];
+  if (!T.owned) return HS_OK;  // SPMD: only the target's process works
+  if (!T.full_memory) HS_FAIL(HS_E_INVAL, "stage %d is not a full-memory worker", tgt);
+  if (!T.load_issued) HS_FAIL(HS_E_STATE, "issue the critical load of the target first");
+  const hs_image_header& h = g->hdr;
+  if (T.img->data_offset > h.embed_off || T.img->data_offset + T.img->data_bytes < h.total_bytes)
+    HS_FAIL(HS_E_INVAL, "the target's host image must cover the whole model for a background load");
+  if (chunk == 0) chunk = kDefaultChunk;
+  DeviceGuard dg(T.device);
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(T.img->data);
+  HS_CUDA(cudaEventRecord(T.ev_bg0, T.copy));
+  T.bg_bytes = 0;
+  for (int k : g->active) {
+    if (k == tgt) continue;
+    const Stage& S = g->st[k];
+    for (uint64_t o = S.slice_begin; o < S.slice_end; o += chunk) {
+      const uint64_t n = std::min(chunk, S.slice_end - o);
+      HS_CUDA(cudaMemcpyAsync(T.wptr(o), src + (o - T.img->data_offset), n, cudaMemcpyHostToDevice, T.copy));
+    }
+    T.bg_bytes += g->plan.stage_bytes[k];
+  }
+  HS_CUDA(cudaEventRecord(T.ev_bg, T.copy));
+  T.bg_issued = true;
+  return HS_OK;
+}
+
 // ------------------------------------------------------------------ forward --------------
 struct CallMeta {
   int T = 0, n = 0, max_nq = 0, max_ctx = 0;
@@ -536,19 +570,21 @@ static hs_status run_layer(hs_group* g, Stage& s, int l, bf16*& x, const CallMet
   if (dec) {  // fused bf16 rounding + RoPE + paged KV write in the stream-K reduction
     a.fuse.kind = FUSE_ROPE; a.fuse.pos = pos; a.fuse.slot = slot; a.fuse.rope_tab = s.rope; a.fuse.q_out = s.q;
     a.fuse.pool = pool; a.fuse.n_heads = c.n_heads; a.fuse.head_dim = c.head_dim; a.fuse.applied = &applied;
+    a.fuse.nslots = g->kv.num_blocks * kBlock;
   }
   { ProfScope ps(g, s, PK_GEMM_QKV, dec, gemm_bytes(3.0 * H, T, H, 3.0 * H, false), 2.0 * 3 * H * T * H);
     HS_TRY(gemm(a, st)); }
   if (!applied) {
     ProfScope ps(g, s, PK_ROPE_KV, dec, 3 * TH2 + 3 * TH2, 0);
-    launch_rope_kv(s.qkv, pos, slot, s.rope, s.q, pool, T, c.n_heads, c.head_dim, st);
+    launch_rope_kv(s.qkv, pos, slot, s.rope, s.q, pool, T, c.n_heads, c.head_dim, g->kv.num_blocks * kBlock, st);
   }
   { ProfScope ps(g, s, PK_ATTN, dec, 2 * TH2 + 2.0 * 2 * H * m.kv_tokens, 4.0 * H * m.attn_pairs);
     if (m.decode)
       launch_attn_decode(s.q, pool, sd, m.n, m.max_ctx, tab, g->max_blocks, s.o, c.n_heads, c.head_dim,
-                         s.attn_ws, attn_decode_splits(m.max_ctx), s.ctr + kCounters / 2, st);
+                         s.attn_ws, attn_decode_splits(m.max_ctx), s.ctr + kCounters / 2, g->kv.num_blocks, st);
     else
-      launch_attn_prefill(s.q, pool, sd, m.n, m.max_nq, tab, g->max_blocks, s.o, c.n_heads, c.head_dim, st); }
+      launch_attn_prefill(s.q, pool, sd, m.n, m.max_nq, tab, g->max_blocks, s.o, c.n_heads, c.head_dim,
+                          g->kv.num_blocks, st); }
   a.fuse = GemmFusion{};
   applied = false;
   a.A = &L.wo; a.B = s.b_o; a.M = H; a.K = H; a.epi = EPI_RESID; a.out = hbuf; a.ldo = H; a.resid = x; a.ldr = H;
@@ -654,7 +690,7 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
         d_tok = reinterpret_cast<const int*>(s.comm + g->cl.tok_in);
       }
       ProfScope ps(g, s, PK_EMBED, dec, 4.0 * m.T * c.hidden, 0);
-      launch_embed(d_tok, E, s.xa, m.T, c.hidden, st);
+      launch_embed(d_tok, E, s.xa, m.T, c.hidden, c.vocab, st);
       x = s.xa;
     } else {
       ProfScope ps(g, s, PK_WAIT, dec, 0, 0);
@@ -732,6 +768,15 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
   if (err) {
     g->dead = true;
     HS_FAIL(HS_E_TIMEOUT, "a cross-stage wait timed out (peer never signalled)");
+  }
+  for (int k : g->active) {
+    if (!g->st[k].owned) continue;
+    DeviceGuard dg(g->st[k].device);
+    const unsigned bad = debug_bad_bits(true);
+    if (bad) {
+      g->dead = true;
+      HS_FAIL(HS_E_CUDA, "device range check failed (bits 0x%x: 1 token id, 2 KV slot, 4 block id)", bad);
+    }
   }
   g->last_ids = ids;
   return HS_OK;
@@ -885,9 +930,14 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
       if (k == tgt) continue;
       Stage& S = g->st[k];
       HS_TRY(open_peer_memory(g, S));
+      if (T.bg_issued) continue;  // the weights come over the target's own PCIe link
       add(reinterpret_cast<uint64_t>(S.arena + (S.slice_begin - S.arena_off0)), reinterpret_cast<uint64_t>(T.wptr(S.slice_begin)),
           S.slice_end - S.slice_begin);
       stats.weight_bytes += g->plan.stage_bytes[k];
+    }
+    if (T.bg_issued) {
+      HS_CUDA(cudaStreamWaitEvent(s2, T.ev_bg, 0));  // background host-path load must be complete
+      stats.weight_bytes_host = T.bg_bytes;
     }
     for (int k : g->active) {
       if (k == tgt) continue;
@@ -1166,4 +1216,12 @@ extern "C" hs_status hs_debug_comm_selftest(const hs_comm* comm) {
       HS_FAIL(HS_E_STATE, "allgather returned wrong bytes for rank %d", r);
   if (comm->barrier(comm->ctx) != 0) HS_FAIL(HS_E_STATE, "barrier failed");
   return HS_OK;
+}
+
+extern "C" hs_status hs_load_background_async(hs_group* g, int32_t target_stage, uint64_t chunk_bytes) {
+  if (!g) HS_FAIL(HS_E_INVAL, "null group");
+  if (g->dead) HS_FAIL(HS_E_CUDA, "group is dead");
+  if (std::find(g->active.begin(), g->active.end(), target_stage) == g->active.end())
+    HS_FAIL(HS_E_INVAL, "stage %d is not active", target_stage);
+  return load_background(g, target_stage, chunk_bytes);
 }

@@ -49,7 +49,7 @@ extern "C" hs_status hs_k_rope_kv(const void* qkv, const int32_t* pos, const int
                                   void* q_out, void* pool, int32_t T, int32_t nh, int32_t d, void* stream) {
   if (!qkv || !pos || !slot || !tab || !q_out || !pool || T <= 0 || (d != 64 && d != 128)) HS_FAIL(HS_E_INVAL, "bad args");
   launch_rope_kv(reinterpret_cast<const bf16*>(qkv), pos, slot, reinterpret_cast<const float2*>(tab),
-                 reinterpret_cast<bf16*>(q_out), reinterpret_cast<bf16*>(pool), T, nh, d,
+                 reinterpret_cast<bf16*>(q_out), reinterpret_cast<bf16*>(pool), T, nh, d, 1 << 30,
                  reinterpret_cast<cudaStream_t>(stream));
   HS_CUDA(cudaGetLastError());
   return HS_OK;
@@ -74,11 +74,11 @@ extern "C" hs_status hs_k_attention(const void* q, const void* pool, const int32
     if ((size_t)n * nh * 4 > (1u << 20)) HS_FAIL(HS_E_INVAL, "too many (seq, head) pairs");
     launch_attn_decode(reinterpret_cast<const bf16*>(q), reinterpret_cast<const bf16*>(pool), sd, n, max_ctx, tables,
                        max_blocks, reinterpret_cast<bf16*>(o), nh, d, reinterpret_cast<float*>(ws),
-                       attn_decode_splits(max_ctx), ctr[dev], st);
+                       attn_decode_splits(max_ctx), ctr[dev], 1 << 30, st);
   }
   else
     launch_attn_prefill(reinterpret_cast<const bf16*>(q), reinterpret_cast<const bf16*>(pool), sd, n, max_nq, tables,
-                        max_blocks, reinterpret_cast<bf16*>(o), nh, d, st);
+                        max_blocks, reinterpret_cast<bf16*>(o), nh, d, 1 << 30, st);
   HS_CUDA(cudaGetLastError());
   return HS_OK;
 }
@@ -92,7 +92,7 @@ extern "C" hs_status hs_k_argmax(const float* logits, int32_t V, int32_t n, int3
 
 extern "C" hs_status hs_k_embed(const int32_t* tok, const void* E, void* x, int32_t T, int32_t H, void* stream) {
   if (!tok || !E || !x || T <= 0 || H % 8) HS_FAIL(HS_E_INVAL, "bad args");
-  launch_embed(tok, reinterpret_cast<const bf16*>(E), reinterpret_cast<bf16*>(x), T, H,
+  launch_embed(tok, reinterpret_cast<const bf16*>(E), reinterpret_cast<bf16*>(x), T, H, 1 << 30,
                reinterpret_cast<cudaStream_t>(stream));
   HS_CUDA(cudaGetLastError());
   return HS_OK;

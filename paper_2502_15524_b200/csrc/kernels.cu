@@ -7,22 +7,43 @@
 
 namespace hs {
 
+// Data-dependent indices (token ids, KV slots, block ids) are range-checked on the device: an
+// out-of-range value is never dereferenced; it sets a bit in g_bad, which the host turns into
+// an error after the call (debug_bad_bits).
+__device__ unsigned g_bad = 0;
+__device__ __forceinline__ void flag_bad(unsigned bit) { atomicOr(&g_bad, bit); }
+
+unsigned debug_bad_bits(bool reset) {
+  unsigned v = 0;
+  cudaMemcpyFromSymbol(&v, g_bad, sizeof(v));
+  if (reset && v) {
+    const unsigned z = 0;
+    cudaMemcpyToSymbol(g_bad, &z, sizeof(z));
+  }
+  return v;
+}
+
 // ------------------------------------------------------------------ embedding (a5) -------
 __global__ void embed_kernel(const int* __restrict__ tok, const uint4* __restrict__ E,
-                             uint4* __restrict__ x, int H8) {
+                             uint4* __restrict__ x, int H8, int V) {
   PDL_LAUNCH();
   PDL_WAIT();
   const int t = blockIdx.x;
-  const uint4* src = E + (size_t)tok[t] * H8;
+  int id = tok[t];
+  if (id < 0 || id >= V) {
+    if (threadIdx.x == 0) flag_bad(1u);
+    id = 0;
+  }
+  const uint4* src = E + (size_t)id * H8;
   uint4* dst = x + (size_t)t * H8;
   for (int i = threadIdx.x; i < H8; i += blockDim.x) dst[i] = __ldg(src + i);
 }
 
-void launch_embed(const int* tok, const bf16* E, bf16* x, int T, int H, cudaStream_t st) {
+void launch_embed(const int* tok, const bf16* E, bf16* x, int T, int H, int V, cudaStream_t st) {
   count_launch();
   const int H8 = H / 8;
   launchk(embed_kernel, T, H8 < 512 ? H8 : 512, 0, st, tok, reinterpret_cast<const uint4*>(E),
-          reinterpret_cast<uint4*>(x), H8);
+          reinterpret_cast<uint4*>(x), H8, V);
 }
 
 // ------------------------------------------------------------------ RMSNorm (a6) ---------
@@ -98,13 +119,18 @@ void launch_rmsnorm(const bf16* x, const int* rows, const bf16* w, bf16* y, int 
 // ------------------------------------------------------------------ RoPE + KV write (a8) -
 __global__ void rope_kv_kernel(const bf16* __restrict__ qkv, const int* __restrict__ pos,
                                const int* __restrict__ slot, const float2* __restrict__ tab,
-                               bf16* __restrict__ q_out, bf16* __restrict__ pool, int nh, int d) {
+                               bf16* __restrict__ q_out, bf16* __restrict__ pool, int nh, int d, int nslots) {
   PDL_LAUNCH();
   PDL_WAIT();
   const int t = blockIdx.x;
   const int H = nh * d, hd = d / 2;
   const bf16* row = qkv + (size_t)t * 3 * H;
-  const int p = pos[t], s = slot[t];
+  const int p = pos[t];
+  int s = slot[t];
+  if (s < 0 || s >= nslots) {
+    if (threadIdx.x == 0) flag_bad(2u);
+    return;
+  }
   const size_t blk = (size_t)(s >> 4), off = (size_t)(s & 15);
   const float2* cs = tab + (size_t)p * hd;
   for (int idx = threadIdx.x; idx < nh * hd; idx += blockDim.x) {
@@ -129,9 +155,9 @@ __global__ void rope_kv_kernel(const bf16* __restrict__ qkv, const int* __restri
 }
 
 void launch_rope_kv(const bf16* qkv, const int* pos, const int* slot, const float2* tab, bf16* q_out,
-                    bf16* pool, int T, int nh, int d, cudaStream_t st) {
+                    bf16* pool, int T, int nh, int d, int nslots, cudaStream_t st) {
   count_launch();
-  launchk(rope_kv_kernel, T, 256, 0, st, qkv, pos, slot, tab, q_out, pool, nh, d);
+  launchk(rope_kv_kernel, T, 256, 0, st, qkv, pos, slot, tab, q_out, pool, nh, d, nslots);
 }
 
 // ------------------------------------------------------------------ attention (a9) -------
@@ -208,7 +234,7 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t&
 template <int D>
 __global__ void __launch_bounds__(128) attn_prefill_kernel(
     const bf16* __restrict__ q, const bf16* __restrict__ pool, const SeqDesc* __restrict__ seqs,
-    const int* __restrict__ tables, int max_blocks, bf16* __restrict__ o, int nh) {
+    const int* __restrict__ tables, int max_blocks, bf16* __restrict__ o, int nh, int nblocks) {
   PDL_LAUNCH();
   PDL_WAIT();
   constexpr int CH = D / 8;  // 16-byte chunks per row
@@ -255,9 +281,14 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(
       uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
       if (r < nk) {
         const int j = kc + r;
-        const size_t base = ((((size_t)tab[j >> 4] * 2) * nh + head) * 16 + (j & 15)) * D;
-        kv = reinterpret_cast<const uint4*>(pool + base)[c];
-        vv = reinterpret_cast<const uint4*>(pool + base + (size_t)nh * 16 * D)[c];
+        const int b = tab[j >> 4];
+        if (b >= 0 && b < nblocks) {
+          const size_t base = ((((size_t)b * 2) * nh + head) * 16 + (j & 15)) * D;
+          kv = reinterpret_cast<const uint4*>(pool + base)[c];
+          vv = reinterpret_cast<const uint4*>(pool + base + (size_t)nh * 16 * D)[c];
+        } else if (c == 0) {
+          flag_bad(4u);
+        }
       }
       Ks[r * CH + (c ^ (r & 7))] = kv;
       Vs[r * CH + (c ^ (r & 7))] = vv;
@@ -363,11 +394,11 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(
 }
 
 void launch_attn_prefill(const bf16* q, const bf16* pool, const SeqDesc* seqs, int n_seqs, int max_nq,
-                         const int* tables, int max_blocks, bf16* o, int nh, int d, cudaStream_t st) {
+                         const int* tables, int max_blocks, bf16* o, int nh, int d, int nblocks, cudaStream_t st) {
   count_launch();
   dim3 grid((max_nq + PF_Q - 1) / PF_Q, nh, n_seqs);
-  if (d == 128) launchk(attn_prefill_kernel<128>, grid, 128, 0, st, q, pool, seqs, tables, max_blocks, o, nh);
-  else launchk(attn_prefill_kernel<64>, grid, 128, 0, st, q, pool, seqs, tables, max_blocks, o, nh);
+  if (d == 128) launchk(attn_prefill_kernel<128>, grid, 128, 0, st, q, pool, seqs, tables, max_blocks, o, nh, nblocks);
+  else launchk(attn_prefill_kernel<64>, grid, 128, 0, st, q, pool, seqs, tables, max_blocks, o, nh, nblocks);
 }
 
 // Decode: CTA = (head, seq, split of DEC_KC = 64 keys).  The split's 4 block ids are read
@@ -381,7 +412,7 @@ template <int D>
 __global__ void __launch_bounds__(128) attn_decode_kernel(
     const bf16* __restrict__ q, const bf16* __restrict__ pool, const SeqDesc* __restrict__ seqs,
     const int* __restrict__ tables, int max_blocks, bf16* __restrict__ o, int nh, float* __restrict__ ws,
-    int splits, unsigned* __restrict__ ctr) {
+    int splits, unsigned* __restrict__ ctr, int nblocks) {
   PDL_LAUNCH();
   PDL_WAIT();
   __shared__ __align__(16) bf16 Ks[DEC_KC][D];
@@ -403,7 +434,14 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(
   float mx = -INFINITY, sum = 0.f, ov = 0.f;
   if (nk > 0) {
     const int* tab = tables + (size_t)s.table * max_blocks;
-    if (tid < DEC_KC / 16) blk[tid] = (k0 + tid * 16 < n_keys) ? tab[(k0 >> 4) + tid] : 0;
+    if (tid < DEC_KC / 16) {
+      int b = (k0 + tid * 16 < n_keys) ? tab[(k0 >> 4) + tid] : 0;
+      if (b < 0 || b >= nblocks) {
+        flag_bad(4u);
+        b = 0;
+      }
+      blk[tid] = b;
+    }
     const float scale = 1.4426950408889634f / sqrtf((float)D);
     for (int e = tid; e < D; e += 128) qs[e] = __bfloat162float(q[(size_t)s.q_start * H + head * D + e]) * scale;
     __syncthreads();
@@ -512,11 +550,11 @@ int attn_decode_splits(int max_ctx) { return (max_ctx + DEC_KC - 1) / DEC_KC; }
 
 void launch_attn_decode(const bf16* q, const bf16* pool, const SeqDesc* seqs, int n_seqs, int max_ctx,
                         const int* tables, int max_blocks, bf16* o, int nh, int d, float* ws, int splits,
-                        unsigned* ctr, cudaStream_t st) {
+                        unsigned* ctr, int nblocks, cudaStream_t st) {
   count_launch();
   dim3 grid(nh, n_seqs, splits);
-  if (d == 128) launchk(attn_decode_kernel<128>, grid, 128, 0, st, q, pool, seqs, tables, max_blocks, o, nh, ws, splits, ctr);
-  else launchk(attn_decode_kernel<64>, grid, 128, 0, st, q, pool, seqs, tables, max_blocks, o, nh, ws, splits, ctr);
+  if (d == 128) launchk(attn_decode_kernel<128>, grid, 128, 0, st, q, pool, seqs, tables, max_blocks, o, nh, ws, splits, ctr, nblocks);
+  else launchk(attn_decode_kernel<64>, grid, 128, 0, st, q, pool, seqs, tables, max_blocks, o, nh, ws, splits, ctr, nblocks);
 }
 
 // ------------------------------------------------------------------ argmax (a15) ---------

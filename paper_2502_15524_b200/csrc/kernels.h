@@ -13,7 +13,9 @@ struct SeqDesc {
 };
 
 // x[t] = E[tok[t]]  (a5)
-void launch_embed(const int* tok, const bf16* E, bf16* x, int T, int H, cudaStream_t st);
+void launch_embed(const int* tok, const bf16* E, bf16* x, int T, int H, int V, cudaStream_t st);
+// Bits set by kernels that met an out-of-range index (1: token id, 2: KV slot, 4: block id).
+unsigned debug_bad_bits(bool reset);
 
 // y[i] = bf16(x[row(i)] * rsqrt(mean(x^2)+eps) * w)   (a6; rows = null => row(i) = i)
 void launch_rmsnorm(const bf16* x, const int* rows, const bf16* w, bf16* y, int T, int H,
@@ -22,20 +24,22 @@ void launch_rmsnorm(const bf16* x, const int* rows, const bf16* w, bf16* y, int 
 // RoPE (rotate-half, fp32 table) on q,k of qkv [T, 3H]; writes q' [T,H] and k', v into the
 // paged pool of this layer: pool[block][K|V][head][16][d]  (a8)
 void launch_rope_kv(const bf16* qkv, const int* pos, const int* slot, const float2* rope_tab,
-                    bf16* q_out, bf16* pool, int T, int n_heads, int head_dim, cudaStream_t st);
+                    bf16* q_out, bf16* pool, int T, int n_heads, int head_dim, int nslots,
+                    cudaStream_t st);
 
 // Causal attention of the packed queries against the paged cache (a9).  Prefill layout:
 // one CTA per (16-query tile, head, sequence).
 void launch_attn_prefill(const bf16* q, const bf16* pool, const SeqDesc* seqs, int n_seqs,
                          int max_nq, const int* tables, int max_blocks, bf16* o, int n_heads,
-                         int head_dim, cudaStream_t st);
+                         int head_dim, int nblocks, cudaStream_t st);
 
 // Decode attention (one query per sequence) with deterministic split-KV (64 keys per split).
 // ws: n_seqs * n_heads * kv_splits * (head_dim + 2) floats; ctr: n_seqs * n_heads zeroed
 // arrival counters (self-resetting).
 void launch_attn_decode(const bf16* q, const bf16* pool, const SeqDesc* seqs, int n_seqs,
                         int max_ctx, const int* tables, int max_blocks, bf16* o, int n_heads,
-                        int head_dim, float* ws, int kv_splits, unsigned* ctr, cudaStream_t st);
+                        int head_dim, float* ws, int kv_splits, unsigned* ctr, int nblocks,
+                        cudaStream_t st);
 int attn_decode_splits(int max_ctx);
 
 // tokens[i] = argmax_v logits[i][v], ties -> lowest id (a15)

@@ -104,7 +104,7 @@ class ProfEntry(C.Structure):
 
 class ConsolidateStats(C.Structure):
     _fields_ = [("weight_bytes", C.c_uint64), ("kv_bytes", C.c_uint64), ("seconds", C.c_double),
-                ("pause_seconds", C.c_double)]
+                ("pause_seconds", C.c_double), ("weight_bytes_host", C.c_uint64)]
 
 
 # exported symbols (include/hs.h + include/hs_kernels.h); tests check every one is present
@@ -116,7 +116,8 @@ SYMBOLS = ["hs_image_layout", "hs_plan_stages", "hs_predict_ttft_eq1", "hs_predi
            "hs_profile_read", "hs_debug_comm_selftest",
            "hs_k_gemm", "hs_k_rmsnorm", "hs_k_rope_kv", "hs_k_attention", "hs_k_argmax", "hs_k_embed",
            "hs_k_span_copy", "hs_debug_gemm_trace", "hs_plan_auto", "hs_links_create", "hs_links_admit",
-           "hs_links_settle", "hs_links_complete", "hs_links_pending", "hs_links_destroy"]
+           "hs_links_settle", "hs_links_complete", "hs_links_pending", "hs_links_destroy",
+           "hs_load_background_async"]
 
 _lib = None
 
@@ -174,6 +175,7 @@ def lib():
     L.hs_links_complete.argtypes = [VP, I32, C.c_int64, C.c_double]
     L.hs_links_pending.argtypes = [VP, I32, I32, P(I32), P(C.c_double), P(C.c_int64)]
     L.hs_links_destroy.argtypes = [VP]
+    L.hs_load_background_async.argtypes = [VP, I32, U64]
     _lib = L
     return L
 
@@ -344,6 +346,9 @@ class Group:
 
     def load_stage_async(self, stage: int = -1, chunk_bytes: int = 0):
         check(lib().hs_load_stage_async(self.h, stage, chunk_bytes))
+
+    def load_background_async(self, target: int = 0, chunk_bytes: int = 0):
+        check(lib().hs_load_background_async(self.h, target, chunk_bytes))
 
     def load_stats(self, stage: int, wait: bool = True) -> LoadStats:
         s = LoadStats()

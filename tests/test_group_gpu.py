@@ -237,3 +237,29 @@ def test_two_gpu_pipeline_and_consolidation(image, oracle_run):
         toks, logits = g.decode_step([0, 1], hist[step - 1][0], want_logits=True)
         assert np.abs(logits - hist[step][1]).max() <= TOL
     g.destroy()
+
+
+@pytest.mark.parametrize("pp", [2, 4])
+def test_background_host_load_then_kv_only_consolidation(image, oracle_run, pp):
+    """the target loads the other stages' layers over its own host link in
+    the background while the group decodes pipelined; consolidation then moves only KV."""
+    prompts, hist, _ = oracle_run
+    g = make_group(image, pp)
+    g.load_stage_async(-1)
+    g.prefill([0, 1], prompts)
+    g.load_background_async(0)
+    for step in range(1, 9):
+        toks, logits = g.decode_step([0, 1], hist[step - 1][0], want_logits=True)
+        assert np.abs(logits - hist[step][1]).max() <= TOL
+    kv_before = {(s, l): g.read_kv(s, l, 0, 40) for s in (0, 1) for l in range(CFG["n_layers"])}
+    st = g.consolidate(0)
+    sb = hs.plan_stages(CFG, [dict(device=d, h2d_gbps=50.0, free_bytes=8 << 30) for d in range(pp)], pp, 1).as_dict()["stage_bytes"]
+    assert st.weight_bytes == 0 and st.weight_bytes_host == sum(sb) - sb[0] and st.kv_bytes > 0
+    for k, v in kv_before.items():
+        assert np.array_equal(g.read_kv(k[0], k[1], 0, 40), v)
+    h = hs.image_layout(CFG)
+    assert np.array_equal(g.read_weights(0, h.embed_off, h.total_bytes - h.embed_off), image.buf.numpy()[h.embed_off:])
+    for step in range(9, 20):
+        toks, logits = g.decode_step([0, 1], hist[step - 1][0], want_logits=True)
+        assert np.abs(logits - hist[step][1]).max() <= TOL
+    g.destroy()
