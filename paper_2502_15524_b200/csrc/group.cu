@@ -38,6 +38,7 @@ static constexpr uint64_t kDefaultChunk = 32ull << 20;
 static constexpr uint64_t kWorkspace = 64ull << 20;
 static constexpr int kSendCtas = 64;
 static constexpr uint64_t kCounters = 1 << 16;
+static constexpr int kMaxChunks = 4;  // prefill micro-batches
 
 // Comm block of a stage (one allocation, shared with peers): flags + token / hidden inputs.
 struct CommLayout {
@@ -291,7 +292,7 @@ static hs_status setup_owned_stage(hs_group* g, int k) {
     HS_ALLOC(s.rope, tab.size() * sizeof(float2));
     HS_CUDA(cudaMemcpy(s.rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
   }
-  s.meta_bytes = (size_t)T * 12 + (size_t)S * (8 + sizeof(SeqDesc) + (size_t)g->max_blocks * 4) + 1024;
+  s.meta_bytes = kMaxChunks * ((size_t)T * 12 + (size_t)S * (8 + sizeof(SeqDesc) + (size_t)g->max_blocks * 4) + 1024);
   HS_ALLOC(s.d_meta, s.meta_bytes);
   // mapped pinned staging: the SMs read call metadata / write tokens directly (see
   // launch_small_copy), so nothing small queues behind the weight stream on the copy engines
@@ -545,17 +546,18 @@ static void layout_meta(CallMeta& m, int max_blocks) {
 // this layer's attn_norm (fused into the previous layer's down-projection epilogue in decode);
 // on return it says whether s.nrm holds the next consumer's norm (next layer's attn_norm, or
 // the final norm into s.fin for the model's last layer).
-static hs_status run_layer(hs_group* g, Stage& s, int l, bf16*& x, const CallMeta& m, bool& normed, bool& fin_done) {
+static hs_status run_layer(hs_group* g, Stage& s, int l, const bf16* x, bf16* xout, const CallMeta& m,
+                           const uint8_t* meta, bool& normed, bool& fin_done) {
   const hs_model_cfg& c = g->cfg;
   const int H = c.hidden, T = m.T;
   LayerDev& L = s.layers[l];
   cudaStream_t st = s.comp;
-  const int* pos = reinterpret_cast<const int*>(s.d_meta + m.o_pos);
-  const int* slot = reinterpret_cast<const int*>(s.d_meta + m.o_slot);
-  const SeqDesc* sd = reinterpret_cast<const SeqDesc*>(s.d_meta + m.o_seqs);
-  const int* tab = reinterpret_cast<const int*>(s.d_meta + m.o_tab);
+  const int* pos = reinterpret_cast<const int*>(meta + m.o_pos);
+  const int* slot = reinterpret_cast<const int*>(meta + m.o_slot);
+  const SeqDesc* sd = reinterpret_cast<const SeqDesc*>(meta + m.o_seqs);
+  const int* tab = reinterpret_cast<const int*>(meta + m.o_tab);
   bf16* pool = s.kv_pool(l, g->kv_layer_bytes);
-  bf16* hbuf = (x == s.xb) ? s.xa : s.xb;
+  bf16* hbuf = s.xb;  // h = x + o W_o^T (temporary); x lives in xout's rows (in place after layer 0)
   const bool dec = m.decode;
   const double TH2 = 2.0 * T * H, F = c.ffn;
   if (!normed) {
@@ -603,7 +605,6 @@ static hs_status run_layer(hs_group* g, Stage& s, int l, bf16*& x, const CallMet
   a.resid = nullptr;
   { ProfScope ps(g, s, PK_GEMM_GU, dec, gemm_bytes(2 * F, T, H, F, false), 2.0 * 2 * F * T * H);
     HS_TRY(gemm(a, st)); }
-  bf16* xout = (hbuf == s.xa) ? s.xb : s.xa;
   a.A = &L.wd; a.B = s.b_act; a.M = H; a.K = c.ffn; a.epi = EPI_RESID; a.out = xout; a.ldo = H; a.resid = hbuf;
   a.ldr = H;
   applied = false;
@@ -625,95 +626,188 @@ static hs_status run_layer(hs_group* g, Stage& s, int l, bf16*& x, const CallMet
     HS_TRY(gemm(a, st)); }
   normed = applied && next_here;
   fin_done = applied && model_last;
-  x = xout;
   return HS_OK;
 }
 
 // Enqueues one call (prefill or decode) on every owned stage; returns after the tokens of
 // the call are on the host.
+//
+// Prefill through s > 1 stages is micro-batched (PAPER.md:399, 405-406:
+// the t_p terms of Eq. 1): every sequence's tokens are cut into m chunks (chunked prefill:
+// chunk c attends to the KV of chunks < c already in the cache), each stage hands chunk c to
+// the next stage as soon as it is through its layers, so stage k+1 works on chunk c while
+// stage k works on chunk c+1.  A stage whose weights are still streaming in runs layer-major
+// (every chunk of layer l as soon as layer l lands: it keeps pace with its PCIe link); a
+// resident stage runs chunk-major (hands chunk 0 on first).  Chunk c of the residual stream
+// lives in rows [R_c, R_c + T_c) of the stage buffers; hand-off flags carry epoch base + c.
+struct Chunk {
+  CallMeta m;
+  size_t meta_off = 0;
+  int row0 = 0;
+};
+
 static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int64_t>& ids,
                           const std::vector<int>& host_tokens, bool feedback, int32_t* out_tokens,
                           float* out_logits) {
   const hs_model_cfg& c = g->cfg;
-  const unsigned ep = ++g->epoch;
   const int first = g->active.front(), last = g->active.back();
-  CallMeta m = m0;
-  layout_meta(m, g->max_blocks);
+  // ---- chunking of prefill: depends on the shapes only (never on the number of stages), so
+  // PP = s stays bitwise equal to PP = 1; chunks keep > 64 tokens (tensor-core tile path,
+  // whose per-row results do not depend on the number of rows)
+  int nchunks = 1;
+  if (!m0.decode) {
+    int min_len = 1 << 30;
+    for (int i = 0; i < m0.n; ++i) min_len = std::min(min_len, g->seqs[ids[i]].ctx);
+    nchunks = std::max(1, std::min<int>({kMaxChunks, min_len / 16, m0.T / 128}));
+  }
+  const unsigned ep0 = g->epoch + 1;   // chunk c is handed over with flag value ep0 + c
+  g->epoch += nchunks;
+  const unsigned ep = g->epoch;        // the call's final epoch (token broadcast)
+  std::vector<Chunk> ch(nchunks);
+  {
+    size_t off = 0;
+    int row = 0;
+    for (int cidx = 0; cidx < nchunks; ++cidx) {
+      CallMeta m = m0;
+      m.T = 0;
+      m.max_nq = 0;
+      m.kv_tokens = 0;
+      m.attn_pairs = 0;
+      for (int i = 0; i < m0.n; ++i) {
+        const SeqState& ss = g->seqs[ids[i]];
+        const int n_new = m0.decode ? 1 : ss.ctx;
+        const int b = (int)((int64_t)n_new * cidx / nchunks), e = (int)((int64_t)n_new * (cidx + 1) / nchunks);
+        m.T += e - b;
+        m.max_nq = std::max(m.max_nq, e - b);
+        m.kv_tokens += (ss.ctx - n_new) + e;
+        m.attn_pairs += m0.decode ? ss.ctx : 0.5 * (double)(e - b) * (2.0 * ((ss.ctx - n_new) + b) + (e - b) + 1);
+      }
+      layout_meta(m, g->max_blocks);
+      ch[cidx].m = m;
+      ch[cidx].meta_off = off;
+      ch[cidx].row0 = row;
+      off += align_up(m.bytes, 256);
+      row += m.T;
+    }
+  }
   for (size_t ai = 0; ai < g->active.size(); ++ai) {
     const int k = g->active[ai];
     Stage& s = g->st[k];
     if (!s.owned) continue;
     if (!s.load_issued) HS_FAIL(HS_E_STATE, "stage %d: no load issued (call hs_load_stage_async first)", k);
-    if (m.bytes > s.meta_bytes) HS_FAIL(HS_E_INVAL, "call metadata too large");
+    if (ch.back().meta_off + ch.back().m.bytes > s.meta_bytes) HS_FAIL(HS_E_INVAL, "call metadata too large");
     DeviceGuard dg(s.device);
     cudaStream_t st = s.comp;
-    // host metadata (identical on every stage: centralised block manager)
-    uint8_t* hm = s.h_meta;
-    int* tok = reinterpret_cast<int*>(hm + m.o_tok);
-    int* pos = reinterpret_cast<int*>(hm + m.o_pos);
-    int* slot = reinterpret_cast<int*>(hm + m.o_slot);
-    int* lastr = reinterpret_cast<int*>(hm + m.o_last);
-    SeqDesc* sd = reinterpret_cast<SeqDesc*>(hm + m.o_seqs);
-    int* tab = reinterpret_cast<int*>(hm + m.o_tab);
-    // per-sequence descriptors, block tables and per-token positions / KV slots
-    int t = 0;
-    for (int i = 0; i < m.n; ++i) {
-      const SeqState& ss = g->seqs[ids[i]];
-      const int n_new = m.decode ? 1 : ss.ctx;  // prefill: ctx == prompt length
-      const int p0 = ss.ctx - n_new;
-      sd[i].q_start = t;
-      sd[i].n_q = n_new;
-      sd[i].pos0 = p0;
-      for (int j = 0; j < n_new; ++j) {
-        const int p = p0 + j;
-        pos[t] = p;
-        slot[t] = ss.blocks[p / kBlock] * kBlock + p % kBlock;
-        tok[t] = host_tokens.empty() ? 0 : host_tokens[t];
-        ++t;
+    // host metadata (identical on every stage: centralised block manager), one block per chunk
+    int tglob = 0;
+    for (int cidx = 0; cidx < nchunks; ++cidx) {
+      const CallMeta& m = ch[cidx].m;
+      uint8_t* hm = s.h_meta + ch[cidx].meta_off;
+      int* tok = reinterpret_cast<int*>(hm + m.o_tok);
+      int* pos = reinterpret_cast<int*>(hm + m.o_pos);
+      int* slot = reinterpret_cast<int*>(hm + m.o_slot);
+      int* lastr = reinterpret_cast<int*>(hm + m.o_last);
+      SeqDesc* sd = reinterpret_cast<SeqDesc*>(hm + m.o_seqs);
+      int* tab = reinterpret_cast<int*>(hm + m.o_tab);
+      int t = 0;
+      for (int i = 0; i < m.n; ++i) {
+        const SeqState& ss = g->seqs[ids[i]];
+        const int n_new = m.decode ? 1 : ss.ctx;  // prefill: ctx == prompt length
+        const int b = (int)((int64_t)n_new * cidx / nchunks), e = (int)((int64_t)n_new * (cidx + 1) / nchunks);
+        const int p0 = ss.ctx - n_new + b;
+        sd[i].q_start = t;
+        sd[i].n_q = e - b;
+        sd[i].pos0 = p0;
+        sd[i].table = i;
+        // host tokens are packed per sequence: sequence i's token j is at offset start_i + j
+        int start_i = 0;
+        if (!host_tokens.empty())
+          for (int q = 0; q < i; ++q) start_i += m.decode ? 1 : g->seqs[ids[q]].ctx;
+        for (int j = b; j < e; ++j) {
+          const int pp = ss.ctx - n_new + j;
+          pos[t] = pp;
+          slot[t] = ss.blocks[pp / kBlock] * kBlock + pp % kBlock;
+          tok[t] = host_tokens.empty() ? 0 : host_tokens[start_i + j];
+          ++t;
+        }
+        lastr[i] = t - 1;
+        for (int bb = 0; bb < g->max_blocks; ++bb)
+          tab[(size_t)i * g->max_blocks + bb] = bb < (int)ss.blocks.size() ? ss.blocks[bb] : 0;
       }
-      lastr[i] = t - 1;
-      for (int b = 0; b < g->max_blocks; ++b)
-        tab[(size_t)i * g->max_blocks + b] = b < (int)ss.blocks.size() ? ss.blocks[b] : 0;
-      sd[i].table = i;
+      tglob += t;
     }
+    (void)tglob;
     HS_CUDA(cudaEventRecord(s.ev_c0, st));
-    launch_small_copy(hm, s.d_meta, m.bytes, st);
-    const int* d_tok = reinterpret_cast<const int*>(s.d_meta + m.o_tok);
-    const bool dec = m.decode;
-    bf16* x = nullptr;
-    if (k == first) {
-      if (s.lb == 0) HS_CUDA(cudaStreamWaitEvent(st, s.ev_embed, 0));
-      const bf16* E = reinterpret_cast<const bf16*>(s.wptr(g->hdr.embed_off));
-      if (feedback) {
+    launch_small_copy(s.h_meta, s.d_meta, ch.back().meta_off + ch.back().m.bytes, st);
+    const bool dec = m0.decode;
+    const bool is_first = k == first, is_last = k == last;
+    Stage* nx = is_last ? nullptr : &g->st[g->active[ai + 1]];
+    const int H = c.hidden;
+    auto meta_of = [&](int cidx) { return s.d_meta + ch[cidx].meta_off; };
+    auto xrows = [&](int cidx) { return s.xa + (size_t)ch[cidx].row0 * H; };
+    auto in_rows = [&](int cidx) { return reinterpret_cast<bf16*>(s.comm + g->cl.x_in) + (size_t)ch[cidx].row0 * H; };
+    // stage input of chunk cidx: embedding (first stage) or the hand-off buffer
+    auto stage_input = [&](int cidx) -> hs_status {
+      if (is_first) {
+        if (cidx == 0 && s.lb == 0) HS_CUDA(cudaStreamWaitEvent(st, s.ev_embed, 0));
+        const bf16* E = reinterpret_cast<const bf16*>(s.wptr(g->hdr.embed_off));
+        const int* d_tok = reinterpret_cast<const int*>(meta_of(cidx) + ch[cidx].m.o_tok);
+        if (feedback) {
+          ProfScope ps(g, s, PK_WAIT, dec, 0, 0);
+          launch_wait(s.flag_tok(), ep0 - 1, s.err(), st);
+          d_tok = reinterpret_cast<const int*>(s.comm + g->cl.tok_in);
+        }
+        ProfScope ps(g, s, PK_EMBED, dec, 4.0 * ch[cidx].m.T * H, 0);
+        launch_embed(d_tok, E, xrows(cidx), ch[cidx].m.T, H, c.vocab, st);
+      } else {
         ProfScope ps(g, s, PK_WAIT, dec, 0, 0);
-        launch_wait(s.flag_tok(), ep - 1, s.err(), st);
-        d_tok = reinterpret_cast<const int*>(s.comm + g->cl.tok_in);
+        launch_wait(s.flag_x(), ep0 + cidx, s.err(), st);
       }
-      ProfScope ps(g, s, PK_EMBED, dec, 4.0 * m.T * c.hidden, 0);
-      launch_embed(d_tok, E, s.xa, m.T, c.hidden, c.vocab, st);
-      x = s.xa;
-    } else {
-      ProfScope ps(g, s, PK_WAIT, dec, 0, 0);
-      launch_wait(s.flag_x(), ep, s.err(), st);
-      x = reinterpret_cast<bf16*>(s.comm + g->cl.x_in);
-    }
+      return HS_OK;
+    };
+    auto hand_off = [&](int cidx) {
+      ProfScope ps(g, s, PK_SEND, dec, 2.0 * ch[cidx].m.T * H, 0);
+      launch_send(xrows(cidx), reinterpret_cast<uint8_t*>(nx->comm + g->cl.x_in) + (size_t)ch[cidx].row0 * H * 2,
+                  (uint64_t)ch[cidx].m.T * H * 2, s.done(), nx->flag_x(), ep0 + cidx, kSendCtas, st);
+    };
     bool normed = false, fin_done = false;
-    for (int l = s.lb; l < s.le; ++l) {
-      HS_CUDA(cudaStreamWaitEvent(st, s.ev_layer[l], 0));
-      if (m.decode && l + 1 == c.n_layers) HS_CUDA(cudaStreamWaitEvent(st, s.ev_final, 0));  // fused final norm
-      HS_TRY(run_layer(g, s, l, x, m, normed, fin_done));
-    }
-    if (k != last) {
-      Stage& nx = g->st[g->active[ai + 1]];
-      ProfScope ps(g, s, PK_SEND, dec, 2.0 * m.T * c.hidden, 0);
-      launch_send(x, nx.comm + g->cl.x_in, (uint64_t)m.T * c.hidden * 2, s.done(), nx.flag_x(), ep, kSendCtas, st);
+    // layer-major while this stage's weights are still arriving, chunk-major once resident
+    const bool loading = nchunks > 1 && is_first && cudaEventQuery(s.ev_l1) == cudaErrorNotReady;
+    cudaGetLastError();
+    if (nchunks == 1 || !loading) {
+      for (int cidx = 0; cidx < nchunks; ++cidx) {
+        HS_TRY(stage_input(cidx));
+        normed = false;
+        for (int l = s.lb; l < s.le; ++l) {
+          HS_CUDA(cudaStreamWaitEvent(st, s.ev_layer[l], 0));
+          if (dec && l + 1 == c.n_layers) HS_CUDA(cudaStreamWaitEvent(st, s.ev_final, 0));  // fused final norm
+          const bf16* xin = (l == s.lb && !is_first) ? in_rows(cidx) : xrows(cidx);
+          HS_TRY(run_layer(g, s, l, xin, xrows(cidx), ch[cidx].m, meta_of(cidx), normed, fin_done));
+        }
+        if (!is_last) hand_off(cidx);
+      }
     } else {
+      for (int cidx = 0; cidx < nchunks; ++cidx) HS_TRY(stage_input(cidx));
+      for (int l = s.lb; l < s.le; ++l) {
+        HS_CUDA(cudaStreamWaitEvent(st, s.ev_layer[l], 0));
+        for (int cidx = 0; cidx < nchunks; ++cidx) {
+          bool nrm = false, fd = false;
+          const bf16* xin = (l == s.lb && !is_first) ? in_rows(cidx) : xrows(cidx);
+          HS_TRY(run_layer(g, s, l, xin, xrows(cidx), ch[cidx].m, meta_of(cidx), nrm, fd));
+          if (l + 1 == s.le && !is_last) hand_off(cidx);
+        }
+      }
+    }
+    if (is_last) {
+      const Chunk& lc = ch.back();
+      const CallMeta& m = lc.m;
       if (s.le == c.n_layers) HS_CUDA(cudaStreamWaitEvent(st, s.ev_final, 0));
-      const int* d_last = reinterpret_cast<const int*>(s.d_meta + m.o_last);
+      const int* d_last = reinterpret_cast<const int*>(meta_of(nchunks - 1) + m.o_last);
       if (!fin_done) {
         ProfScope ps(g, s, PK_RMSNORM, dec, 4.0 * m.n * c.hidden, 0);
-        launch_rmsnorm(x, d_last, reinterpret_cast<const bf16*>(s.wptr(g->hdr.final_off + g->hdr.t_final_norm)),
-                       s.fin, m.n, c.hidden, c.rms_eps, st);
+        launch_rmsnorm(xrows(nchunks - 1), d_last,
+                       reinterpret_cast<const bf16*>(s.wptr(g->hdr.final_off + g->hdr.t_final_norm)), s.fin, m.n,
+                       c.hidden, c.rms_eps, st);
       }
       GemmArgs a{};
       a.A = &s.lm; a.B = s.b_fin; a.M = c.vocab; a.N = m.n; a.K = c.hidden; a.epi = EPI_F32; a.out = s.logits;
@@ -739,15 +833,16 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
       if (out_logits)
         HS_CUDA(cudaMemcpyAsync(out_logits, s.logits, (size_t)m.n * c.vocab * 4, cudaMemcpyDeviceToHost, st));
     }
-    if (k != last && g->spmd) {  // non-last SPMD ranks read the broadcast tokens
+    if (!is_last && g->spmd) {  // non-last SPMD ranks read the broadcast tokens
       launch_wait(s.flag_tok(), ep, s.err(), st);
-      launch_small_copy(s.comm + g->cl.tok_in, s.h_out, align_up((uint64_t)m.n * 4, 16), st);
+      launch_small_copy(s.comm + g->cl.tok_in, s.h_out, align_up((uint64_t)m0.n * 4, 16), st);
     }
-    launch_small_copy(s.comm, s.h_out + align_up((uint64_t)m.n, 4), 16, st);  // flags + err word
+    launch_small_copy(s.comm, s.h_out + align_up((uint64_t)m0.n, 4), 16, st);  // flags + err word
     HS_CUDA(cudaEventRecord(s.ev_c1, st));
     s.called = true;
   }
   // wait for the result on the stage(s) this process owns
+  const int n = m0.n;
   int err = 0;
   bool got = false;
   for (int k : g->active) {
@@ -759,9 +854,9 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
       g->dead = true;
       HS_FAIL(HS_E_CUDA, "stage %d: %s", k, cudaGetErrorString(e));
     }
-    err |= s.h_out[align_up((uint64_t)m.n, 4) + CommLayout::ERR / 4];
+    err |= s.h_out[align_up((uint64_t)n, 4) + CommLayout::ERR / 4];
     if (k == last || (g->spmd && !got)) {
-      memcpy(out_tokens, s.h_out, (size_t)m.n * 4);
+      memcpy(out_tokens, s.h_out, (size_t)n * 4);
       got = true;
     }
   }
