@@ -432,10 +432,11 @@ struct SkCfg {
   static constexpr int B_BYTES = BN * 64 * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // BN <= 32: 5 stages (~100 KB) so two CTAs fit an SM: the next kernel's CTA (PDL) becomes
-  // resident and prefetches its weights while this one drains
-  static constexpr int STAGES = BN >= 64 ? 6 : 5;
+  // resident and prefetches its weights while this one drains.  BN = 128 (small-tile-count
+  // prefill chunks) uses 4 stages and no RoPE staging buffer.
+  static constexpr int STAGES = BN >= 128 ? 4 : (BN >= 64 ? 6 : 5);
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int VALS_BYTES = 128 * BN * 4;  // tile values for the RoPE pairing
+  static constexpr int VALS_BYTES = BN <= 64 ? 128 * BN * 4 : 0;  // tile values for the RoPE pairing
   static constexpr int SMEM = STAGES * STAGE_BYTES + VALS_BYTES + 1024 + 512;
 };
 
@@ -972,7 +973,8 @@ static hs_status launch_sk(const GemmArgs& a, cudaStream_t st, bool* done) {
   const uint64_t ctr_bytes = align_up((uint64_t)(tiles + 1) * 4, 256);
   if (ctr_bytes + (uint64_t)tiles * maxp * BN * 128 * 4 > a.workspace_bytes || !a.counters) return HS_OK;
   const GemmFusion& f = a.fuse;
-  if (f.kind == FUSE_ROPE && (a.epi != EPI_BF16 || (f.head_dim != 64 && f.head_dim != 128))) return HS_OK;
+  if (f.kind == FUSE_ROPE && (a.epi != EPI_BF16 || (f.head_dim != 64 && f.head_dim != 128) || BN > 64)) return HS_OK;
+  if (f.kind == FUSE_NORM && BN > 64) return HS_OK;
   static bool attr_set[64] = {};
   if (dev < 64 && !attr_set[dev]) {
     HS_CUDA(cudaFuncSetAttribute(gemm_sk_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -1039,9 +1041,14 @@ hs_status gemm(const GemmArgs& a, cudaStream_t st) {
     int dev = 0;
     cudaGetDevice(&dev);
     const int G = num_sms(dev), mt = a.M / 128;
-    const long long c128 = cdiv((long long)mt * cdiv(a.N, 128), G) * 128;
-    const long long c256 = cdiv((long long)mt * cdiv(a.N, 256), G) * 256;
-    return c256 < c128 ? launch_tp<256>(a, st) : launch_tp<128>(a, st);
+    // too few 128-token tiles to fill the SMs (prefill chunks x small M): tiled kernel with
+    // deterministic split-K below (its reduction is one fully parallel pass)
+    if (!(a.workspace && (long long)mt * cdiv(a.N, 128) < G))
+    {
+      const long long c128 = cdiv((long long)mt * cdiv(a.N, 128), G) * 128;
+      const long long c256 = cdiv((long long)mt * cdiv(a.N, 256), G) * 256;
+      return c256 < c128 ? launch_tp<256>(a, st) : launch_tp<128>(a, st);
+    }
   }
   const int tiles = (a.M / 128) * (int)cdiv(a.N, BN);
   const int nkb = a.K / 64;

@@ -38,7 +38,8 @@ static constexpr uint64_t kDefaultChunk = 32ull << 20;
 static constexpr uint64_t kWorkspace = 64ull << 20;
 static constexpr int kSendCtas = 64;
 static constexpr uint64_t kCounters = 1 << 16;
-static constexpr int kMaxChunks = 4;  // prefill micro-batches
+static constexpr int kMaxChunks = 4;       // prefill micro-batches
+static constexpr int kChunkTokens = 1024;  // minimum tokens per micro-batch
 
 // Comm block of a stage (one allocation, shared with peers): flags + token / hidden inputs.
 struct CommLayout {
@@ -652,13 +653,16 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
   const hs_model_cfg& c = g->cfg;
   const int first = g->active.front(), last = g->active.back();
   // ---- chunking of prefill: depends on the shapes only (never on the number of stages), so
-  // PP = s stays bitwise equal to PP = 1; chunks keep > 64 tokens (tensor-core tile path,
-  // whose per-row results do not depend on the number of rows)
+  // PP = s stays bitwise equal to PP = 1.  A chunk keeps >= kChunkTokens tokens: below that a
+  // chunk's GEMMs fall under the B200 ridge point (every chunk re-reads the layer's weights;
+  // ~210 flop/byte needs ~210 tokens per weight read), and micro-batching would cost more than
+  // the pipelining saves (measured: 4 x 128-token chunks of a 512-token prompt made PP=2 TTFT
+  // 6 ms slower).
   int nchunks = 1;
   if (!m0.decode) {
     int min_len = 1 << 30;
     for (int i = 0; i < m0.n; ++i) min_len = std::min(min_len, g->seqs[ids[i]].ctx);
-    nchunks = std::max(1, std::min<int>({kMaxChunks, min_len / 16, m0.T / 128}));
+    nchunks = std::max(1, std::min<int>({kMaxChunks, min_len / 16, m0.T / kChunkTokens}));
   }
   const unsigned ep0 = g->epoch + 1;   // chunk c is handed over with flag value ep0 + c
   g->epoch += nchunks;

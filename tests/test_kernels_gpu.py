@@ -51,6 +51,7 @@ GEMM_CASES = [  # (M, K, N)
     (256, 256, 1), (256, 256, 16), (384, 256, 37), (256, 512, 64), (512, 256, 130),
     (768, 256, 300), (256, 768, 1100), (128, 64, 5),
     (2048, 4096, 7), (1536, 2048, 64), (4096, 11008, 3),  # stream-K (decode) path when ws is given
+    (4096, 4096, 128), (2048, 1024, 200),                 # prefill chunks: tiled split-K / persistent
 ]
 
 
