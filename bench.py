@@ -137,7 +137,7 @@ def run_ours(args):
         pp = 1
     hdr = hs.image_layout(cfg)
     gpus = [dict(device=i, h2d_gbps=PCIE_H2D_GBS, free_bytes=torch.cuda.mem_get_info(local)[1]) for i in range(pp)]
-    plan = hs.plan_stages(cfg, gpus, pp, 1)
+    plan = hs.plan_stages(cfg, gpus, pp, pp if args.scale_up else 1)
     for k in range(pp):
         plan.device[k] = k if world > 1 else local
     pd = plan.as_dict()
@@ -188,7 +188,7 @@ def run_ours(args):
         dev = 0.0
         t2 = time.perf_counter()
         for _ in range(dsteps):
-            g.decode_step(ids)
+            last_toks, _ = g.decode_step(ids)
             dev += g.timing(stage).call_ms
         r["decode_host"] = time.perf_counter() - t2
         r["decode_dev"] = dev / 1e3
@@ -197,6 +197,29 @@ def run_ours(args):
             for _ in range(PROFILE_STEPS):
                 g.decode_step(ids)
             g.profile(False)
+        if consolidate and args.scale_up:
+            # every stage becomes an endpoint (all-gather of the weights + each sequence's KV)
+            eps, st = g.scale_up()
+            r["cons_s"], r["cons_pause"] = st.seconds, st.pause_seconds
+            r["cons_bytes"] = st.weight_bytes + st.kv_bytes
+            r["cons_w"], r["cons_kv"], r["cons_w_host"] = st.weight_bytes, st.kv_bytes, 0
+            ep = eps[0]
+            if rank == 0:  # sequence 0 lives on endpoint 0
+                dev2 = 0.0
+                t3 = time.perf_counter()
+                ep.decode_step(ids, last_toks)
+                for _ in range(dsteps - 1):
+                    ep.decode_step(ids)
+                    dev2 += ep.timing(0).call_ms
+                r["decode2_host"] = time.perf_counter() - t3
+                r["decode2_dev"] = dev2 / 1e3
+            r["prof"] = g.profile_read(reset=True) if profile else {}
+            barrier()
+            for e in eps:
+                e.destroy()
+            g.destroy()
+            state["g"] = None
+            return r
         if consolidate:
             st = g.consolidate(0)
             r["cons_s"] = st.seconds
@@ -324,7 +347,8 @@ def run_ours(args):
         if consolidate:
             cs = statistics.median(s["cons_s"] for s in steps)
             cb = statistics.median(s["cons_bytes"] for s in steps)
-            out["consolidation"] = {"bytes": int(cb), "weight_bytes": int(steps[0]["cons_w"]), "kv_bytes": int(steps[0]["cons_kv"]),
+            out["consolidation"] = {"mode": "scale-up (all-gather to every stage)" if args.scale_up else "scale-down to stage 0",
+                                    "bytes": int(cb), "weight_bytes": int(steps[0]["cons_w"]), "kv_bytes": int(steps[0]["cons_kv"]),
                                     "weight_bytes_via_host_background": int(steps[0]["cons_w_host"]),
                                     "seconds": round(cs, 5), "gbs": round(cb / cs / 1e9, 1),
                                     "frac_of_nvlink_900": round(cb / cs / 1e9 / NVLINK_GBS, 4),
@@ -412,6 +436,9 @@ def main():
     ap.add_argument("--decode-steps", type=int, default=64)
     ap.add_argument("--chunk-mb", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scale-up", action="store_true",
+                    help="N>1: every stage becomes a standalone endpoint (scale-up consolidation) instead of "
+                         "scale-down into stage 0")
     ap.add_argument("--bg-load", action="store_true",
                     help="N>1: the target loads the other stages' weights over its own PCIe link in the "
                          "background after the first token (paper's mechanism); consolidation moves KV only")

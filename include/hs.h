@@ -280,6 +280,19 @@ hs_status hs_load_background_async(hs_group* g, int32_t target_stage, uint64_t c
  * HS_E_STATE, HS_E_CUDA. */
 hs_status hs_consolidate(hs_group* g, int32_t target_stage, hs_consolidate_stats* out);
 
+/* Scale-up consolidation ("converting all cold-start
+ * workers into individual serving endpoints"): every stage becomes a standalone single-stage
+ * group holding the whole model.  Each stage pulls the weight slices it lacks from the other
+ * stages over NVLink (an all-gather: every GPU receives (s-1)/s of the model concurrently) and
+ * the KV blocks, for the layers it lacks, of the live sequences assigned to it (same block
+ * ids).  seq_owner[i] is the endpoint (stage index) of the i-th live sequence in ascending
+ * seq-id order (NULL: round-robin).  Every stage must be full-memory.  On success the group
+ * is emptied (destroy it) and out[k] (local mode: k = 0..pp-1; SPMD: out[0] = this rank's
+ * endpoint) receive the new groups; stats (optional) sums the migrated bytes.
+ * Errors: HS_E_INVAL (a stage not full-memory, bad owner), HS_E_STATE, HS_E_CUDA. */
+hs_status hs_scale_up(hs_group* g, const int32_t* seq_owner, int32_t n_live, hs_group** out,
+                      hs_consolidate_stats* stats);
+
 hs_status hs_group_destroy(hs_group* g);
 const char* hs_last_error(void);
 

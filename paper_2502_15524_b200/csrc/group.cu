@@ -1097,6 +1097,160 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
   return HS_OK;
 }
 
+
+// ------------------------------------------------------------------ scale-up ---------------
+static hs_status scale_up(hs_group* g, const int32_t* owner_in, int32_t n_live, hs_group** out,
+                          hs_consolidate_stats* out_stats) {
+  const auto t_enter = std::chrono::steady_clock::now();
+  if (g->dead) HS_FAIL(HS_E_CUDA, "group is dead");
+  if (!out) HS_FAIL(HS_E_INVAL, "null out");
+  const hs_model_cfg& c = g->cfg;
+  const int np = (int)g->active.size();
+  for (int k : g->active)
+    if (!g->st[k].full_memory) HS_FAIL(HS_E_INVAL, "stage %d is not a full-memory worker", k);
+  // live sequences in ascending id order -> owner endpoint
+  std::vector<int64_t> live;
+  for (auto& kv : g->seqs) live.push_back(kv.first);
+  if (owner_in && n_live != (int)live.size()) HS_FAIL(HS_E_INVAL, "n_live %d != %zu live sequences", n_live, live.size());
+  std::map<int64_t, int> owner;
+  for (size_t i = 0; i < live.size(); ++i) {
+    const int o = owner_in ? owner_in[i] : g->active[i % np];
+    if (std::find(g->active.begin(), g->active.end(), o) == g->active.end()) HS_FAIL(HS_E_INVAL, "bad owner %d", o);
+    owner[live[i]] = o;
+  }
+  // drain every stage ("wait for all on-the-fly batches")
+  for (int k : g->active) {
+    Stage& s = g->st[k];
+    if (!s.owned) continue;
+    DeviceGuard dg(s.device);
+    HS_CUDA(cudaStreamSynchronize(s.comp));
+    HS_CUDA(cudaStreamSynchronize(s.copy));
+  }
+  if (g->spmd && g->comm.barrier(g->comm.ctx) != 0) HS_FAIL(HS_E_STATE, "barrier failed");
+  hs_consolidate_stats tot{};
+  const uint64_t piece = 64ull << 10;
+  struct Pending { int k; CopyDesc* d; cudaEvent_t e0, e1; };
+  std::vector<Pending> pend;
+  for (int t : g->active) {  // every stage pulls what it lacks, all GPUs concurrently
+    Stage& T = g->st[t];
+    if (!T.owned) continue;
+    DeviceGuard dg(T.device);
+    std::vector<CopyDesc> list;
+    auto add = [&](uint64_t src, uint64_t dst, uint64_t bytes) {
+      for (uint64_t o = 0; o < bytes; o += piece) list.push_back({src + o, dst + o, std::min(piece, bytes - o)});
+    };
+    for (int k : g->active) {
+      if (k == t) continue;
+      Stage& S = g->st[k];
+      HS_TRY(open_peer_memory(g, S));
+      add(reinterpret_cast<uint64_t>(S.arena + (S.slice_begin - S.arena_off0)), reinterpret_cast<uint64_t>(T.wptr(S.slice_begin)),
+          S.slice_end - S.slice_begin);
+      tot.weight_bytes += g->plan.stage_bytes[k];
+      for (int l = S.lb; l < S.le; ++l)
+        for (auto& kvp : g->seqs) {
+          if (owner[kvp.first] != t) continue;
+          for (int b : kvp.second.blocks) {
+            add(reinterpret_cast<uint64_t>(S.kv_pool(l, g->kv_layer_bytes)) + (uint64_t)b * g->kv_block_bytes,
+                reinterpret_cast<uint64_t>(T.kv_pool(l, g->kv_layer_bytes)) + (uint64_t)b * g->kv_block_bytes,
+                g->kv_block_bytes);
+            tot.kv_bytes += g->kv_block_bytes;
+          }
+        }
+    }
+    Pending p{t, nullptr, nullptr, nullptr};
+    HS_CUDA(cudaEventCreate(&p.e0));
+    HS_CUDA(cudaEventCreate(&p.e1));
+    if (!list.empty()) {
+      HS_CUDA(cudaMalloc(&p.d, list.size() * sizeof(CopyDesc)));
+      HS_CUDA(cudaMemcpy(p.d, list.data(), list.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+    }
+    HS_CUDA(cudaEventRecord(p.e0, T.comp));
+    launch_copy_list(p.d, (int)list.size(), 8 * num_sms(T.device), T.comp);
+    HS_CUDA(cudaEventRecord(p.e1, T.comp));
+    pend.push_back(p);
+  }
+  double secs = 0;
+  for (auto& p : pend) {
+    DeviceGuard dg(g->st[p.k].device);
+    HS_CUDA(cudaEventSynchronize(p.e1));
+    float ms = 0;
+    HS_CUDA(cudaEventElapsedTime(&ms, p.e0, p.e1));
+    secs = std::max(secs, (double)ms / 1e3);
+    cudaEventDestroy(p.e0);
+    cudaEventDestroy(p.e1);
+    if (p.d) cudaFree(p.d);
+  }
+  tot.seconds = secs;
+  if (g->spmd && g->comm.barrier(g->comm.ctx) != 0) HS_FAIL(HS_E_STATE, "barrier failed");
+  // split: each owned stage becomes a single-stage group with its sequences
+  int n_out = 0;
+  std::vector<int> owned_stages;
+  for (int k : g->active)
+    if (g->st[k].owned) owned_stages.push_back(k);
+  for (int k : owned_stages) {
+    Stage& S = g->st[k];
+    std::unique_ptr<hs_group> ng(new hs_group());
+    ng->cfg = g->cfg;
+    ng->hdr = g->hdr;
+    ng->kv = g->kv;
+    ng->cl = g->cl;
+    ng->kv_layer_bytes = g->kv_layer_bytes;
+    ng->kv_block_bytes = g->kv_block_bytes;
+    ng->max_blocks = g->max_blocks;
+    ng->plan = g->plan;
+    ng->plan.pp = 1;
+    ng->plan.device[0] = S.device;
+    ng->plan.layer_begin[0] = 0;
+    ng->plan.layer_end[0] = c.n_layers;
+    ng->plan.full_memory[0] = 1;
+    ng->plan.stage_bytes[0] = g->hdr.param_bytes;
+    ng->plan.slice_begin[0] = g->hdr.embed_off;
+    ng->plan.slice_end[0] = g->hdr.total_bytes;
+    ng->st.resize(1);
+    ng->st[0] = std::move(S);
+    S = Stage{};  // the old group no longer owns anything of this stage
+    S.owned = false;
+    Stage& T = ng->st[0];
+    T.idx = 0;
+    T.lb = 0;
+    T.le = c.n_layers;
+    T.slice_begin = g->hdr.embed_off;
+    T.slice_end = g->hdr.total_bytes;
+    if (!T.owns_streams) {  // stages that shared a device's streams get their own
+      DeviceGuard dg(T.device);
+      int lo = 0, hi = 0;
+      HS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      HS_CUDA(cudaStreamCreateWithPriority(&T.comp, cudaStreamNonBlocking, hi));
+      HS_CUDA(cudaStreamCreateWithPriority(&T.copy, cudaStreamNonBlocking, lo));
+      T.owns_streams = true;
+    }
+    for (int l = 0; l < c.n_layers; ++l)
+      if (!T.layers[l].maps) HS_TRY(make_layer_maps(ng.get(), T, l));
+    {
+      DeviceGuard dg(T.device);
+      for (int l = 0; l < c.n_layers; ++l) HS_CUDA(cudaEventRecord(T.ev_layer[l], T.copy));
+      HS_CUDA(cudaEventRecord(T.ev_embed, T.copy));
+      HS_CUDA(cudaEventRecord(T.ev_final, T.copy));
+      HS_CUDA(cudaMemset(T.comm, 0, 16));  // flags restart with the new group's epochs
+      HS_CUDA(cudaDeviceSynchronize());
+    }
+    T.load_issued = true;
+    ng->active = {0};
+    for (int b = 0; b < g->kv.num_blocks; ++b) ng->free_blocks.insert(b);
+    for (auto& kvp : g->seqs)
+      if (owner[kvp.first] == k) {
+        ng->seqs[kvp.first] = kvp.second;
+        for (int b : kvp.second.blocks) ng->free_blocks.erase(b);
+      }
+    out[n_out++] = ng.release();
+  }
+  // the old group keeps only remote views (closed by destroy)
+  g->active.clear();
+  tot.pause_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_enter).count();
+  if (out_stats) *out_stats = tot;
+  return HS_OK;
+}
+
 }  // namespace hs
 
 // ------------------------------------------------------------------ C ABI -----------------
@@ -1159,6 +1313,14 @@ extern "C" hs_status hs_release_seq(hs_group* g, int64_t seq_id) {
 extern "C" hs_status hs_consolidate(hs_group* g, int32_t target_stage, hs_consolidate_stats* out) {
   if (!g) HS_FAIL(HS_E_INVAL, "null group");
   hs_status r = consolidate(g, target_stage, out);
+  if (r == HS_E_CUDA) g->dead = true;
+  return r;
+}
+
+extern "C" hs_status hs_scale_up(hs_group* g, const int32_t* seq_owner, int32_t n_live, hs_group** out,
+                                 hs_consolidate_stats* stats) {
+  if (!g) HS_FAIL(HS_E_INVAL, "null group");
+  hs_status r = scale_up(g, seq_owner, n_live, out, stats);
   if (r == HS_E_CUDA) g->dead = true;
   return r;
 }

@@ -117,7 +117,7 @@ SYMBOLS = ["hs_image_layout", "hs_plan_stages", "hs_predict_ttft_eq1", "hs_predi
            "hs_k_gemm", "hs_k_rmsnorm", "hs_k_rope_kv", "hs_k_attention", "hs_k_argmax", "hs_k_embed",
            "hs_k_span_copy", "hs_debug_gemm_trace", "hs_plan_auto", "hs_links_create", "hs_links_admit",
            "hs_links_settle", "hs_links_complete", "hs_links_pending", "hs_links_destroy",
-           "hs_load_background_async"]
+           "hs_load_background_async", "hs_scale_up"]
 
 _lib = None
 
@@ -176,6 +176,7 @@ def lib():
     L.hs_links_pending.argtypes = [VP, I32, I32, P(I32), P(C.c_double), P(C.c_int64)]
     L.hs_links_destroy.argtypes = [VP]
     L.hs_load_background_async.argtypes = [VP, I32, U64]
+    L.hs_scale_up.argtypes = [VP, P(I32), I32, P(VP), P(ConsolidateStats)]
     _lib = L
     return L
 
@@ -383,6 +384,26 @@ class Group:
         s = ConsolidateStats()
         check(lib().hs_consolidate(self.h, target, C.byref(s)))
         return s
+
+    def scale_up(self, seq_owner=None):
+        """Every stage becomes a standalone endpoint; returns (list of Group, stats).  This group
+        is emptied (destroy it).  The first decode of each endpoint must pass in_tokens."""
+        pp = self.plan.pp
+        outs = (C.c_void_p * pp)()
+        st = ConsolidateStats()
+        if seq_owner is not None:
+            arr = (C.c_int32 * len(seq_owner))(*seq_owner)
+            check(lib().hs_scale_up(self.h, arr, len(seq_owner), outs, C.byref(st)))
+        else:
+            check(lib().hs_scale_up(self.h, None, 0, outs, C.byref(st)))
+        groups = []
+        for i in range(pp if self._comm is None else 1):
+            g = Group.__new__(Group)
+            g.cfg, g.plan, g._c, g._img, g._keep, g._stage_imgs, g._kv, g._comm = \
+                self.cfg, self.plan, self._c, self._img, self._keep, self._stage_imgs, self._kv, None
+            g.h = C.c_void_p(outs[i])
+            groups.append(g)
+        return groups, st
 
     def info(self):
         pp, owned = C.c_int32(), C.c_int32()

@@ -263,3 +263,41 @@ def test_background_host_load_then_kv_only_consolidation(image, oracle_run, pp):
         toks, logits = g.decode_step([0, 1], hist[step - 1][0], want_logits=True)
         assert np.abs(logits - hist[step][1]).max() <= TOL
     g.destroy()
+
+
+def test_scale_up_every_stage_becomes_an_endpoint(image, oracle_run):
+    """PP=2 with both stages full-memory; after 8 steps
+    every stage becomes a standalone endpoint holding the whole model and the KV of the
+    sequences assigned to it; each endpoint then decodes its sequence alone == PP=1 run."""
+    prompts, hist, _ = oracle_run
+    n = torch.cuda.device_count()
+    gpus = [dict(device=d, h2d_gbps=50.0, free_bytes=8 << 30) for d in range(max(n, 2))]
+    plan = hs.plan_stages(CFG, gpus, 2, 2)
+    plan.device[0] = plan.device[1] = 0
+    g = hs.Group(CFG, plan, image, num_blocks=64, max_seqs=8, max_tokens=256)
+    g.load_stage_async(-1)
+    g1 = make_group(image, 1)
+    g1.load_stage_async(-1)
+    g.prefill([0, 1], prompts)
+    g1.prefill([0, 1], prompts)
+    for step in range(1, 9):
+        g.decode_step([0, 1], hist[step - 1][0])
+        g1.decode_step([0, 1], hist[step - 1][0])
+    kv_before = {(s_, l): g.read_kv(s_, l, 0, 40) for s_ in (0, 1) for l in range(CFG["n_layers"])}
+    eps, st = g.scale_up([0, 1])  # seq 0 -> endpoint 0, seq 1 -> endpoint 1
+    assert len(eps) == 2 and st.kv_bytes > 0
+    h = hs.image_layout(CFG)
+    for k, e in enumerate(eps):
+        assert e.info()[0] == 1
+        assert np.array_equal(e.read_weights(0, h.embed_off, h.total_bytes - h.embed_off), image.buf.numpy()[h.embed_off:])
+        for l in range(CFG["n_layers"]):
+            assert np.array_equal(e.read_kv(k, l, 0, 40), kv_before[(k, l)])
+    for step in range(9, 20):
+        ref = g1.decode_step([0, 1], hist[step - 1][0], want_logits=True)
+        for k, e in enumerate(eps):
+            t, lg = e.decode_step([k], [hist[step - 1][0][k]], want_logits=True)
+            assert t[0] == ref[0][k] and np.array_equal(lg[0], ref[1][k])
+    for e in eps:
+        e.destroy()
+    g.destroy()
+    g1.destroy()
