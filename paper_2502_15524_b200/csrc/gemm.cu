@@ -1041,9 +1041,9 @@ hs_status gemm(const GemmArgs& a, cudaStream_t st) {
     int dev = 0;
     cudaGetDevice(&dev);
     const int G = num_sms(dev), mt = a.M / 128;
-    // too few 128-token tiles to fill the SMs (prefill chunks x small M): tiled kernel with
-    // deterministic split-K below (its reduction is one fully parallel pass)
-    if (!(a.workspace && (long long)mt * cdiv(a.N, 128) < G))
+    // too few 128-token tiles to fill half the SMs (prefill chunks x small M): tiled kernel
+    // with deterministic split-K below (its reduction is one fully parallel pass)
+    if (!(a.workspace && 2LL * mt * cdiv(a.N, 128) <= G))
     {
       const long long c128 = cdiv((long long)mt * cdiv(a.N, 128), G) * 128;
       const long long c256 = cdiv((long long)mt * cdiv(a.N, 256), G) * 256;
