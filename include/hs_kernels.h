@@ -26,7 +26,8 @@ hs_status hs_k_rmsnorm(const void* x, const int32_t* rows, const void* w, void* 
 hs_status hs_k_rope_kv(const void* qkv, const int32_t* pos, const int32_t* slot, const void* tab,
                        void* q_out, void* pool, int32_t T, int32_t n_heads, int32_t head_dim,
                        void* stream);
-/* seqs: int32 [n][4] = {q_start, n_q, pos0, table_row}; tables int32 [n][max_blocks]. */
+/* seqs: int32 [n][4] = {q_start, n_q, pos0, table_row}; tables int32 [n][max_blocks].
+ * decode != 0: one query per sequence and table_row must equal the sequence's index. */
 hs_status hs_k_attention(const void* q, const void* pool, const int32_t* seqs, int32_t n_seqs,
                          int32_t max_nq, int32_t max_ctx, const int32_t* tables, int32_t max_blocks,
                          void* o, int32_t n_heads, int32_t head_dim, int32_t decode, void* ws,

@@ -6,6 +6,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -547,8 +548,19 @@ static void layout_meta(CallMeta& m, int max_blocks) {
 // this layer's attn_norm (fused into the previous layer's down-projection epilogue in decode);
 // on return it says whether s.nrm holds the next consumer's norm (next layer's attn_norm, or
 // the final norm into s.fin for the model's last layer).
+// HS_DEBUG_SKIP (timing experiments only; results are garbage): bit 1 attention, 2 QKV,
+// 4 O-proj, 8 gate_up, 16 down, 32 norm kernels
+static int debug_skip() {
+  static int v = [] {
+    const char* e = getenv("HS_DEBUG_SKIP");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 static hs_status run_layer(hs_group* g, Stage& s, int l, const bf16* x, bf16* xout, const CallMeta& m,
                            const uint8_t* meta, bool& normed, bool& fin_done) {
+  const int skip = m.decode ? debug_skip() : 0;
   const hs_model_cfg& c = g->cfg;
   const int H = c.hidden, T = m.T;
   LayerDev& L = s.layers[l];
@@ -561,7 +573,7 @@ static hs_status run_layer(hs_group* g, Stage& s, int l, const bf16* x, bf16* xo
   bf16* hbuf = s.xb;  // h = x + o W_o^T (temporary); x lives in xout's rows (in place after layer 0)
   const bool dec = m.decode;
   const double TH2 = 2.0 * T * H, F = c.ffn;
-  if (!normed) {
+  if (!normed && !(skip & 32)) {
     ProfScope ps(g, s, PK_RMSNORM, dec, 2 * TH2 + 2.0 * H, 0);
     if (dec && H <= 8192) launch_rownorm_decode(x, L.attn_norm, s.nrm, T, H, c.rms_eps, st);
     else launch_rmsnorm(x, nullptr, L.attn_norm, s.nrm, T, H, c.rms_eps, st);
@@ -575,13 +587,18 @@ static hs_status run_layer(hs_group* g, Stage& s, int l, const bf16* x, bf16* xo
     a.fuse.pool = pool; a.fuse.n_heads = c.n_heads; a.fuse.head_dim = c.head_dim; a.fuse.applied = &applied;
     a.fuse.nslots = g->kv.num_blocks * kBlock;
   }
-  { ProfScope ps(g, s, PK_GEMM_QKV, dec, gemm_bytes(3.0 * H, T, H, 3.0 * H, false), 2.0 * 3 * H * T * H);
-    HS_TRY(gemm(a, st)); }
+  if (!(skip & 2)) {
+    ProfScope ps(g, s, PK_GEMM_QKV, dec, gemm_bytes(3.0 * H, T, H, 3.0 * H, false), 2.0 * 3 * H * T * H);
+    HS_TRY(gemm(a, st));
+  } else {
+    applied = true;
+  }
   if (!applied) {
     ProfScope ps(g, s, PK_ROPE_KV, dec, 3 * TH2 + 3 * TH2, 0);
     launch_rope_kv(s.qkv, pos, slot, s.rope, s.q, pool, T, c.n_heads, c.head_dim, g->kv.num_blocks * kBlock, st);
   }
-  { ProfScope ps(g, s, PK_ATTN, dec, 2 * TH2 + 2.0 * 2 * H * m.kv_tokens, 4.0 * H * m.attn_pairs);
+  if (!(skip & 1)) {
+    ProfScope ps(g, s, PK_ATTN, dec, 2 * TH2 + 2.0 * 2 * H * m.kv_tokens, 4.0 * H * m.attn_pairs);
     if (m.decode)
       launch_attn_decode(s.q, pool, sd, m.n, m.max_ctx, tab, g->max_blocks, s.o, c.n_heads, c.head_dim,
                          s.attn_ws, attn_decode_splits(m.max_ctx), s.ctr + kCounters / 2, g->kv.num_blocks, st);
@@ -595,8 +612,12 @@ static hs_status run_layer(hs_group* g, Stage& s, int l, const bf16* x, bf16* xo
     a.fuse.kind = FUSE_NORM; a.fuse.norm_w = L.ffn_norm; a.fuse.norm_out = s.nrm; a.fuse.eps = c.rms_eps;
     a.fuse.applied = &applied;
   }
-  { ProfScope ps(g, s, PK_GEMM_O, dec, gemm_bytes(H, T, H, H, true), 2.0 * H * T * H);
-    HS_TRY(gemm(a, st)); }
+  if (!(skip & 4)) {
+    ProfScope ps(g, s, PK_GEMM_O, dec, gemm_bytes(H, T, H, H, true), 2.0 * H * T * H);
+    HS_TRY(gemm(a, st));
+  } else {
+    applied = true;
+  }
   if (!applied) {
     ProfScope ps(g, s, PK_RMSNORM, dec, 2 * TH2 + 2.0 * H, 0);
     launch_rmsnorm(hbuf, nullptr, L.ffn_norm, s.nrm, T, H, c.rms_eps, st);
@@ -604,8 +625,10 @@ static hs_status run_layer(hs_group* g, Stage& s, int l, const bf16* x, bf16* xo
   a.fuse = GemmFusion{};
   a.A = &L.wgu; a.B = s.b_nrm; a.M = 2 * c.ffn; a.K = H; a.epi = EPI_SILU_MUL; a.out = s.act; a.ldo = c.ffn;
   a.resid = nullptr;
-  { ProfScope ps(g, s, PK_GEMM_GU, dec, gemm_bytes(2 * F, T, H, F, false), 2.0 * 2 * F * T * H);
-    HS_TRY(gemm(a, st)); }
+  if (!(skip & 8)) {
+    ProfScope ps(g, s, PK_GEMM_GU, dec, gemm_bytes(2 * F, T, H, F, false), 2.0 * 2 * F * T * H);
+    HS_TRY(gemm(a, st));
+  }
   a.A = &L.wd; a.B = s.b_act; a.M = H; a.K = c.ffn; a.epi = EPI_RESID; a.out = xout; a.ldo = H; a.resid = hbuf;
   a.ldr = H;
   applied = false;
@@ -623,8 +646,12 @@ static hs_status run_layer(hs_group* g, Stage& s, int l, const bf16* x, bf16* xo
       a.fuse.norm_out = s.fin;
     }
   }
-  { ProfScope ps(g, s, PK_GEMM_DOWN, dec, gemm_bytes(H, T, F, H, true), 2.0 * H * T * F);
-    HS_TRY(gemm(a, st)); }
+  if (!(skip & 16)) {
+    ProfScope ps(g, s, PK_GEMM_DOWN, dec, gemm_bytes(H, T, F, H, true), 2.0 * H * T * F);
+    HS_TRY(gemm(a, st));
+  } else {
+    applied = next_here || model_last;
+  }
   normed = applied && next_here;
   fin_done = applied && model_last;
   return HS_OK;

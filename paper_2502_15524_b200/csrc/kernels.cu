@@ -4,6 +4,7 @@
 #include "kernels.h"
 
 #include <cfloat>
+#include <type_traits>
 
 namespace hs {
 
@@ -401,160 +402,174 @@ void launch_attn_prefill(const bf16* q, const bf16* pool, const SeqDesc* seqs, i
   else launchk(attn_prefill_kernel<64>, grid, 128, 0, st, q, pool, seqs, tables, max_blocks, o, nh, nblocks);
 }
 
-// Decode: CTA = (head, seq, split of DEC_KC = 64 keys).  The split's 4 block ids are read
-// first, then every K/V row of the split is issued as 16-byte loads into registers at once
-// (memory-level parallelism, no dependent per-key chain) and staged in shared memory;
-// scores with 2 threads per key, block softmax, P.V with one thread per output dimension.
-// The CTA that finishes a (seq, head) last merges the splits in split order (deterministic).
-constexpr int DEC_KC = 64;
+// Decode (one query per sequence), latency-oriented: CTA = (head, seq, split), 16 warps; warp
+// w owns KV blocks b0 + w, b0 + w + 16, ... of the split.  For a 16-token block lane l loads
+// dims [E l, E l + E) of all 16 K rows and 16 V rows straight into registers (32 independent
+// 8-byte loads in flight per lane, no shared-memory staging), computes the 16 scores with warp
+// all-reduces, and keeps an online softmax (m, l, o[E]) per warp.  Warps are merged through
+// shared memory in warp order; splits (long contexts only: DEC_BLOCKS_PER_SPLIT blocks each)
+// are merged by the CTA that finishes a (seq, head) last, in split order.  Deterministic.
+constexpr int DEC_WARPS = 16;
+constexpr int DEC_BLOCKS_PER_SPLIT = 64;  // 1024 tokens per CTA
 
 template <int D>
-__global__ void __launch_bounds__(128) attn_decode_kernel(
+__global__ void __launch_bounds__(DEC_WARPS * 32) attn_decode_kernel(
     const bf16* __restrict__ q, const bf16* __restrict__ pool, const SeqDesc* __restrict__ seqs,
     const int* __restrict__ tables, int max_blocks, bf16* __restrict__ o, int nh, float* __restrict__ ws,
     int splits, unsigned* __restrict__ ctr, int nblocks) {
   PDL_LAUNCH();
   PDL_WAIT();
-  __shared__ __align__(16) bf16 Ks[DEC_KC][D];
-  __shared__ __align__(16) bf16 Vs[DEC_KC][D];
-  __shared__ float qs[D];
-  __shared__ float ps[DEC_KC];
-  __shared__ float red[8];
-  __shared__ float part[128];
-  __shared__ int blk[DEC_KC / 16];
+  constexpr int E = D / 32;  // dims per lane (4 or 2)
+  __shared__ float sm_m[DEC_WARPS], sm_l[DEC_WARPS];
+  __shared__ float sm_o[DEC_WARPS][D];
   __shared__ int is_last;
   const int head = blockIdx.x, si = blockIdx.y, sp = blockIdx.z;
-  const SeqDesc s = seqs[si];
-  const int tid = threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = nh * D;
+  const int* tab = tables + (size_t)si * max_blocks;  // table row == sequence index of the call
+  const SeqDesc s = seqs[si];
   const int n_keys = s.pos0 + 1;
-  const int k0 = sp * DEC_KC;
-  const int nk = min(DEC_KC, n_keys - k0);
-  float* w = ws + (((size_t)si * nh + head) * splits + sp) * (D + 2);
-  float mx = -INFINITY, sum = 0.f, ov = 0.f;
-  if (nk > 0) {
-    const int* tab = tables + (size_t)s.table * max_blocks;
-    if (tid < DEC_KC / 16) {
-      int b = (k0 + tid * 16 < n_keys) ? tab[(k0 >> 4) + tid] : 0;
-      if (b < 0 || b >= nblocks) {
-        flag_bad(4u);
-        b = 0;
-      }
-      blk[tid] = b;
-    }
-    const float scale = 1.4426950408889634f / sqrtf((float)D);
-    for (int e = tid; e < D; e += 128) qs[e] = __bfloat162float(q[(size_t)s.q_start * H + head * D + e]) * scale;
-    __syncthreads();
-    constexpr int RU4 = D / 8;                    // 16-byte units per row
-    constexpr int PER = DEC_KC * RU4 / 128;       // units per thread per matrix
-    const size_t vstride = (size_t)nh * 16 * D;
-    uint4 kr[PER], vr[PER];
-#pragma unroll
-    for (int r = 0; r < PER; ++r) {
-      const int idx = tid + r * 128, jj = idx / RU4, u = idx % RU4;
-      if (jj < nk) {
-        const size_t base = ((((size_t)blk[jj >> 4] * 2) * nh + head) * 16 + (jj & 15)) * D;
-        kr[r] = __ldcs(reinterpret_cast<const uint4*>(pool + base) + u);
-        vr[r] = __ldcs(reinterpret_cast<const uint4*>(pool + base + vstride) + u);
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < PER; ++r) {
-      const int idx = tid + r * 128, jj = idx / RU4, u = idx % RU4;
-      if (jj < nk) {
-        reinterpret_cast<uint4*>(&Ks[jj][0])[u] = kr[r];
-        reinterpret_cast<uint4*>(&Vs[jj][0])[u] = vr[r];
-      }
-    }
-    __syncthreads();
-    {  // scores: thread pair per key
-      const int jj = tid >> 1, hf = tid & 1;
-      float acc = 0.f;
-      if (jj < nk) {
-        const __nv_bfloat162* kk2 = reinterpret_cast<const __nv_bfloat162*>(&Ks[jj][hf * (D / 2)]);
-#pragma unroll 8
-        for (int e = 0; e < D / 4; ++e) {
-          const float2 kk = __bfloat1622float2(kk2[e]);
-          acc += qs[hf * (D / 2) + 2 * e] * kk.x + qs[hf * (D / 2) + 2 * e + 1] * kk.y;
-        }
-      }
-      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-      if (hf == 0) ps[jj] = jj < nk ? acc : -INFINITY;
-    }
-    __syncthreads();
-    {
-      const float v0 = tid < DEC_KC ? ps[tid] : -INFINITY;
-      float m = v0;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-      if ((tid & 31) == 0) red[tid >> 5] = m;
-      __syncthreads();
-      mx = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
-      const float pr = tid < nk ? exp2f(v0 - mx) : 0.f;
-      __syncthreads();
-      if (tid < DEC_KC) ps[tid] = pr;
-      float t = pr;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
-      if ((tid & 31) == 0) red[4 + (tid >> 5)] = t;
-      __syncthreads();
-      sum = (red[4] + red[5]) + (red[6] + red[7]);
-    }
-    if constexpr (D == 128) {
-#pragma unroll 8
-      for (int jj = 0; jj < nk; ++jj) ov += ps[jj] * __bfloat162float(Vs[jj][tid]);
+  const int nb = (n_keys + 15) >> 4;
+  const int b0 = sp * DEC_BLOCKS_PER_SPLIT, b1 = min(nb, b0 + DEC_BLOCKS_PER_SPLIT);
+  const float scale = 1.4426950408889634f / sqrtf((float)D);
+  float qv[E];
+  {
+    const bf16* qp = q + (size_t)s.q_start * H + head * D + lane * E;
+    if constexpr (E == 4) {
+      const uint2 u = *reinterpret_cast<const uint2*>(qp);
+      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+      const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+      qv[0] = a.x * scale; qv[1] = a.y * scale; qv[2] = b.x * scale; qv[3] = b.y * scale;
     } else {
-      const int e = tid & (D - 1), hl = tid / D;
-      float a = 0.f;
-      for (int jj = hl; jj < nk; jj += 2) a += ps[jj] * __bfloat162float(Vs[jj][e]);
-      part[tid] = a;
-      __syncthreads();
-      ov = tid < D ? part[tid] + part[tid + D] : 0.f;
+      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(qp));
+      qv[0] = a.x * scale; qv[1] = a.y * scale;
+    }
+  }
+  float m = -INFINITY, l = 0.f, acc[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) acc[e] = 0.f;
+  const size_t vstride = (size_t)nh * 16 * D;
+  for (int b = b0 + warp; b < b1; b += DEC_WARPS) {
+    int blk = tab[b];
+    if (blk < 0 || blk >= nblocks) {
+      if (lane == 0) flag_bad(4u);
+      blk = 0;
+    }
+    const bf16* kb = pool + ((((size_t)blk * 2) * nh + head) * 16) * D + lane * E;
+    using VT = typename std::conditional<E == 4, uint2, uint32_t>::type;
+    VT kr[16], vr[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      kr[j] = __ldcs(reinterpret_cast<const VT*>(kb + j * D));
+      vr[j] = __ldcs(reinterpret_cast<const VT*>(kb + vstride + j * D));
+    }
+    float sc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      float part;
+      if constexpr (E == 4) {
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&kr[j].x));
+        const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&kr[j].y));
+        part = qv[0] * a.x + qv[1] * a.y + qv[2] * c.x + qv[3] * c.y;
+      } else {
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&kr[j]));
+        part = qv[0] * a.x + qv[1] * a.y;
+      }
+      sc[j] = part;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+      for (int j = 0; j < 16; ++j) sc[j] += __shfl_xor_sync(0xffffffffu, sc[j], off);
+    float mb = m;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (b * 16 + j >= n_keys) sc[j] = -INFINITY;
+      mb = fmaxf(mb, sc[j]);
+    }
+    const float corr = exp2f(m - mb);
+    l *= corr;
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] *= corr;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float pj = exp2f(sc[j] - mb);
+      l += pj;
+      if constexpr (E == 4) {
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vr[j].x));
+        const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vr[j].y));
+        acc[0] += pj * a.x; acc[1] += pj * a.y; acc[2] += pj * c.x; acc[3] += pj * c.y;
+      } else {
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vr[j]));
+        acc[0] += pj * a.x; acc[1] += pj * a.y;
+      }
+    }
+    m = mb;
+  }
+  // merge the warps (fixed order)
+  if (lane == 0) { sm_m[warp] = m; sm_l[warp] = l; }
+#pragma unroll
+  for (int e = 0; e < E; ++e) sm_o[warp][lane * E + e] = acc[e];
+  __syncthreads();
+  const int t = threadIdx.x;
+  float M = -INFINITY, L = 0.f, A = 0.f;
+  if (t < D) {
+#pragma unroll
+    for (int w = 0; w < DEC_WARPS; ++w) M = fmaxf(M, sm_m[w]);
+#pragma unroll
+    for (int w = 0; w < DEC_WARPS; ++w) {
+      const float f = sm_m[w] == -INFINITY ? 0.f : exp2f(sm_m[w] - M);
+      L += sm_l[w] * f;
+      A += sm_o[w][t] * f;
     }
   }
   if (splits == 1) {
-    if (tid < D) o[(size_t)s.q_start * H + head * D + tid] = __float2bfloat16_rn(ov / sum);
+    if (t < D) o[(size_t)s.q_start * H + head * D + t] = __float2bfloat16_rn(A / L);
     return;
   }
-  if (tid < D) {
-    if (tid == 0) { w[0] = mx; w[1] = sum; }
-    w[2 + tid] = ov;
+  float* wsp = ws + (((size_t)si * nh + head) * splits + sp) * (D + 2);
+  if (t < D) {
+    if (t == 0) { wsp[0] = M; wsp[1] = L; }
+    wsp[2 + t] = A;
   }
-  __threadfence();
   __syncthreads();
-  if (tid == 0) {
+  if (t == 0) {
+    __threadfence();
     unsigned* c = ctr + (size_t)si * nh + head;
     const unsigned old = atomicAdd(c, 1u);
     is_last = old == (unsigned)(splits - 1);
-    if (is_last) *c = 0;
+    if (is_last) {
+      *c = 0;
+      __threadfence();
+    }
   }
   __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  if (tid < D) {  // merge the splits in split order
-    const float* w0 = ws + ((size_t)si * nh + head) * splits * (D + 2);
-    float M = -INFINITY;
-    for (int k = 0; k < splits; ++k) M = fmaxf(M, __ldcg(w0 + k * (D + 2)));
-    float L = 0.f, A = 0.f;
-    for (int k = 0; k < splits; ++k) {
-      const float ms = __ldcg(w0 + k * (D + 2));
-      const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
-      L += __ldcg(w0 + k * (D + 2) + 1) * f;
-      A += __ldcg(w0 + k * (D + 2) + 2 + tid) * f;
-    }
-    o[(size_t)s.q_start * H + head * D + tid] = __float2bfloat16_rn(A / L);
+  if (!is_last || t >= D) return;
+  const float* w0 = ws + ((size_t)si * nh + head) * splits * (D + 2);
+  float MM = -INFINITY;
+  for (int k = 0; k < splits; ++k) MM = fmaxf(MM, __ldcg(w0 + k * (D + 2)));
+  float LL = 0.f, AA = 0.f;
+  for (int k = 0; k < splits; ++k) {
+    const float ms = __ldcg(w0 + k * (D + 2));
+    const float f = ms == -INFINITY ? 0.f : exp2f(ms - MM);
+    LL += __ldcg(w0 + k * (D + 2) + 1) * f;
+    AA += __ldcg(w0 + k * (D + 2) + 2 + t) * f;
   }
+  o[(size_t)s.q_start * H + head * D + t] = __float2bfloat16_rn(AA / LL);
 }
 
-int attn_decode_splits(int max_ctx) { return (max_ctx + DEC_KC - 1) / DEC_KC; }
+int attn_decode_splits(int max_ctx) {
+  const int nb = (max_ctx + 15) / 16;
+  return (nb + DEC_BLOCKS_PER_SPLIT - 1) / DEC_BLOCKS_PER_SPLIT;
+}
 
 void launch_attn_decode(const bf16* q, const bf16* pool, const SeqDesc* seqs, int n_seqs, int max_ctx,
                         const int* tables, int max_blocks, bf16* o, int nh, int d, float* ws, int splits,
                         unsigned* ctr, int nblocks, cudaStream_t st) {
   count_launch();
   dim3 grid(nh, n_seqs, splits);
-  if (d == 128) launchk(attn_decode_kernel<128>, grid, 128, 0, st, q, pool, seqs, tables, max_blocks, o, nh, ws, splits, ctr, nblocks);
-  else launchk(attn_decode_kernel<64>, grid, 128, 0, st, q, pool, seqs, tables, max_blocks, o, nh, ws, splits, ctr, nblocks);
+  if (d == 128) launchk(attn_decode_kernel<128>, grid, DEC_WARPS * 32, 0, st, q, pool, seqs, tables, max_blocks, o, nh, ws, splits, ctr, nblocks);
+  else launchk(attn_decode_kernel<64>, grid, DEC_WARPS * 32, 0, st, q, pool, seqs, tables, max_blocks, o, nh, ws, splits, ctr, nblocks);
 }
 
 // ------------------------------------------------------------------ argmax (a15) ---------

@@ -165,8 +165,8 @@ def attention_ref(q, K, V, pos, want_scale=False):
 def test_attention_paged(nh, d, decode):
     rng = np.random.default_rng(nh + d + decode)
     lens = [37, 1, 130, 16] if not decode else [1, 1, 1, 1]
-    ctxs = [37, 1, 130, 16] if not decode else [37, 1, 600, 16]
-    nblk, maxb = 64, 48
+    ctxs = [37, 1, 130, 16] if not decode else [37, 1, 1100, 16]  # 1100: two 1024-token splits
+    nblk, maxb = 128, 80
     free = list(rng.permutation(nblk))
     pool = np.zeros((nblk, 2, nh, 16, d), dtype=np.uint16)
     seqs, tables, qs, outs_ref, t0 = [], np.zeros((len(lens), maxb), np.int32), [], [], 0
