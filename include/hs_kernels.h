@@ -44,6 +44,13 @@ hs_status hs_k_span_copy(const uint64_t* src, const uint64_t* dst, int32_t n, ui
  * host_out (optional) receives n_ctas * 8 uint64.  enable == 0 frees the buffer. */
 hs_status hs_debug_gemm_trace(int32_t enable, void* host_out, int32_t n_ctas);
 
+/* Test-only instrumentation of the decode-stack kernel (one launch = every layer of a stage
+ * for one decode step): enable != 0 makes it record, per CTA and layer, 32 %globaltimer
+ * stamps (activation loads issued per GEMM, epilogue / attention / row-norm completion,
+ * weight loads issued per GEMM) of its latest launch, layout [n_sms][n_layers][32];
+ * host_out (optional) receives n_words uint64.  enable == 0 frees the buffer. */
+hs_status hs_debug_dstack_trace(int32_t enable, void* host_out, int64_t n_words);
+
 #ifdef __cplusplus
 }
 #endif

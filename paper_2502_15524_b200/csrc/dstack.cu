@@ -1,0 +1,977 @@
+// dstack.cu — decode stack kernel (see dstack.h for the dataflow).
+//
+// One CTA per SM, 12 warps:
+//   warp 0  lane 0 : weight producer.  Streams the 128 x 64 weight tiles of the CTA's stream-K
+//                    range of every GEMM (QKV, O, gate_up, down) of every layer, in order, into
+//                    a ring of STAGES slots.  Never waits for activations.
+//   warp 1         : TMEM owner; lane 0 issues tcgen05.mma (M = 128, N = BN, K = 16) per slot
+//                    into one of two TMEM accumulators (one per stream-K segment).
+//   warp 2  lane 0 : activation producer.  Per k-block: waits the flag of the data it needs,
+//                    then TMA-loads the [BN x 64] activation tile into the same slot.  A slot
+//                    is full when both producers arrived and both transfers landed.
+//   warps 4-7      : epilogue.  Drain a segment's accumulator to the fp32 stream-K workspace;
+//                    the last CTA to finish a tile sums the parts in part order (deterministic)
+//                    and applies the fused epilogue (RoPE + paged KV write | residual | SiLU*up),
+//                    then publishes the tile's flag.
+//   warps 4-11     : decode attention (one warp per (sequence, head, KV chunk) item) and the
+//                    row RMSNorms (done by the CTA that completes the last O / down tile).
+// Flags carry tags (launch number << 8 | layer + 1) and are compared wrap-safe, so nothing is
+// reset between steps; arrival counters are reset by their last arriver.
+//
+// Numerics follow the per-kernel path: fp32 accumulation in TMEM, partial sums
+// added in part order, bf16 rounding at the same points (q/k/v, RoPE outputs, attention output,
+// h = x + o W_o^T, a = silu(g) u, x' = h + a W_d^T, RMSNorm outputs).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <vector>
+
+#include "dstack.h"
+#include "tc.h"
+
+namespace hs {
+
+constexpr int DS_THREADS = 384;
+constexpr int DS_MAXSEQ = 64;
+constexpr int DS_AWARPS = 8;   // attention warps per CTA (warps 4-11)
+
+struct DsParams {
+  int N, H, F, nh, hd, nl, G;
+  float eps;
+  unsigned tag0;
+  int tiles[4], nkb[4], maxp[4];
+  float* ws[4];
+  const bf16 *attn_norm, *ffn_norm;
+  long long norm_stride;
+  const bf16* final_norm;
+  bf16* fin;
+  const bf16* x_in;
+  bf16 *x, *hbuf, *nrm, *q, *o, *act;
+  bf16* pool;
+  long long pool_stride;
+  int nslots, nblocks, max_blocks;
+  const int *pos, *slot, *tables;
+  const SeqDesc* seqs;
+  const float2* rope;
+  int ch;
+  int pf_dist;  // weight k-blocks prefetched into L2 ahead of the ring
+  float* ws_attn;
+  unsigned *c_tile[4], *c_all, *c_ih, *c_h, *f_na, *f_nf, *f_qkv, *f_attn, *f_gu;
+  unsigned long long* trace;  // optional: [G][nl][16] globaltimer stamps (hs_debug_dstack_trace)
+};
+
+// trace slots per (CTA, layer)
+enum { TR_B0 = 0, TR_B1, TR_B2, TR_B3, TR_B3_END, TR_E_QKV, TR_E_ATTN, TR_E_O, TR_E_NF, TR_E_GU, TR_E_D, TR_E_NA,
+       TR_A1, TR_A2, TR_A3, TR_A0, TR_O_LAST, TR_O_BAR, TR_NF_NORM, TR_D_LAST, TR_D_BAR, TR_NA_NORM,
+       TR_AT_FLAGS, TR_AT_KV, TR_Q_TFULL, TR_Q_LAST, TR_Q_PUB, TR_Q_DRAIN, TR_Q_ATOM, TR_Q_VALS, TR_Q_STORES,
+       TR_AT_END };
+#define DS_TR(slot_)                                                                      \
+  do {                                                                                    \
+    if (p.trace) p.trace[((size_t)blockIdx.x * p.nl + l) * 32 + (slot_)] = gtimer();      \
+  } while (0)
+
+// Stream-K range of CTA c over W k-blocks: with W < G only the first W CTAs take (one) block
+// each, so every CTA that owns part of a tile has work (the arrival counts stay exact).
+__device__ __forceinline__ void ds_range(int c, long long W, int G, int& beg, int& end, int& Gk) {
+  Gk = W < G ? (int)W : G;
+  beg = c < Gk ? sk_begin(c, W, Gk) : 0;
+  end = c < Gk ? sk_begin(c + 1, W, Gk) : 0;
+}
+
+// Cursor over a CTA's weight k-blocks in stream order (layer, GEMM kind, k-block).
+struct DsIt {
+  int l, k, x, beg, end;
+};
+
+__device__ __forceinline__ bool ds_it_fix(const DsParams& p, DsIt& it) {
+  while (it.x >= it.end) {
+    if (++it.k == 4) {
+      it.k = 0;
+      if (++it.l >= p.nl) return false;
+    }
+    int Gk;
+    ds_range(blockIdx.x, (long long)p.tiles[it.k] * p.nkb[it.k], p.G, it.beg, it.end, Gk);
+    it.x = it.beg;
+  }
+  return true;
+}
+
+__device__ __forceinline__ bool ds_it_begin(const DsParams& p, DsIt& it) {
+  int Gk;
+  it.l = 0;
+  it.k = 0;
+  ds_range(blockIdx.x, (long long)p.tiles[0] * p.nkb[0], p.G, it.beg, it.end, Gk);
+  it.x = it.beg;
+  return p.nl > 0 && ds_it_fix(p, it);
+}
+
+__device__ __forceinline__ bool ds_it_next(const DsParams& p, DsIt& it) {
+  ++it.x;
+  return ds_it_fix(p, it);
+}
+
+template <int BN>
+struct DsCfg {
+  static constexpr int A_BYTES = 128 * 64 * 2;
+  static constexpr int B_BYTES = BN * 64 * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int VALS_BYTES = 128 * BN * 4;  // tile values for the RoPE pairing
+  static constexpr int ROPE_BYTES = BN * 64 * 8;   // cos/sin of the call's positions (head_dim <= 128)
+  static constexpr int ATT_BYTES = (2 * 8 + 8 * 128) * 4 + 128;  // attention warp merge
+  static constexpr int MISC = 2048;
+  static constexpr int FIT = (232448 - 1024 - MISC - VALS_BYTES - ROPE_BYTES - ATT_BYTES) / STAGE_BYTES;
+  static constexpr int STAGES = FIT > 12 ? 12 : FIT;
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + VALS_BYTES + ROPE_BYTES + ATT_BYTES + 1024 + MISC;
+};
+
+__device__ __constant__ unsigned p_backoff_ns = 128;
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Release store of a flag: cumulative over the writes this thread observed (its CTA's writes
+// ordered before it by bar.sync / __syncwarp).
+__device__ __forceinline__ void publish(unsigned* f, unsigned tag) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(tag) : "memory");
+}
+
+// Waits until the flag reached `tag` (wrap-safe); traps after ~2 s (protocol bug: end the
+// kernel rather than hang the GPU).
+// Polls back off (nanosleep) so that many waiters on one flag do not saturate its L2 slice.
+__device__ __noinline__ void wait_tag(const unsigned* f, unsigned tag) {
+  if ((int)(ld_acquire(f) - tag) >= 0) return;
+  const unsigned long long t0 = gtimer();
+  for (unsigned it = 1;; ++it) {
+    __nanosleep(p_backoff_ns);
+    if ((int)(ld_acquire(f) - tag) >= 0) return;
+    if ((it & 255) == 0 && gtimer() - t0 > 2000000000ull) __trap();
+  }
+}
+
+// RMSNorm of N rows of src [N, H] into dst by the 256 threads of warps 4-11 (t = 0..255):
+// up to 8 rows at a time, 256 / ng threads per row; fixed summation order (per N).  Compact
+// rolled loops on purpose: this runs once per layer on whichever SM completed the last tile,
+// so its code is usually cold in that SM's instruction cache.
+__device__ __forceinline__ void ds_norm(const bf16* __restrict__ src, const bf16* __restrict__ w, bf16* __restrict__ dst,
+                                     int N, int H, float eps, int t, float* red) {
+  const int n8 = H >> 3;
+  int ng = 1;
+  while (ng * 2 <= min(N, 8)) ng *= 2;
+  const int tpg = 256 / ng, g = t / tpg, gt = t % tpg, wpg = tpg >> 5;
+  const uint4* w4 = reinterpret_cast<const uint4*>(w);
+  for (int r0 = 0; r0 < N; r0 += ng) {
+    const int r = r0 + g;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src) + (size_t)r * n8;
+    float ss = 0.f;
+    if (r < N) {
+#pragma unroll 2
+      for (int c = gt; c < n8; c += tpg) {
+        const uint4 v = __ldcg(s4 + c);
+        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __bfloat1622float2(p2[k]);
+          ss = fmaf(f.x, f.x, ss);
+          ss = fmaf(f.y, f.y, ss);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((t & 31) == 0) red[t >> 5] = ss;
+    named_bar(2, 256);
+    float tot = 0.f;
+    for (int k = 0; k < wpg; ++k) tot += red[g * wpg + k];
+    const float rs = 1.0f / sqrtf(tot / (float)H + eps);
+    if (r < N) {
+      uint4* d4 = reinterpret_cast<uint4*>(dst) + (size_t)r * n8;
+#pragma unroll 2
+      for (int c = gt; c < n8; c += tpg) {
+        const uint4 v = __ldcg(s4 + c), wv = w4[c];
+        uint4 o;
+        const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&v);
+        const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&wv);
+        __nv_bfloat162* rr = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 x = __bfloat1622float2(a[k]), gg = __bfloat1622float2(b[k]);
+          rr[k] = __floats2bfloat162_rn(x.x * rs * gg.x, x.y * rs * gg.y);
+        }
+        d4[c] = o;
+      }
+    }
+    named_bar(2, 256);
+  }
+}
+
+// One attention unit: sequence i, head h, KV blocks [sp * DS_SPLIT, (sp + 1) * DS_SPLIT) of the
+// sequence, by the 8 attention warps of a CTA (t = 0..255).  Warp w takes blocks w, w + 8, ...:
+// for a 16-token block lane l loads dims [E l, E l + E) of its 16 K and 16 V rows (32
+// independent loads in flight), computes the scores with warp all-reduces and keeps an online
+// softmax (m, l, acc).  The warps are merged through shared memory in warp order; with several
+// splits (long contexts) the partial goes to ws_attn[u] and the last split merges the splits in
+// order.  The last sequence of head h publishes the head's flag.  Deterministic.
+constexpr int DS_SPLIT = 64;  // KV blocks (1024 tokens) per unit
+
+template <int D>
+__device__ __forceinline__ void ds_attn_unit(const DsParams& p, int l, unsigned tag, int i, int h, int sp, int nsp,
+                                             int u, int t, float* sm) {
+  constexpr int E = D / 32;
+  const int warp = t >> 5, lane = t & 31;
+  const int H = p.nh * D;
+  const SeqDesc s = p.seqs[i];
+  const int n_keys = __shfl_sync(0xffffffffu, s.pos0 + 1, 0), nb = (n_keys + 15) >> 4;
+  const int b0 = sp * p.ch, b1 = min(nb, b0 + p.ch);
+  const int q_start = __shfl_sync(0xffffffffu, s.q_start, 0);
+  if (t == 0) {
+    const int tq = (h * D) / 128, th = H / 128;
+    wait_tag(p.f_qkv + tq, tag);
+    wait_tag(p.f_qkv + tq + th, tag);
+    wait_tag(p.f_qkv + tq + 2 * th, tag);
+    if (p.trace) DS_TR(TR_AT_FLAGS);
+  }
+  named_bar(2, 256);
+  const float scale = 1.4426950408889634f / sqrtf((float)D);
+  float qv[E];
+  {
+    const bf16* qp = p.q + (size_t)q_start * H + h * D + lane * E;
+    if constexpr (E == 4) {
+      const uint2 uu = __ldcg(reinterpret_cast<const uint2*>(qp));
+      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&uu.x));
+      const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&uu.y));
+      qv[0] = a.x * scale; qv[1] = a.y * scale; qv[2] = b.x * scale; qv[3] = b.y * scale;
+    } else {
+      const unsigned uu = __ldcg(reinterpret_cast<const unsigned*>(qp));
+      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&uu));
+      qv[0] = a.x * scale; qv[1] = a.y * scale;
+    }
+  }
+  const bf16* pool = p.pool + (size_t)l * p.pool_stride;
+  const int* tab = p.tables + (size_t)i * p.max_blocks;
+  const size_t vstride = (size_t)p.nh * 16 * D;
+  float m = -INFINITY, lsum = 0.f, acc[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) acc[e] = 0.f;
+  using VT = typename std::conditional<E == 4, uint2, unsigned>::type;
+  // this warp's block ids, loaded lane-parallel up front (<= 32 blocks per warp per unit)
+  const int my_blk = (b0 + warp + lane * DS_AWARPS < b1) ? tab[b0 + warp + lane * DS_AWARPS] : 0;
+  for (int b = b0 + warp, bi = 0; b < b1; b += DS_AWARPS, ++bi) {
+    int blk = __shfl_sync(0xffffffffu, my_blk, bi & 31);
+    if (bi >= 32) blk = tab[b];
+    if (blk < 0 || blk >= p.nblocks) blk = 0;
+    const bf16* kb = pool + (((size_t)blk * 2 * p.nh + h) * 16) * D + lane * E;
+    VT kr[16], vr[16];
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      kr[jj] = __ldcg(reinterpret_cast<const VT*>(kb + jj * D));
+      vr[jj] = __ldcg(reinterpret_cast<const VT*>(kb + vstride + jj * D));
+    }
+    float sc[16];
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      if constexpr (E == 4) {
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&kr[jj].x));
+        const float2 cc = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&kr[jj].y));
+        sc[jj] = qv[0] * a.x + qv[1] * a.y + qv[2] * cc.x + qv[3] * cc.y;
+      } else {
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&kr[jj]));
+        sc[jj] = qv[0] * a.x + qv[1] * a.y;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) sc[jj] += __shfl_xor_sync(0xffffffffu, sc[jj], off);
+    float mb = m;
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      if (b * 16 + jj >= n_keys) sc[jj] = -INFINITY;
+      mb = fmaxf(mb, sc[jj]);
+    }
+    const float corr = exp2f(m - mb);
+    lsum *= corr;
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] *= corr;
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      const float pj = exp2f(sc[jj] - mb);
+      lsum += pj;
+      if constexpr (E == 4) {
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vr[jj].x));
+        const float2 cc = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vr[jj].y));
+        acc[0] += pj * a.x; acc[1] += pj * a.y; acc[2] += pj * cc.x; acc[3] += pj * cc.y;
+      } else {
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vr[jj]));
+        acc[0] += pj * a.x; acc[1] += pj * a.y;
+      }
+    }
+    m = mb;
+  }
+  if (p.trace && t == 0) DS_TR(TR_AT_KV);
+  // merge the 8 warps through shared memory (warp order)
+  float* sm_m = sm;                 // [8]
+  float* sm_l = sm + DS_AWARPS;     // [8]
+  float* sm_a = sm + 2 * DS_AWARPS; // [8][D]
+  if (lane == 0) { sm_m[warp] = m; sm_l[warp] = lsum; }
+#pragma unroll
+  for (int e = 0; e < E; ++e) sm_a[warp * D + lane * E + e] = acc[e];
+  named_bar(2, 256);
+  float M = -INFINITY, L = 0.f, A = 0.f;
+  if (t < D) {
+#pragma unroll
+    for (int w = 0; w < DS_AWARPS; ++w) M = fmaxf(M, sm_m[w]);
+#pragma unroll
+    for (int w = 0; w < DS_AWARPS; ++w) {
+      const float f = sm_m[w] == -INFINITY ? 0.f : exp2f(sm_m[w] - M);
+      L += sm_l[w] * f;
+      A += sm_a[w * D + t] * f;
+    }
+  }
+  bf16* orow = p.o + (size_t)q_start * H + h * D;
+  bool head_arrive = true;
+  if (nsp > 1) {  // long context: partial of this split, the last split merges in split order
+    float* w = p.ws_attn + (size_t)u * (D + 4);
+    if (t == 0) { w[0] = M; w[1] = L; }
+    if (t < D) w[4 + t] = A;
+    named_bar(2, 256);
+    if (t == 0) {
+      unsigned* cc = p.c_ih + (size_t)i * p.nh + h;
+      const unsigned old = atom_add_acq_rel(cc, 1u);
+      const int last = old == (unsigned)(nsp - 1);
+      if (last) *cc = 0;
+      sm_m[0] = last ? 1.f : 0.f;
+    }
+    named_bar(2, 256);
+    head_arrive = sm_m[0] != 0.f;
+    if (head_arrive && t < D) {
+      const float* w0 = p.ws_attn + (size_t)(u - sp) * (D + 4);
+      float MM = -INFINITY;
+      for (int k = 0; k < nsp; ++k) MM = fmaxf(MM, __ldcg(w0 + (size_t)k * (D + 4)));
+      float LL = 0.f, AA = 0.f;
+      for (int k = 0; k < nsp; ++k) {
+        const float* wk = w0 + (size_t)k * (D + 4);
+        const float ms = __ldcg(wk);
+        const float f = ms == -INFINITY ? 0.f : exp2f(ms - MM);
+        LL += __ldcg(wk + 1) * f;
+        AA += __ldcg(wk + 4 + t) * f;
+      }
+      orow[t] = __float2bfloat16_rn(AA / LL);
+    }
+  } else if (t < D) {
+    orow[t] = __float2bfloat16_rn(A / L);
+  }
+  named_bar(2, 256);  // o written (and sm reusable)
+  if (head_arrive && t == 0) {
+    if (p.trace) DS_TR(TR_AT_END);
+    const unsigned old = atom_add_acq_rel(p.c_h + h, 1u);
+    if (old == (unsigned)(p.N - 1)) {
+      p.c_h[h] = 0;
+      publish(p.f_attn + h, tag);
+      if (p.trace && h < 64) p.trace[(size_t)p.G * p.nl * 32 + (size_t)l * 256 + 128 + h] = gtimer();
+    }
+  }
+}
+
+// The epilogue warps' part of GEMM kind k (0 qkv, 1 o, 2 gate_up, 3 down) of layer l: drains
+// the CTA's stream-K segments; the last arriver of a tile applies the epilogue.  Returns the
+// running segment count (TMEM double-buffer phase).
+template <int BN>
+__device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsigned tag, int seg, uint32_t tmem,
+                                           uint64_t* tfull, uint64_t* tempty, float* vals, volatile int* flag,
+                                           volatile unsigned* norm_tag, int et, int lane, int quad,
+                                           const int* s_pos, const int* s_slot, const float2* s_rope) {
+  const int nkb = p.nkb[k], tiles = p.tiles[k];
+  const long long W = (long long)tiles * nkb;
+  int beg, end, Gk;
+  ds_range(blockIdx.x, W, p.G, beg, end, Gk);
+  const int ml = et;
+  int lastt[4], nlast = 0;
+  // pass 1: drain every segment of the phase and arrive on its tile
+  for (int cur = beg; cur < end; ++seg) {
+    const int t = cur / nkb, kb_lo = cur % nkb, kb_hi = min(nkb, kb_lo + (end - cur));
+    const int buf = seg & 1;
+    mbar_wait(&tfull[buf], (seg >> 1) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (k == 0 && et == 0 && cur == beg) DS_TR(TR_Q_TFULL);
+    const int first = sk_owner((long long)t * nkb, W, Gk);
+    const int np = sk_owner((long long)(t + 1) * nkb - 1, W, Gk) - first + 1;
+    const int part = blockIdx.x - first;
+    float* tws = p.ws[k] + (size_t)t * p.maxp[k] * BN * 128;
+    {
+      float* dst = tws + (size_t)part * BN * 128 + ml;
+      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + buf * BN;
+      constexpr int CH = BN < 32 ? 16 : 32;
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += CH) {
+        float v[32];
+        if constexpr (CH == 32) tmem_ld32(taddr + c0, v);
+        else tmem_ld16(taddr + c0, v);
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+          if (c0 + j < p.N) dst[(size_t)(c0 + j) * 128] = v[j];
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf])) : "memory");
+    const bool first_seg = cur == beg;
+    if (k == 0 && et == 0 && first_seg) DS_TR(TR_Q_DRAIN);
+    cur += kb_hi - kb_lo;
+    named_bar(1, 128);
+    if (et == 0) {
+      const unsigned old = atom_add_acq_rel(&p.c_tile[k][t], 1u);
+      const int last = old == (unsigned)(np - 1);
+      if (last) p.c_tile[k][t] = 0;
+      *flag = last;
+      if (k == 0 && first_seg) DS_TR(TR_Q_ATOM);
+    }
+    named_bar(1, 128);
+    if (__shfl_sync(0xffffffffu, *flag, 0)) {  // (warp-uniform for the compiler)
+      if (nlast == 4) __trap();
+      lastt[nlast++] = t;
+    }
+  }
+  // pass 2: the epilogues of the tiles this CTA completed (after every arrival of the phase,
+  // so a CTA's later segments never wait behind its earlier tiles' epilogues)
+  for (int q = 0; q < nlast; ++q) {
+    const int t = lastt[q];
+    const int first = sk_owner((long long)t * nkb, W, Gk);
+    const int np = sk_owner((long long)(t + 1) * nkb - 1, W, Gk) - first + 1;
+    float* tws = p.ws[k] + (size_t)t * p.maxp[k] * BN * 128;
+    if (k == 0 && et == 0) DS_TR(TR_Q_LAST);
+    const int m = t * 128 + ml;
+    const int H = p.H;
+    if (k == 0) {  // bf16(q, k, v); RoPE of q, k; k', v -> paged pool; q' -> q
+      for (int n = 0; n < p.N; ++n) {
+        float a = 0.f;
+        for (int pt = 0; pt < np; ++pt) a += __ldcg(tws + (size_t)pt * BN * 128 + (size_t)n * 128 + ml);
+        vals[ml * BN + n] = __bfloat162float(__float2bfloat16_rn(a));
+      }
+      named_bar(1, 128);
+      if (et == 0) DS_TR(TR_Q_VALS);
+      const int half = p.hd >> 1;
+      const int region = (t * 128) / H, r0 = (t * 128) % H;  // 0 q, 1 k, 2 v
+      if (et < 64) {
+        const int hl = et / half, i = et % half;
+        const int ra = hl * p.hd + i, rb = ra + half;
+        const int head = (r0 + ra) / p.hd;
+        bf16* pool = p.pool + (size_t)l * p.pool_stride;
+        for (int n = 0; n < p.N; ++n) {
+          const float a = vals[ra * BN + n], b = vals[rb * BN + n];
+          const int sl = s_slot[n];
+          if (sl < 0 || sl >= p.nslots) continue;
+          const size_t blk = (size_t)(sl >> 4), off = (size_t)(sl & 15);
+          if (region == 2) {
+            bf16* vd = pool + (((blk * 2 + 1) * p.nh + head) * 16 + off) * p.hd;
+            vd[i] = __float2bfloat16_rn(a);
+            vd[i + half] = __float2bfloat16_rn(b);
+          } else {
+            const float2 cs = s_rope[n * half + i];
+            const bf16 x1 = __float2bfloat16_rn(a * cs.x - b * cs.y), x2 = __float2bfloat16_rn(b * cs.x + a * cs.y);
+            bf16* d = region == 0 ? p.q + (size_t)n * H + head * p.hd
+                                  : pool + (((blk * 2 + 0) * p.nh + head) * 16 + off) * p.hd;
+            d[i] = x1;
+            d[i + half] = x2;
+          }
+        }
+      }
+      if (et == 0) DS_TR(TR_Q_STORES);
+      named_bar(1, 128);
+      if (et == 0) publish(p.f_qkv + t, tag);
+      if (et == 0) DS_TR(TR_Q_PUB);
+      if (et == 0 && p.trace && t < 128) p.trace[(size_t)p.G * p.nl * 32 + (size_t)l * 256 + t] = gtimer();
+    } else if (k == 2) {  // a = bf16(silu(g) * u): lanes 0-15 gate rows, 16-31 their up rows
+      for (int n = 0; n < p.N; ++n) {
+        float a = 0.f;
+        for (int pt = 0; pt < np; ++pt) a += __ldcg(tws + (size_t)pt * BN * 128 + (size_t)n * 128 + ml);
+        const float u = __shfl_xor_sync(0xffffffffu, a, 16);
+        if (lane < 16) p.act[(size_t)n * p.F + (m >> 5) * 16 + lane] = __float2bfloat16_rn(silu_f(a) * u);
+      }
+      named_bar(1, 128);
+      if (et == 0) publish(p.f_gu + t, tag);
+    } else {  // residual: h = bf16(x + o W_o^T) (k = 1) / x' = bf16(h + a W_d^T) (k = 3)
+      const bf16* resid = k == 1 ? (l == 0 ? p.x_in : p.x) : p.hbuf;
+      bf16* out = k == 1 ? p.hbuf : p.x;
+      for (int n = 0; n < p.N; ++n) {
+        float a = 0.f;
+        for (int pt = 0; pt < np; ++pt) a += __ldcg(tws + (size_t)pt * BN * 128 + (size_t)n * 128 + ml);
+        out[(size_t)n * H + m] = __float2bfloat16_rn(a + __bfloat162float(__ldcg(resid + (size_t)n * H + m)));
+      }
+      named_bar(1, 128);
+      if (et == 0) {  // grid-level arrival: the CTA completing the last tile normalises the rows
+        unsigned* ca = p.c_all + (k == 1 ? 0 : 1);
+        const unsigned old = atom_add_acq_rel(ca, 1u);
+        if (old == (unsigned)(tiles - 1)) {
+          *ca = 0;
+          norm_tag[k == 1 ? 0 : 1] = tag;
+          DS_TR(k == 1 ? TR_O_LAST : TR_D_LAST);
+        }
+      }
+    }
+  }
+  return seg;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(DS_THREADS, 1)
+    dstack_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtensorMap tw1,
+                  const __grid_constant__ CUtensorMap tw2, const __grid_constant__ CUtensorMap tw3,
+                  const __grid_constant__ CUtensorMap tbn, const __grid_constant__ CUtensorMap tbo,
+                  const __grid_constant__ CUtensorMap tba, const __grid_constant__ DsParams p) {
+  using C = DsCfg<BN>;
+  PDL_LAUNCH();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* vals = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES);
+  float2* s_rope = reinterpret_cast<float2*>(smem + C::STAGES * C::STAGE_BYTES + C::VALS_BYTES);
+  float* s_att = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + C::VALS_BYTES + C::ROPE_BYTES);
+  uint8_t* misc = smem + C::STAGES * C::STAGE_BYTES + C::VALS_BYTES + C::ROPE_BYTES + C::ATT_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(misc);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  volatile int* flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
+  volatile unsigned* norm_tag = reinterpret_cast<volatile unsigned*>(tmem_slot + 2);  // [2]
+  float* red = reinterpret_cast<float*>(tmem_slot + 4);                                // [8]
+  int* s_nc = reinterpret_cast<int*>(red + 8);                                         // [64]
+  int* s_base = s_nc + DS_MAXSEQ;                                                      // [65]
+  int* s_pos = s_base + DS_MAXSEQ + 4;                                                 // [64]
+  int* s_slot = s_pos + DS_MAXSEQ;                                                     // [64]
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int G = p.G;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 2); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    norm_tag[0] = 0;
+    norm_tag[1] = 0;
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"((uint32_t)C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- weight producer (independent of every earlier kernel and flag)
+      // While the ring is full (the MMA waits for activations) the producer keeps HBM busy by
+      // prefetching the next items into L2, up to pf_dist items ahead of the ring.
+      const CUtensorMap* wm[4] = {&tw0, &tw1, &tw2, &tw3};
+      DsIt ld, pf;
+      bool ld_ok = ds_it_begin(p, ld), pf_ok = ld_ok;
+      pf = ld;
+      int i = 0, j = 0;
+      while (ld_ok) {
+        const int s = i % C::STAGES;
+        const uint32_t par = ((i / C::STAGES) & 1) ^ 1;
+        unsigned long long t0 = 0;
+        for (unsigned it = 0; !mbar_test(&empty[s], par); ++it) {
+          if (pf_ok && j < i + p.pf_dist) {
+            if (j >= i) tma_prefetch_3d(wm[pf.k], (pf.x % p.nkb[pf.k]) * 64, (pf.x / p.nkb[pf.k]) * 128, pf.l);
+            pf_ok = ds_it_next(p, pf);
+            ++j;
+          } else if ((it & 1023) == 1023) {
+            if (t0 == 0) t0 = gtimer();
+            else if (gtimer() - t0 > 4000000000ull) __trap();
+          }
+        }
+        if (j <= i) {  // keep the prefetch cursor ahead of the load cursor
+          pf = ld;
+          pf_ok = ds_it_next(p, pf);
+          j = i + 1;
+        }
+        const int l = ld.l, k = ld.k, x = ld.x;
+        if (x == ld.beg && p.trace) DS_TR(k == 0 ? TR_A0 : TR_A1 + k - 1);
+        mbar_expect_tx(&full[s], C::A_BYTES);
+        tma_load_3d(wm[k], &full[s], smem + s * C::STAGE_BYTES, (x % p.nkb[k]) * 64, (x / p.nkb[k]) * 128, l);
+        ld_ok = ds_it_next(p, ld);
+        ++i;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      constexpr uint32_t idesc = instr_desc<BN>();
+      int i = 0, seg = 0;
+      for (int l = 0; l < p.nl; ++l)
+        for (int k = 0; k < 4; ++k) {
+          const int nkb = p.nkb[k];
+          const long long W = (long long)p.tiles[k] * nkb;
+          int beg, end, Gk;
+          ds_range(blockIdx.x, W, G, beg, end, Gk);
+          for (int cur = beg; cur < end; ++seg) {
+            const int kb_lo = cur % nkb, kb_hi = min(nkb, kb_lo + (end - cur));
+            const int buf = seg & 1;
+            mbar_wait(&tempty[buf], ((seg >> 1) & 1) ^ 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t acc = tmem + buf * BN;
+            for (int kb = kb_lo; kb < kb_hi; ++kb, ++i) {
+              const int s = i % C::STAGES;
+              mbar_wait(&full[s], (i / C::STAGES) & 1);
+              asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+              const uint8_t* sa = smem + s * C::STAGE_BYTES;
+              const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + C::A_BYTES);
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                umma_bf16(acc, da + 2 * kk, db + 2 * kk, idesc, (kb > kb_lo || kk > 0) ? 1u : 0u);
+              umma_commit(&empty[s]);
+            }
+            umma_commit(&tfull[buf]);
+            cur += kb_hi - kb_lo;
+          }
+        }
+    }
+  } else if (warp == 2) {
+    // ---- activation producer: flag-gated.  The whole warp polls up to 32 k-blocks' flags at
+    // once (one L2 round trip per poll instead of one per k-block); lane 0 issues the TMA loads
+    // of the ready prefix in order.
+    PDL_WAIT();
+    const CUtensorMap* bm[4] = {&tbn, &tbo, &tbn, &tba};
+    int i = 0;
+    for (int l = 0; l < p.nl; ++l) {
+      const unsigned tag = p.tag0 + l;
+      for (int k = 0; k < 4; ++k) {
+        const int nkb = p.nkb[k];
+        const long long W = (long long)p.tiles[k] * nkb;
+        int beg, end, Gk;
+        ds_range(blockIdx.x, W, G, beg, end, Gk);
+        if (beg == end) continue;
+        if (k == 0 || k == 2) {  // one flag for the whole phase (a row norm)
+          if (lane == 0) wait_tag(k == 0 ? p.f_na : p.f_nf, tag);
+          __syncwarp();
+        }
+        for (int x0 = beg; x0 < end; x0 += 32) {
+          const int cnt = min(32, end - x0);
+          const int kbl = (x0 + lane) % nkb;
+          const unsigned* f = k == 1 ? p.f_attn + (kbl * 64) / p.hd : p.f_gu + kbl;
+          int issued = 0;
+          unsigned long long t_spin = 0;
+          while (issued < cnt) {
+            bool ok = lane < issued || lane >= cnt;
+            if (!ok) ok = (k == 0 || k == 2) || (int)(ld_acquire(f) - tag) >= 0;
+            const unsigned mask = __ballot_sync(0xffffffffu, ok);
+            const int upto = min(cnt, mask == 0xffffffffu ? 32 : __ffs(~mask) - 1);
+            __syncwarp();
+            if (upto > issued) {
+              if (lane == 0) {
+                if (p.trace && x0 == beg && issued == 0) DS_TR(k);
+                asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
+                for (int q = issued; q < upto; ++q) {
+                  const int ii = i + (x0 - beg) + q;
+                  const int s = ii % C::STAGES;
+                  mbar_wait(&empty[s], ((ii / C::STAGES) & 1) ^ 1);
+                  mbar_expect_tx(&full[s], C::B_BYTES);
+                  tma_load_2d(bm[k], &full[s], smem + s * C::STAGE_BYTES + C::A_BYTES, ((x0 + q) % nkb) * 64, 0);
+                }
+              }
+              issued = upto;
+            } else {
+              __nanosleep(p_backoff_ns);
+              if (t_spin == 0) t_spin = gtimer();
+              else if (gtimer() - t_spin > 2000000000ull) __trap();
+            }
+          }
+        }
+        i += end - beg;
+        if (k == 3 && lane == 0) DS_TR(TR_B3_END);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---- epilogue (warps 4-7), attention + row norms (warps 4-11)
+    PDL_WAIT();
+    const bool epi = warp < 8;
+    const int t256 = threadIdx.x - 128;
+    const int quad = warp & 3;
+    const int aw = warp - 4;
+    if (t256 == 0) {
+      int b = 0;
+      for (int i = 0; i < p.N; ++i) {
+        const int nb = (p.seqs[i].pos0 + 1 + 15) >> 4;
+        const int nc = (nb + p.ch - 1) / p.ch;
+        s_nc[i] = nc;
+        s_base[i] = b;
+        b += p.nh * nc;
+      }
+      s_base[p.N] = b;
+    }
+    {  // the call's positions, KV slots and RoPE rows (read by the QKV epilogues of every layer)
+      const int half = p.hd >> 1;
+      if (t256 < p.N) {
+        s_pos[t256] = p.pos[t256];
+        s_slot[t256] = p.slot[t256];
+      }
+      for (int idx = t256; idx < p.N * half; idx += 256)
+        s_rope[idx] = p.rope[(size_t)p.pos[idx / half] * half + idx % half];
+    }
+    named_bar(2, 256);
+    const int total = __shfl_sync(0xffffffffu, s_base[p.N], 0);
+    int seg = 0;
+    // One call site per routine (they are inlined into a warp-uniform context and their code
+    // stays resident in the instruction cache): step (l, k) = [pending row norm] -> GEMM k's
+    // segments (epilogue warps) -> attention (k = 0) -> grid-last check (k = 1, 3).
+    bool pend = blockIdx.x == 0;  // the stage input's attn RMSNorm (layer 0)
+    const bf16* n_src = p.x_in;
+    const bf16* n_w = p.attn_norm;
+    bf16* n_dst = p.nrm;
+    unsigned* n_flag = p.f_na;
+    unsigned n_tag = p.tag0;
+    for (int step = 0; step <= 4 * p.nl; ++step) {
+      const int l = step >> 2, k = step & 3;
+      if (pend) {
+        ds_norm(n_src, n_w, n_dst, p.N, p.H, p.eps, t256, red);
+        if (n_flag && t256 == 0) publish(n_flag, n_tag);
+        if (t256 == 0 && step < 4 * p.nl) DS_TR(n_flag == p.f_nf ? TR_E_NF : TR_E_NA);
+        pend = false;
+      }
+      if (step == 4 * p.nl) break;
+      const unsigned tag = p.tag0 + l;
+      if (epi) seg = ds_segments<BN>(p, k, l, tag, seg, tmem, tfull, tempty, vals, flag, norm_tag, t256, lane, quad,
+                                     s_pos, s_slot, s_rope);
+      if (t256 == 0) DS_TR(TR_E_QKV + (k == 0 ? 0 : k == 1 ? 2 : k == 2 ? 4 : 5));
+      if (k == 0) {
+        // units (seq, head, split) over the CTAs; every CTA loops uniformly
+        for (int u = blockIdx.x; u < total; u += G) {
+          int i = 0;
+          while (i + 1 < p.N && s_base[i + 1] <= u) ++i;
+          i = __shfl_sync(0xffffffffu, i, 0);
+          const int nsp = __shfl_sync(0xffffffffu, s_nc[i], 0), r = u - __shfl_sync(0xffffffffu, s_base[i], 0);
+          if (p.hd == 128) ds_attn_unit<128>(p, l, tag, i, r / nsp, r % nsp, nsp, u, t256, s_att);
+          else ds_attn_unit<64>(p, l, tag, i, r / nsp, r % nsp, nsp, u, t256, s_att);
+        }
+        if (t256 == 0) DS_TR(TR_E_ATTN);
+      } else if (k == 1 || k == 3) {
+        named_bar(2, 256);
+        if (__shfl_sync(0xffffffffu, norm_tag[k >> 1], 0) == tag) {  // this CTA completed the last tile
+          if (k == 1) {
+            pend = true; n_src = p.hbuf; n_w = p.ffn_norm + (size_t)l * p.norm_stride; n_dst = p.nrm;
+            n_flag = p.f_nf; n_tag = tag;
+          } else if (l + 1 < p.nl) {
+            pend = true; n_src = p.x; n_w = p.attn_norm + (size_t)(l + 1) * p.norm_stride; n_dst = p.nrm;
+            n_flag = p.f_na; n_tag = tag + 1;
+          } else if (p.final_norm) {
+            pend = true; n_src = p.x; n_w = p.final_norm; n_dst = p.fin; n_flag = nullptr;
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)C::TMEM_COLS));
+}
+
+// ------------------------------------------------------------------ host side -----------
+struct DstackState {
+  int device = 0, G = 0;
+  int H = 0, F = 0, nh = 0, hd = 0, max_seqs = 0, bn_max = 16;
+  int tiles[4] = {}, nkb[4] = {}, maxp[4] = {};
+  float* ws = nullptr;
+  size_t ws_off[4] = {};
+  float* ws_attn = nullptr;
+  size_t attn_items_max = 0;
+  unsigned* ctr = nullptr;
+  size_t ctr_words = 0;
+  unsigned seq_no = 0;
+};
+
+// HS debug: per-CTA phase timestamps of the last launch (hs_debug_dstack_trace)
+static unsigned long long* g_ds_trace = nullptr;
+static constexpr size_t kTraceWords = (size_t)148 * 2 * 256 * 32;
+
+static int max_parts(int tiles, int nkb, int G) {
+  const long long W = (long long)tiles * nkb;
+  if (W < G) G = (int)W;
+  int mp = 1;
+  for (int t = 0; t < tiles; ++t)
+    mp = std::max(mp, sk_owner((long long)(t + 1) * nkb - 1, W, G) - sk_owner((long long)t * nkb, W, G) + 1);
+  return mp;
+}
+
+bool dstack_supported(int N, int hd) {
+  static int on = [] {
+    const char* e = getenv("HS_DSTACK");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return on && N >= 1 && N <= DS_MAXSEQ && (hd == 64 || hd == 128);
+}
+
+hs_status dstack_create(DstackState** out, int H, int F, int nh, int hd, int max_seqs, int max_ctx) {
+  DstackState* s = new DstackState();
+  HS_CUDA(cudaGetDevice(&s->device));
+  s->G = num_sms(s->device);
+  s->H = H; s->F = F; s->nh = nh; s->hd = hd; s->max_seqs = std::min(max_seqs, DS_MAXSEQ);
+  s->bn_max = gemm_bn(std::max(1, s->max_seqs));
+  const int M[4] = {3 * H, H, 2 * F, H}, K[4] = {H, H, H, F};
+  size_t off = 0;
+  for (int k = 0; k < 4; ++k) {
+    s->tiles[k] = M[k] / 128;
+    s->nkb[k] = K[k] / 64;
+    s->maxp[k] = max_parts(s->tiles[k], s->nkb[k], s->G);
+    s->ws_off[k] = off;
+    off += align_up((size_t)s->tiles[k] * s->maxp[k] * s->bn_max * 128, 64);
+  }
+  cudaError_t e = cudaMalloc(&s->ws, off * 4);
+  s->attn_items_max = std::max((size_t)s->G, (size_t)s->max_seqs * nh * ((std::max(max_ctx, 1) + 16 * DS_SPLIT - 1) / (16 * DS_SPLIT)));
+  if (e == cudaSuccess) e = cudaMalloc(&s->ws_attn, s->attn_items_max * (hd + 4) * 4);
+  s->ctr_words = 4096 + (size_t)DS_MAXSEQ * nh + 4 * (size_t)(s->tiles[0] + s->tiles[1] + s->tiles[2] + s->tiles[3]);
+  if (e == cudaSuccess) e = cudaMalloc(&s->ctr, s->ctr_words * 4);
+  if (e == cudaSuccess) e = cudaMemset(s->ctr, 0, s->ctr_words * 4);
+  if (e != cudaSuccess) {
+    dstack_destroy(s);
+    HS_FAIL(e == cudaErrorMemoryAllocation ? HS_E_OOM : HS_E_CUDA, "dstack workspace: %s", cudaGetErrorString(e));
+  }
+  *out = s;
+  return HS_OK;
+}
+
+void dstack_destroy(DstackState* s) {
+  if (!s) return;
+  DeviceGuard dg(s->device);
+  if (s->ws) cudaFree(s->ws);
+  if (s->ws_attn) cudaFree(s->ws_attn);
+  if (s->ctr) cudaFree(s->ctr);
+  delete s;
+}
+
+template <int BN>
+static hs_status launch_bn(DstackState* s, const DstackArgs& a, const DsParams& p, int bi, cudaStream_t st) {
+  using C = DsCfg<BN>;
+  static bool attr_set[64] = {};
+  if (s->device < 64 && !attr_set[s->device]) {
+    HS_CUDA(cudaFuncSetAttribute(dstack_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set[s->device] = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(s->G);
+  cfg.blockDim = dim3(DS_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  at[na].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (they wait on each other's flags)
+  at[na].val.cooperative = 1;
+  ++na;
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  HS_CUDA(cudaLaunchKernelEx(&cfg, dstack_kernel<BN>, a.wqkv->map, a.wo->map, a.wgu->map, a.wd->map, a.b_nrm[bi].map,
+                             a.b_o[bi].map, a.b_act[bi].map, p));
+  count_launch();
+  return HS_OK;
+}
+
+hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
+  if (!dstack_supported(a.N, a.hd) || a.N > s->max_seqs || a.H != s->H || a.F != s->F || a.nh != s->nh ||
+      a.hd != s->hd || a.nl < 1 || a.nl > 255)
+    HS_FAIL(HS_E_INVAL, "dstack: unsupported call (N=%d nl=%d)", a.N, a.nl);
+  const int BN = gemm_bn(a.N);
+  if (BN > s->bn_max) HS_FAIL(HS_E_INVAL, "dstack: N=%d above the workspace's tile width", a.N);
+  int bi = 0;
+  while (gemm_bn_value(bi) != BN) ++bi;
+  if (a.b_nrm[bi].box_rows != BN || a.b_o[bi].box_rows != BN || a.b_act[bi].box_rows != BN)
+    HS_FAIL(HS_E_INVAL, "dstack: activation TMA box mismatch");
+  DsParams p{};
+  p.N = a.N; p.H = a.H; p.F = a.F; p.nh = a.nh; p.hd = a.hd; p.nl = a.nl; p.G = s->G; p.eps = a.eps;
+  if (++s->seq_no >= (1u << 24)) s->seq_no = 1;  // tags stay wrap-safe: flags are compared by difference
+  p.tag0 = (s->seq_no << 8) + 1;
+  for (int k = 0; k < 4; ++k) {
+    p.tiles[k] = s->tiles[k];
+    p.nkb[k] = s->nkb[k];
+    p.maxp[k] = s->maxp[k];
+    p.ws[k] = s->ws + s->ws_off[k];
+  }
+  p.attn_norm = a.attn_norm; p.ffn_norm = a.ffn_norm; p.norm_stride = a.norm_stride;
+  p.final_norm = a.final_norm; p.fin = a.fin;
+  p.x_in = a.x_in; p.x = a.x; p.hbuf = a.hbuf; p.nrm = a.nrm; p.q = a.q; p.o = a.o; p.act = a.act;
+  p.pool = a.pool; p.pool_stride = a.pool_stride; p.nslots = a.nslots; p.nblocks = a.nblocks;
+  p.max_blocks = a.max_blocks; p.pos = a.pos; p.slot = a.slot; p.tables = a.tables; p.seqs = a.seqs; p.rope = a.rope;
+  {  // KV blocks per attention unit: the smallest split that keeps the units within one wave
+     // of CTAs (short contexts use more SMs), at most DS_SPLIT; a function of the shapes only
+    auto units_of = [&](int ch) {
+      size_t u = 0;
+      for (int i = 0; i < a.N; ++i) u += (size_t)a.nh * (((a.ctx[i] + 15) / 16 + ch - 1) / ch);
+      return u;
+    };
+    int ch = 1;
+    while (ch < DS_SPLIT && units_of(ch) > (size_t)s->G) ++ch;
+    if (units_of(ch) > s->attn_items_max) HS_FAIL(HS_E_INVAL, "dstack: context longer than the workspace was sized for");
+    p.ch = ch;
+  }
+  p.ws_attn = s->ws_attn;
+  {
+    static int pf = [] {
+      const char* e = getenv("HS_DSTACK_PF");
+      return e ? atoi(e) : 0;  // measured: L2 prefetch ahead of the ring only slows the step (r01)
+    }();
+    p.pf_dist = pf;
+    static bool bo_set[64] = {};
+    if (s->device < 64 && !bo_set[s->device]) {
+      const char* e = getenv("HS_DSTACK_BACKOFF");
+      const unsigned ns = e ? (unsigned)atoi(e) : 128u;
+      HS_CUDA(cudaMemcpyToSymbol(p_backoff_ns, &ns, sizeof(ns)));
+      bo_set[s->device] = true;
+    }
+  }
+  p.trace = g_ds_trace && (size_t)s->G * a.nl * 32 + (size_t)a.nl * 256 <= kTraceWords ? g_ds_trace : nullptr;
+  unsigned* c = s->ctr;
+  size_t o = 0;
+  for (int k = 0; k < 4; ++k) { p.c_tile[k] = c + o; o += s->tiles[k]; }
+  p.c_all = c + o; o += 2;
+  p.c_ih = c + o; o += (size_t)DS_MAXSEQ * s->nh;
+  p.c_h = c + o; o += s->nh;
+  o = align_up(o, 32);
+  p.f_na = c + o; o += 32;
+  p.f_nf = c + o; o += 32;
+  p.f_qkv = c + o; o += s->tiles[0];
+  p.f_attn = c + o; o += s->nh;
+  p.f_gu = c + o; o += s->tiles[2];
+  if (o > s->ctr_words) HS_FAIL(HS_E_INVAL, "dstack: counter layout overflow");
+  switch (BN) {
+    case 16: return launch_bn<16>(s, a, p, bi, st);
+    case 32: return launch_bn<32>(s, a, p, bi, st);
+    default: return launch_bn<64>(s, a, p, bi, st);
+  }
+}
+
+void warm_dstack() {
+  cudaFuncAttributes at;
+  cudaFuncSetAttribute(dstack_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, DsCfg<16>::SMEM);
+  cudaFuncSetAttribute(dstack_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, DsCfg<32>::SMEM);
+  cudaFuncSetAttribute(dstack_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, DsCfg<64>::SMEM);
+  cudaFuncGetAttributes(&at, dstack_kernel<16>);
+  cudaFuncGetAttributes(&at, dstack_kernel<32>);
+  cudaFuncGetAttributes(&at, dstack_kernel<64>);
+}
+
+}  // namespace hs
+
+extern "C" hs_status hs_debug_dstack_trace(int32_t enable, void* host_out, int64_t n_words) {
+  using namespace hs;
+  if (enable && !g_ds_trace) {
+    HS_CUDA(cudaMalloc(&g_ds_trace, kTraceWords * 8));
+    HS_CUDA(cudaMemset(g_ds_trace, 0, kTraceWords * 8));
+  }
+  if (host_out && g_ds_trace) {
+    HS_CUDA(cudaDeviceSynchronize());
+    HS_CUDA(cudaMemcpy(host_out, g_ds_trace, (size_t)std::min<int64_t>(n_words, kTraceWords) * 8, cudaMemcpyDeviceToHost));
+  }
+  if (!enable && g_ds_trace) {
+    cudaFree(g_ds_trace);
+    g_ds_trace = nullptr;
+  }
+  return HS_OK;
+}

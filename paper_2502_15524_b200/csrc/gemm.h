@@ -26,6 +26,10 @@ struct TmaMat {
 
 // Encodes a 128B-swizzled K-major tile map (box = 64 cols x box_rows rows).
 hs_status make_tma(TmaMat* t, const void* ptr, int64_t rows, int64_t cols, int box_rows);
+// Layered weight map [layers][rows][cols] (layers layer_stride_bytes apart), box 64 x 128 x 1:
+// one descriptor addresses the same matrix of every layer of a stage.
+hs_status make_tma3(TmaMat* t, const void* ptr, int64_t layers, int64_t layer_stride_bytes, int64_t rows,
+                    int64_t cols);
 
 // Decode-path fusions applied by the stream-K reduction (the whole output row of a token is
 // available there):

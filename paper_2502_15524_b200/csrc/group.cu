@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "common.h"
+#include "dstack.h"
 #include "gemm.h"
 #include "kernels.h"
 
@@ -105,6 +106,11 @@ struct Stage {
   TmaMat lm;
   TmaMat b_nrm[5], b_o[5], b_act[5], b_fin[5];
   const hs_image* img = nullptr;
+  // decode stack (dstack.h): workspace + layered weight maps of the current layer range
+  DstackState* ds = nullptr;
+  TmaMat ds_w[4];
+  int ds_lb = -1, ds_le = -1;
+  const void* ds_arena = nullptr;
 
   uint8_t* wptr(uint64_t image_off) const { return arena + (image_off - arena_off0); }
   bf16* kv_pool(int l, uint64_t layer_bytes) const {
@@ -161,9 +167,10 @@ static hs_status stage_of_layer(hs_group* g, int layer, int* out) {
 
 // ---- per-kernel-kind profile ------------------------------------------------------------
 enum ProfKind { PK_EMBED, PK_RMSNORM, PK_GEMM_QKV, PK_ROPE_KV, PK_ATTN, PK_GEMM_O, PK_GEMM_GU, PK_GEMM_DOWN,
-                PK_LM_HEAD, PK_ARGMAX, PK_SEND, PK_WAIT, PK_N };
+                PK_LM_HEAD, PK_ARGMAX, PK_SEND, PK_WAIT, PK_DSTACK, PK_N };
 static const char* kProfNames[PK_N] = {"embed", "rmsnorm", "gemm_qkv", "rope_kv", "attention", "gemm_o",
-                                       "gemm_gate_up", "gemm_down", "gemm_lm_head", "argmax", "send", "wait"};
+                                       "gemm_gate_up", "gemm_down", "gemm_lm_head", "argmax", "send", "wait",
+                                       "decode_stack"};
 
 static cudaEvent_t prof_event(hs_group* g, int dev) {
   auto& v = g->ev_free[dev];
@@ -215,6 +222,7 @@ static void free_stage(Stage& s) {
     F(s.act); F(s.fin); F(s.logits); F(s.ws); F(s.attn_ws); F(s.ctr); F(s.rope); F(s.d_meta); F(s.d_tok_out);
     if (s.h_meta) cudaFreeHost(s.h_meta);
     if (s.h_out) cudaFreeHost(s.h_out);
+    if (s.ds) dstack_destroy(s.ds);
     for (auto e : s.ev_layer) if (e) cudaEventDestroy(e);
     for (auto e : {s.ev_embed, s.ev_final, s.ev_l0, s.ev_l1, s.ev_c0, s.ev_c1, s.ev_bg0, s.ev_bg}) if (e) cudaEventDestroy(e);
     if (s.owns_streams && s.comp) cudaStreamDestroy(s.comp);
@@ -337,6 +345,7 @@ static hs_status setup_owned_stage(hs_group* g, int k) {
   HS_TRY(make_act_maps(s.b_fin, s.fin, std::max(S, 16), H));
   warm_gemm_kernels();
   warm_kernels();
+  warm_dstack();
   HS_CUDA(cudaDeviceSynchronize());
   return HS_OK;
 }
@@ -657,6 +666,63 @@ static hs_status run_layer(hs_group* g, Stage& s, int l, const bf16* x, bf16* xo
   return HS_OK;
 }
 
+// Decode through the decode-stack kernel (dstack.h): every layer of the stage in one launch.
+// Returns false in *used when the call's shape is not covered (the per-kernel path runs).
+static hs_status run_dstack(hs_group* g, Stage& s, const CallMeta& m, const uint8_t* meta, const bf16* x_in,
+                            bf16* x, const std::vector<int>& ctx, bool* used, bool* fin_done) {
+  *used = false;
+  const hs_model_cfg& c = g->cfg;
+  if (!m.decode || !dstack_supported(m.n, c.head_dim) || m.n != m.T) return HS_OK;
+  const int nl = s.le - s.lb;
+  if (nl < 1 || nl > 255) return HS_OK;
+  if (!s.ds) {
+    HS_TRY(dstack_create(&s.ds, c.hidden, c.ffn, c.n_heads, c.head_dim, g->kv.max_seqs, c.max_seq));
+  }
+  if (m.n > std::min(64, g->kv.max_seqs)) return HS_OK;
+  const hs_image_header& h = g->hdr;
+  if (s.ds_lb != s.lb || s.ds_le != s.le || s.ds_arena != s.arena) {
+    const uint64_t L0 = h.layer_off[s.lb];
+    HS_TRY(make_tma3(&s.ds_w[0], s.wptr(L0 + h.t_wqkv), nl, h.layer_bytes, 3 * c.hidden, c.hidden));
+    HS_TRY(make_tma3(&s.ds_w[1], s.wptr(L0 + h.t_wo), nl, h.layer_bytes, c.hidden, c.hidden));
+    HS_TRY(make_tma3(&s.ds_w[2], s.wptr(L0 + h.t_wgu), nl, h.layer_bytes, 2 * c.ffn, c.hidden));
+    HS_TRY(make_tma3(&s.ds_w[3], s.wptr(L0 + h.t_wd), nl, h.layer_bytes, c.hidden, c.ffn));
+    s.ds_lb = s.lb;
+    s.ds_le = s.le;
+    s.ds_arena = s.arena;
+  }
+  const uint64_t L0 = h.layer_off[s.lb];
+  DstackArgs a{};
+  a.N = m.n; a.H = c.hidden; a.F = c.ffn; a.nh = c.n_heads; a.hd = c.head_dim; a.nl = nl; a.eps = c.rms_eps;
+  a.wqkv = &s.ds_w[0]; a.wo = &s.ds_w[1]; a.wgu = &s.ds_w[2]; a.wd = &s.ds_w[3];
+  a.attn_norm = reinterpret_cast<const bf16*>(s.wptr(L0 + h.t_attn_norm));
+  a.ffn_norm = reinterpret_cast<const bf16*>(s.wptr(L0 + h.t_ffn_norm));
+  a.norm_stride = (int64_t)(h.layer_bytes / 2);
+  const bool model_last = s.le == c.n_layers;
+  a.final_norm = model_last ? reinterpret_cast<const bf16*>(s.wptr(h.final_off + h.t_final_norm)) : nullptr;
+  a.fin = s.fin;
+  a.x_in = x_in; a.x = x; a.hbuf = s.xb; a.nrm = s.nrm; a.q = s.q; a.o = s.o; a.act = s.act;
+  a.b_nrm = s.b_nrm; a.b_o = s.b_o; a.b_act = s.b_act;
+  a.pool = s.kv_pool(s.lb, g->kv_layer_bytes);
+  a.pool_stride = (int64_t)(g->kv_layer_bytes / 2);
+  a.nslots = g->kv.num_blocks * kBlock; a.nblocks = g->kv.num_blocks; a.max_blocks = g->max_blocks;
+  a.pos = reinterpret_cast<const int*>(meta + m.o_pos);
+  a.slot = reinterpret_cast<const int*>(meta + m.o_slot);
+  a.tables = reinterpret_cast<const int*>(meta + m.o_tab);
+  a.seqs = reinterpret_cast<const SeqDesc*>(meta + m.o_seqs);
+  a.rope = s.rope;
+  a.ctx = ctx.data();
+  {
+    const double H = c.hidden, F = c.ffn;
+    const double wbytes = (double)nl * 2.0 * (4 * H * H + 3 * F * H + 2 * H);
+    const double kv = (double)nl * 2.0 * 2 * H * (m.kv_tokens + m.n);
+    ProfScope ps(g, s, PK_DSTACK, true, wbytes + kv, 2.0 * m.n * (wbytes / 2) + 4.0 * H * m.attn_pairs * nl);
+    HS_TRY(dstack_launch(s.ds, a, s.comp));
+  }
+  *used = true;
+  *fin_done = model_last;
+  return HS_OK;
+}
+
 // Enqueues one call (prefill or decode) on every owned stage; returns after the tokens of
 // the call are on the host.
 //
@@ -691,6 +757,9 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
     for (int i = 0; i < m0.n; ++i) min_len = std::min(min_len, g->seqs[ids[i]].ctx);
     nchunks = std::max(1, std::min<int>({kMaxChunks, min_len / 16, m0.T / kChunkTokens}));
   }
+  std::vector<int> dctx;  // decode: keys per sequence after this step (decode-stack item split)
+  if (m0.decode)
+    for (int i = 0; i < m0.n; ++i) dctx.push_back(g->seqs[ids[i]].ctx);
   const unsigned ep0 = g->epoch + 1;   // chunk c is handed over with flag value ep0 + c
   g->epoch += nchunks;
   const unsigned ep = g->epoch;        // the call's final epoch (token broadcast)
@@ -809,7 +878,14 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
       for (int cidx = 0; cidx < nchunks; ++cidx) {
         HS_TRY(stage_input(cidx));
         normed = false;
-        for (int l = s.lb; l < s.le; ++l) {
+        bool used = false;
+        if (dec) {
+          for (int l = s.lb; l < s.le; ++l) HS_CUDA(cudaStreamWaitEvent(st, s.ev_layer[l], 0));
+          if (s.le == c.n_layers) HS_CUDA(cudaStreamWaitEvent(st, s.ev_final, 0));  // fused final norm
+          HS_TRY(run_dstack(g, s, ch[cidx].m, meta_of(cidx), is_first ? xrows(cidx) : in_rows(cidx), xrows(cidx),
+                            dctx, &used, &fin_done));
+        }
+        for (int l = s.lb; l < s.le && !used; ++l) {
           HS_CUDA(cudaStreamWaitEvent(st, s.ev_layer[l], 0));
           if (dec && l + 1 == c.n_layers) HS_CUDA(cudaStreamWaitEvent(st, s.ev_final, 0));  // fused final norm
           const bf16* xin = (l == s.lb && !is_first) ? in_rows(cidx) : xrows(cidx);
