@@ -34,6 +34,7 @@ namespace hs {
 constexpr int DS_THREADS = 384;
 constexpr int DS_MAXSEQ = 64;
 constexpr int DS_AWARPS = 8;   // attention warps per CTA (warps 4-11)
+// NC: tokens per register chunk in the tile epilogues (1 for single-sequence decode, else 8)
 
 struct DsParams {
   int N, H, F, nh, hd, nl, G;
@@ -56,7 +57,13 @@ struct DsParams {
   int ch;
   int pf_dist;  // weight k-blocks prefetched into L2 ahead of the ring
   float* ws_attn;
-  unsigned *c_tile[4], *c_all, *c_ih, *c_h, *f_na, *f_nf, *f_qkv, *f_attn, *f_gu;
+  unsigned *c_tile[4], *c_ih, *c_h, *f_qkv, *f_attn, *f_gu;
+  // distributed row norms: residual tiles publish sum-of-squares partials ssq[tile][64] and
+  // bump c_rows (cumulative); every CTA then normalises its column slice and bumps c_norm
+  // (cumulative).  Targets are launch bases + counts (wrap-safe compares).
+  float* ssq;
+  unsigned *c_rows, *c_norm;
+  unsigned base_rows, base_norm;
   unsigned long long* trace;  // optional: [G][nl][16] globaltimer stamps (hs_debug_dstack_trace)
 };
 
@@ -152,60 +159,76 @@ __device__ __noinline__ void wait_tag(const unsigned* f, unsigned tag) {
   }
 }
 
-// RMSNorm of N rows of src [N, H] into dst by the 256 threads of warps 4-11 (t = 0..255):
-// up to 8 rows at a time, 256 / ng threads per row; fixed summation order (per N).  Compact
-// rolled loops on purpose: this runs once per layer on whichever SM completed the last tile,
-// so its code is usually cold in that SM's instruction cache.
-__device__ __forceinline__ void ds_norm(const bf16* __restrict__ src, const bf16* __restrict__ w, bf16* __restrict__ dst,
-                                     int N, int H, float eps, int t, float* red) {
-  const int n8 = H >> 3;
-  int ng = 1;
-  while (ng * 2 <= min(N, 8)) ng *= 2;
-  const int tpg = 256 / ng, g = t / tpg, gt = t % tpg, wpg = tpg >> 5;
-  const uint4* w4 = reinterpret_cast<const uint4*>(w);
-  for (int r0 = 0; r0 < N; r0 += ng) {
-    const int r = r0 + g;
-    const uint4* s4 = reinterpret_cast<const uint4*>(src) + (size_t)r * n8;
-    float ss = 0.f;
-    if (r < N) {
-#pragma unroll 2
-      for (int c = gt; c < n8; c += tpg) {
-        const uint4 v = __ldcg(s4 + c);
-        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&v);
+// Sum of squares of one 128-row tile of the residual stream per token: thread et (0..127) holds
+// row et's bf16-rounded values v[j] for tokens n0 + j; warp xor-tree, then the 4 warps in
+// order.  The ONE summation used for every RMSNorm of the decode stack (stage inputs too), so
+// PP = s stays bitwise equal to PP = 1.  scratch: 4 * NC floats; bar 1 (warps 4-7).
+template <int NC>
+__device__ __forceinline__ void ds_ssq_chunk(const float* v, int n0, int N, int et, float* scratch, float* ssq_t) {
+  const int lane = et & 31, wq = et >> 5;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float2 f = __bfloat1622float2(p2[k]);
-          ss = fmaf(f.x, f.x, ss);
-          ss = fmaf(f.y, f.y, ss);
-        }
-      }
-    }
+  for (int j = 0; j < NC; ++j) {
+    float q = v[j] * v[j];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    if ((t & 31) == 0) red[t >> 5] = ss;
-    named_bar(2, 256);
-    float tot = 0.f;
-    for (int k = 0; k < wpg; ++k) tot += red[g * wpg + k];
-    const float rs = 1.0f / sqrtf(tot / (float)H + eps);
-    if (r < N) {
-      uint4* d4 = reinterpret_cast<uint4*>(dst) + (size_t)r * n8;
-#pragma unroll 2
-      for (int c = gt; c < n8; c += tpg) {
-        const uint4 v = __ldcg(s4 + c), wv = w4[c];
-        uint4 o;
-        const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&v);
-        const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&wv);
-        __nv_bfloat162* rr = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float2 x = __bfloat1622float2(a[k]), gg = __bfloat1622float2(b[k]);
-          rr[k] = __floats2bfloat162_rn(x.x * rs * gg.x, x.y * rs * gg.y);
-        }
-        d4[c] = o;
-      }
-    }
-    named_bar(2, 256);
+    for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    if (lane == 0) scratch[wq * NC + j] = q;
   }
+  named_bar(1, 128);
+  if (et < NC && n0 + et < N)
+    ssq_t[n0 + et] = (scratch[et] + scratch[NC + et]) + (scratch[2 * NC + et] + scratch[3 * NC + et]);
+  named_bar(1, 128);
+}
+
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Waits (thread 0 of warps 4-11, then bar 2) until a cumulative counter reached target.
+__device__ __forceinline__ void ds_wait_count(const unsigned* c, unsigned target, int t) {
+  if (t == 0) wait_tag(c, target);
+  named_bar(2, 256);
+}
+
+// One row-norm event of the decode stack, by warps 4-11 of EVERY CTA: rs[n] from the tile
+// partials (tile order), then this CTA's column slice of y = bf16(x * rs * w) for all rows,
+// then one release-add on c_norm.  dst == nullptr: nothing to normalise (count only).
+__device__ __forceinline__ void ds_norm_slice(const DsParams& p, const bf16* __restrict__ src,
+                                              const bf16* __restrict__ w, bf16* __restrict__ dst, int t, float* s_rs) {
+  const int T = p.H / 128;
+  if (dst) {
+    {  // rs[n]: the T tile partials of row n summed lane-parallel (fixed xor tree), warp w: n = w (mod 8)
+      const int wq = t >> 5, ln = t & 31;
+      for (int n = wq; n < p.N; n += 8) {
+        float acc = 0.f;
+        for (int tt = ln; tt < T; tt += 32) acc += __ldcg(p.ssq + (size_t)tt * DS_MAXSEQ + n);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (ln == 0) s_rs[n] = 1.0f / sqrtf(acc / (float)p.H + p.eps);
+      }
+    }
+    named_bar(2, 256);
+    const int n8 = p.H >> 3;
+    const int c0 = (int)((long long)blockIdx.x * n8 / p.G), c1 = (int)((long long)(blockIdx.x + 1) * n8 / p.G);
+    const int w8 = c1 - c0;
+    const uint4* w4 = reinterpret_cast<const uint4*>(w);
+    for (int idx = t; idx < p.N * w8; idx += 256) {
+      const int n = idx / w8, c = c0 + idx % w8;
+      const uint4 xv = __ldcg(reinterpret_cast<const uint4*>(src) + (size_t)n * n8 + c), wv = __ldg(w4 + c);
+      const float rs = s_rs[n];
+      uint4 o;
+      const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&xv);
+      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&wv);
+      __nv_bfloat162* rr = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 x = __bfloat1622float2(a[k]), g = __bfloat1622float2(b[k]);
+        rr[k] = __floats2bfloat162_rn(x.x * rs * g.x, x.y * rs * g.y);
+      }
+      reinterpret_cast<uint4*>(dst)[(size_t)n * n8 + c] = o;
+    }
+  }
+  named_bar(2, 256);
+  if (t == 0) red_release_add(p.c_norm, 1u);
 }
 
 // One attention unit: sequence i, head h, KV blocks [sp * DS_SPLIT, (sp + 1) * DS_SPLIT) of the
@@ -227,14 +250,12 @@ __device__ __forceinline__ void ds_attn_unit(const DsParams& p, int l, unsigned 
   const int n_keys = __shfl_sync(0xffffffffu, s.pos0 + 1, 0), nb = (n_keys + 15) >> 4;
   const int b0 = sp * p.ch, b1 = min(nb, b0 + p.ch);
   const int q_start = __shfl_sync(0xffffffffu, s.q_start, 0);
-  if (t == 0) {
-    const int tq = (h * D) / 128, th = H / 128;
-    wait_tag(p.f_qkv + tq, tag);
-    wait_tag(p.f_qkv + tq + th, tag);
-    wait_tag(p.f_qkv + tq + 2 * th, tag);
-    if (p.trace) DS_TR(TR_AT_FLAGS);
-  }
+  const int* tab = p.tables + (size_t)i * p.max_blocks;
+  // block ids of this warp's blocks (call metadata: independent of the flags, fetched first)
+  const int my_blk = (b0 + warp + lane * DS_AWARPS < b1) ? tab[b0 + warp + lane * DS_AWARPS] : 0;
+  if (t < 3) wait_tag(p.f_qkv + (h * D) / 128 + t * (H / 128), tag);  // q, k, v tiles of head h
   named_bar(2, 256);
+  if (p.trace && t == 0) DS_TR(TR_AT_FLAGS);
   const float scale = 1.4426950408889634f / sqrtf((float)D);
   float qv[E];
   {
@@ -251,14 +272,11 @@ __device__ __forceinline__ void ds_attn_unit(const DsParams& p, int l, unsigned 
     }
   }
   const bf16* pool = p.pool + (size_t)l * p.pool_stride;
-  const int* tab = p.tables + (size_t)i * p.max_blocks;
   const size_t vstride = (size_t)p.nh * 16 * D;
   float m = -INFINITY, lsum = 0.f, acc[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) acc[e] = 0.f;
   using VT = typename std::conditional<E == 4, uint2, unsigned>::type;
-  // this warp's block ids, loaded lane-parallel up front (<= 32 blocks per warp per unit)
-  const int my_blk = (b0 + warp + lane * DS_AWARPS < b1) ? tab[b0 + warp + lane * DS_AWARPS] : 0;
   for (int b = b0 + warp, bi = 0; b < b1; b += DS_AWARPS, ++bi) {
     int blk = __shfl_sync(0xffffffffu, my_blk, bi & 31);
     if (bi >= 32) blk = tab[b];
@@ -376,13 +394,30 @@ __device__ __forceinline__ void ds_attn_unit(const DsParams& p, int l, unsigned 
   }
 }
 
+// Sum of the np stream-K parts (in part order) of tile row ml for tokens n0 .. n0 + NC - 1,
+// with every load of a part group in flight together (the tail of each tile is latency bound).
+template <int NC>
+__device__ __forceinline__ void ds_part_sums(const float* tws, int np, int n0, int N, int ml, float* a, int BN) {
+#pragma unroll
+  for (int j = 0; j < NC; ++j) a[j] = 0.f;
+#pragma unroll 2
+  for (int pt = 0; pt < np; ++pt) {
+    float v[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j)
+      v[j] = n0 + j < N ? __ldcg(tws + (size_t)pt * BN * 128 + (size_t)(n0 + j) * 128 + ml) : 0.f;
+#pragma unroll
+    for (int j = 0; j < NC; ++j) a[j] += v[j];
+  }
+}
+
 // The epilogue warps' part of GEMM kind k (0 qkv, 1 o, 2 gate_up, 3 down) of layer l: drains
 // the CTA's stream-K segments; the last arriver of a tile applies the epilogue.  Returns the
 // running segment count (TMEM double-buffer phase).
-template <int BN>
+template <int BN, int NC>
 __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsigned tag, int seg, uint32_t tmem,
                                            uint64_t* tfull, uint64_t* tempty, float* vals, volatile int* flag,
-                                           volatile unsigned* norm_tag, int et, int lane, int quad,
+                                           int et, int lane, int quad,
                                            const int* s_pos, const int* s_slot, const float2* s_rope) {
   const int nkb = p.nkb[k], tiles = p.tiles[k];
   const long long W = (long long)tiles * nkb;
@@ -446,10 +481,12 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
     const int m = t * 128 + ml;
     const int H = p.H;
     if (k == 0) {  // bf16(q, k, v); RoPE of q, k; k', v -> paged pool; q' -> q
-      for (int n = 0; n < p.N; ++n) {
-        float a = 0.f;
-        for (int pt = 0; pt < np; ++pt) a += __ldcg(tws + (size_t)pt * BN * 128 + (size_t)n * 128 + ml);
-        vals[ml * BN + n] = __bfloat162float(__float2bfloat16_rn(a));
+      for (int n0 = 0; n0 < p.N; n0 += NC) {
+        float a[NC];
+        ds_part_sums<NC>(tws, np, n0, p.N, ml, a, BN);
+#pragma unroll
+        for (int j = 0; j < NC; ++j)
+          if (n0 + j < p.N) vals[ml * BN + n0 + j] = __bfloat162float(__float2bfloat16_rn(a[j]));
       }
       named_bar(1, 128);
       if (et == 0) DS_TR(TR_Q_VALS);
@@ -485,38 +522,42 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
       if (et == 0) DS_TR(TR_Q_PUB);
       if (et == 0 && p.trace && t < 128) p.trace[(size_t)p.G * p.nl * 32 + (size_t)l * 256 + t] = gtimer();
     } else if (k == 2) {  // a = bf16(silu(g) * u): lanes 0-15 gate rows, 16-31 their up rows
-      for (int n = 0; n < p.N; ++n) {
-        float a = 0.f;
-        for (int pt = 0; pt < np; ++pt) a += __ldcg(tws + (size_t)pt * BN * 128 + (size_t)n * 128 + ml);
-        const float u = __shfl_xor_sync(0xffffffffu, a, 16);
-        if (lane < 16) p.act[(size_t)n * p.F + (m >> 5) * 16 + lane] = __float2bfloat16_rn(silu_f(a) * u);
+      for (int n0 = 0; n0 < p.N; n0 += NC) {
+        float a[NC];
+        ds_part_sums<NC>(tws, np, n0, p.N, ml, a, BN);
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          const float u = __shfl_xor_sync(0xffffffffu, a[j], 16);
+          if (lane < 16 && n0 + j < p.N)
+            p.act[(size_t)(n0 + j) * p.F + (m >> 5) * 16 + lane] = __float2bfloat16_rn(silu_f(a[j]) * u);
+        }
       }
       named_bar(1, 128);
       if (et == 0) publish(p.f_gu + t, tag);
     } else {  // residual: h = bf16(x + o W_o^T) (k = 1) / x' = bf16(h + a W_d^T) (k = 3)
       const bf16* resid = k == 1 ? (l == 0 ? p.x_in : p.x) : p.hbuf;
       bf16* out = k == 1 ? p.hbuf : p.x;
-      for (int n = 0; n < p.N; ++n) {
-        float a = 0.f;
-        for (int pt = 0; pt < np; ++pt) a += __ldcg(tws + (size_t)pt * BN * 128 + (size_t)n * 128 + ml);
-        out[(size_t)n * H + m] = __float2bfloat16_rn(a + __bfloat162float(__ldcg(resid + (size_t)n * H + m)));
-      }
-      named_bar(1, 128);
-      if (et == 0) {  // grid-level arrival: the CTA completing the last tile normalises the rows
-        unsigned* ca = p.c_all + (k == 1 ? 0 : 1);
-        const unsigned old = atom_add_acq_rel(ca, 1u);
-        if (old == (unsigned)(tiles - 1)) {
-          *ca = 0;
-          norm_tag[k == 1 ? 0 : 1] = tag;
-          DS_TR(k == 1 ? TR_O_LAST : TR_D_LAST);
+      for (int n0 = 0; n0 < p.N; n0 += NC) {
+        float r[NC], a[NC];
+#pragma unroll
+        for (int j = 0; j < NC; ++j)
+          r[j] = n0 + j < p.N ? __bfloat162float(__ldcg(resid + (size_t)(n0 + j) * H + m)) : 0.f;
+        ds_part_sums<NC>(tws, np, n0, p.N, ml, a, BN);
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          const bf16 y = __float2bfloat16_rn(a[j] + r[j]);
+          a[j] = n0 + j < p.N ? __bfloat162float(y) : 0.f;
+          if (n0 + j < p.N) out[(size_t)(n0 + j) * H + m] = y;
         }
+        ds_ssq_chunk<NC>(a, n0, p.N, et, vals, p.ssq + (size_t)t * DS_MAXSEQ);
       }
+      if (et == 0) red_release_add(p.c_rows, 1u);  // rows of this tile + their partial sums
     }
   }
   return seg;
 }
 
-template <int BN>
+template <int BN, int NC>
 __global__ void __launch_bounds__(DS_THREADS, 1)
     dstack_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant__ CUtensorMap tw1,
                   const __grid_constant__ CUtensorMap tw2, const __grid_constant__ CUtensorMap tw3,
@@ -536,7 +577,6 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   volatile int* flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
-  volatile unsigned* norm_tag = reinterpret_cast<volatile unsigned*>(tmem_slot + 2);  // [2]
   float* red = reinterpret_cast<float*>(tmem_slot + 4);                                // [8]
   int* s_nc = reinterpret_cast<int*>(red + 8);                                         // [64]
   int* s_base = s_nc + DS_MAXSEQ;                                                      // [65]
@@ -549,8 +589,6 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 2); mbar_init(&empty[s], 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    norm_tag[0] = 0;
-    norm_tag[1] = 0;
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -645,8 +683,8 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
         int beg, end, Gk;
         ds_range(blockIdx.x, W, G, beg, end, Gk);
         if (beg == end) continue;
-        if (k == 0 || k == 2) {  // one flag for the whole phase (a row norm)
-          if (lane == 0) wait_tag(k == 0 ? p.f_na : p.f_nf, tag);
+        if (k == 0 || k == 2) {  // the row norm feeding this GEMM: every CTA's slice written
+          if (lane == 0) wait_tag(p.c_norm, p.base_norm + (unsigned)(2 * l + (k == 0 ? 1 : 2)) * (unsigned)G);
           __syncwarp();
         }
         for (int x0 = beg; x0 < end; x0 += 32) {
@@ -718,23 +756,27 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
     // One call site per routine (they are inlined into a warp-uniform context and their code
     // stays resident in the instruction cache): step (l, k) = [pending row norm] -> GEMM k's
     // segments (epilogue warps) -> attention (k = 0) -> grid-last check (k = 1, 3).
-    bool pend = blockIdx.x == 0;  // the stage input's attn RMSNorm (layer 0)
-    const bf16* n_src = p.x_in;
-    const bf16* n_w = p.attn_norm;
-    bf16* n_dst = p.nrm;
-    unsigned* n_flag = p.f_na;
-    unsigned n_tag = p.tag0;
-    for (int step = 0; step <= 4 * p.nl; ++step) {
-      const int l = step >> 2, k = step & 3;
-      if (pend) {
-        ds_norm(n_src, n_w, n_dst, p.N, p.H, p.eps, t256, red);
-        if (n_flag && t256 == 0) publish(n_flag, n_tag);
-        if (t256 == 0 && step < 4 * p.nl) DS_TR(n_flag == p.f_nf ? TR_E_NF : TR_E_NA);
-        pend = false;
+    const int T = p.H / 128;
+    {  // the stage input's RMSNorm (layer 0): CTA c < T publishes tile c's partial sums of x_in
+      if (blockIdx.x < T && epi) {
+        for (int n0 = 0; n0 < p.N; n0 += NC) {
+          float v[NC];
+#pragma unroll
+          for (int j = 0; j < NC; ++j)
+            v[j] = n0 + j < p.N ? __bfloat162float(__ldcg(p.x_in + (size_t)(n0 + j) * p.H + blockIdx.x * 128 + t256)) : 0.f;
+          ds_ssq_chunk<NC>(v, n0, p.N, t256, vals, p.ssq + (size_t)blockIdx.x * DS_MAXSEQ);
+        }
+        if (t256 == 0) red_release_add(p.c_rows, 1u);
       }
-      if (step == 4 * p.nl) break;
+      ds_wait_count(p.c_rows, p.base_rows + (unsigned)T, t256);
+      ds_norm_slice(p, p.x_in, p.attn_norm, p.nrm, t256, s_att);
+      const int l = 0;
+      if (t256 == 0) DS_TR(TR_E_NA);
+    }
+    for (int step = 0; step < 4 * p.nl; ++step) {
+      const int l = step >> 2, k = step & 3;
       const unsigned tag = p.tag0 + l;
-      if (epi) seg = ds_segments<BN>(p, k, l, tag, seg, tmem, tfull, tempty, vals, flag, norm_tag, t256, lane, quad,
+      if (epi) seg = ds_segments<BN, NC>(p, k, l, tag, seg, tmem, tfull, tempty, vals, flag, t256, lane, quad,
                                      s_pos, s_slot, s_rope);
       if (t256 == 0) DS_TR(TR_E_QKV + (k == 0 ? 0 : k == 1 ? 2 : k == 2 ? 4 : 5));
       if (k == 0) {
@@ -748,19 +790,17 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
           else ds_attn_unit<64>(p, l, tag, i, r / nsp, r % nsp, nsp, u, t256, s_att);
         }
         if (t256 == 0) DS_TR(TR_E_ATTN);
-      } else if (k == 1 || k == 3) {
-        named_bar(2, 256);
-        if (__shfl_sync(0xffffffffu, norm_tag[k >> 1], 0) == tag) {  // this CTA completed the last tile
-          if (k == 1) {
-            pend = true; n_src = p.hbuf; n_w = p.ffn_norm + (size_t)l * p.norm_stride; n_dst = p.nrm;
-            n_flag = p.f_nf; n_tag = tag;
-          } else if (l + 1 < p.nl) {
-            pend = true; n_src = p.x; n_w = p.attn_norm + (size_t)(l + 1) * p.norm_stride; n_dst = p.nrm;
-            n_flag = p.f_na; n_tag = tag + 1;
-          } else if (p.final_norm) {
-            pend = true; n_src = p.x; n_w = p.final_norm; n_dst = p.fin; n_flag = nullptr;
-          }
-        }
+      } else if (k == 1 || k == 3) {  // row-norm event 2l+1 (ffn) / 2l+2 (next attn or final)
+        const unsigned ev = (unsigned)(2 * l + (k == 1 ? 1 : 2));
+        ds_wait_count(p.c_rows, p.base_rows + (unsigned)T * (ev + 1), t256);
+        if (t256 == 0) DS_TR(k == 1 ? TR_O_LAST : TR_D_LAST);
+        if (k == 1)
+          ds_norm_slice(p, p.hbuf, p.ffn_norm + (size_t)l * p.norm_stride, p.nrm, t256, s_att);
+        else if (l + 1 < p.nl)
+          ds_norm_slice(p, p.x, p.attn_norm + (size_t)(l + 1) * p.norm_stride, p.nrm, t256, s_att);
+        else
+          ds_norm_slice(p, p.x, p.final_norm, p.final_norm ? p.fin : nullptr, t256, s_att);
+        if (t256 == 0) DS_TR(k == 1 ? TR_E_NF : TR_E_NA);
       }
     }
   }
@@ -782,6 +822,8 @@ struct DstackState {
   unsigned* ctr = nullptr;
   size_t ctr_words = 0;
   unsigned seq_no = 0;
+  float* ssq = nullptr;                 // [H / 128][64] row sum-of-squares partials
+  unsigned base_rows = 0, base_norm = 0;  // cumulative counter values at the next launch
 };
 
 // HS debug: per-CTA phase timestamps of the last launch (hs_debug_dstack_trace)
@@ -826,6 +868,7 @@ hs_status dstack_create(DstackState** out, int H, int F, int nh, int hd, int max
   s->ctr_words = 4096 + (size_t)DS_MAXSEQ * nh + 4 * (size_t)(s->tiles[0] + s->tiles[1] + s->tiles[2] + s->tiles[3]);
   if (e == cudaSuccess) e = cudaMalloc(&s->ctr, s->ctr_words * 4);
   if (e == cudaSuccess) e = cudaMemset(s->ctr, 0, s->ctr_words * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&s->ssq, (size_t)(H / 128) * DS_MAXSEQ * 4);
   if (e != cudaSuccess) {
     dstack_destroy(s);
     HS_FAIL(e == cudaErrorMemoryAllocation ? HS_E_OOM : HS_E_CUDA, "dstack workspace: %s", cudaGetErrorString(e));
@@ -840,15 +883,16 @@ void dstack_destroy(DstackState* s) {
   if (s->ws) cudaFree(s->ws);
   if (s->ws_attn) cudaFree(s->ws_attn);
   if (s->ctr) cudaFree(s->ctr);
+  if (s->ssq) cudaFree(s->ssq);
   delete s;
 }
 
-template <int BN>
+template <int BN, int NC>
 static hs_status launch_bn(DstackState* s, const DstackArgs& a, const DsParams& p, int bi, cudaStream_t st) {
   using C = DsCfg<BN>;
   static bool attr_set[64] = {};
   if (s->device < 64 && !attr_set[s->device]) {
-    HS_CUDA(cudaFuncSetAttribute(dstack_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    HS_CUDA(cudaFuncSetAttribute(dstack_kernel<BN, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr_set[s->device] = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -868,7 +912,7 @@ static hs_status launch_bn(DstackState* s, const DstackArgs& a, const DsParams& 
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  HS_CUDA(cudaLaunchKernelEx(&cfg, dstack_kernel<BN>, a.wqkv->map, a.wo->map, a.wgu->map, a.wd->map, a.b_nrm[bi].map,
+  HS_CUDA(cudaLaunchKernelEx(&cfg, dstack_kernel<BN, NC>, a.wqkv->map, a.wo->map, a.wgu->map, a.wd->map, a.b_nrm[bi].map,
                              a.b_o[bi].map, a.b_act[bi].map, p));
   count_launch();
   return HS_OK;
@@ -876,7 +920,7 @@ static hs_status launch_bn(DstackState* s, const DstackArgs& a, const DsParams& 
 
 hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
   if (!dstack_supported(a.N, a.hd) || a.N > s->max_seqs || a.H != s->H || a.F != s->F || a.nh != s->nh ||
-      a.hd != s->hd || a.nl < 1 || a.nl > 255)
+      a.hd != s->hd || a.nl < 1 || a.nl > 255 || a.H / 128 > s->G)
     HS_FAIL(HS_E_INVAL, "dstack: unsupported call (N=%d nl=%d)", a.N, a.nl);
   const int BN = gemm_bn(a.N);
   if (BN > s->bn_max) HS_FAIL(HS_E_INVAL, "dstack: N=%d above the workspace's tile width", a.N);
@@ -930,31 +974,37 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
   unsigned* c = s->ctr;
   size_t o = 0;
   for (int k = 0; k < 4; ++k) { p.c_tile[k] = c + o; o += s->tiles[k]; }
-  p.c_all = c + o; o += 2;
   p.c_ih = c + o; o += (size_t)DS_MAXSEQ * s->nh;
   p.c_h = c + o; o += s->nh;
   o = align_up(o, 32);
-  p.f_na = c + o; o += 32;
-  p.f_nf = c + o; o += 32;
+  p.c_rows = c + o; o += 32;
+  p.c_norm = c + o; o += 32;
   p.f_qkv = c + o; o += s->tiles[0];
   p.f_attn = c + o; o += s->nh;
   p.f_gu = c + o; o += s->tiles[2];
+  p.ssq = s->ssq;
+  p.base_rows = s->base_rows;
+  p.base_norm = s->base_norm;
+  s->base_rows += (unsigned)(s->H / 128) * (unsigned)(2 * a.nl + 1);
+  s->base_norm += (unsigned)s->G * (unsigned)(2 * a.nl + 1);
   if (o > s->ctr_words) HS_FAIL(HS_E_INVAL, "dstack: counter layout overflow");
   switch (BN) {
-    case 16: return launch_bn<16>(s, a, p, bi, st);
-    case 32: return launch_bn<32>(s, a, p, bi, st);
-    default: return launch_bn<64>(s, a, p, bi, st);
+    case 16: return a.N == 1 ? launch_bn<16, 1>(s, a, p, bi, st) : launch_bn<16, 8>(s, a, p, bi, st);
+    case 32: return launch_bn<32, 8>(s, a, p, bi, st);
+    default: return launch_bn<64, 8>(s, a, p, bi, st);
   }
 }
 
 void warm_dstack() {
   cudaFuncAttributes at;
-  cudaFuncSetAttribute(dstack_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, DsCfg<16>::SMEM);
-  cudaFuncSetAttribute(dstack_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, DsCfg<32>::SMEM);
-  cudaFuncSetAttribute(dstack_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, DsCfg<64>::SMEM);
-  cudaFuncGetAttributes(&at, dstack_kernel<16>);
-  cudaFuncGetAttributes(&at, dstack_kernel<32>);
-  cudaFuncGetAttributes(&at, dstack_kernel<64>);
+  cudaFuncSetAttribute(dstack_kernel<16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, DsCfg<16>::SMEM);
+  cudaFuncSetAttribute(dstack_kernel<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, DsCfg<16>::SMEM);
+  cudaFuncSetAttribute(dstack_kernel<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, DsCfg<32>::SMEM);
+  cudaFuncSetAttribute(dstack_kernel<64, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, DsCfg<64>::SMEM);
+  cudaFuncGetAttributes(&at, dstack_kernel<16, 1>);
+  cudaFuncGetAttributes(&at, dstack_kernel<16, 8>);
+  cudaFuncGetAttributes(&at, dstack_kernel<32, 8>);
+  cudaFuncGetAttributes(&at, dstack_kernel<64, 8>);
 }
 
 }  // namespace hs

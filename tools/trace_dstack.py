@@ -13,7 +13,7 @@ from paper_2502_15524_b200 import hs  # noqa: E402
 
 NAMES = ["B0 qkv act", "B1 o act", "B2 gu act", "B3 down act", "B3 down act end", "E qkv done", "E attn done",
          "E o done", "E norm_f", "E gu done", "E down done", "E norm_a", "A1 o w", "A2 gu w", "A3 down w", "A0 qkv w",
-         "o grid-last", "o norm start", "o norm done", "d grid-last", "d norm start", "d norm done",
+         "o grid-last", "o norm pass1 (wave 0)", "o norm pass2 (wave 0)", "d grid-last", "d norm start", "d norm done",
          "attn flags ok", "attn kv done", "qkv tfull", "qkv last-arriver", "qkv published",
          "qkv seg0 drained", "qkv seg0 atom", "qkv vals", "qkv stores", "attn item end"]
 
