@@ -242,7 +242,7 @@ constexpr int DS_SPLIT = 64;  // KV blocks (1024 tokens) per unit
 
 template <int D>
 __device__ __forceinline__ void ds_attn_unit(const DsParams& p, int l, unsigned tag, int i, int h, int sp, int nsp,
-                                             int u, int t, float* sm) {
+                                             int u, int t, float* sm, int uph, const int* s_nc, const int* s_base) {
   constexpr int E = D / 32;
   const int warp = t >> 5, lane = t & 31;
   const int H = p.nh * D;
@@ -350,48 +350,50 @@ __device__ __forceinline__ void ds_attn_unit(const DsParams& p, int l, unsigned 
     }
   }
   bf16* orow = p.o + (size_t)q_start * H + h * D;
-  bool head_arrive = true;
-  if (nsp > 1) {  // long context: partial of this split, the last split merges in split order
+  if (nsp > 1) {  // long context: partial of this split (merged by the head's last unit)
     float* w = p.ws_attn + (size_t)u * (D + 4);
     if (t == 0) { w[0] = M; w[1] = L; }
     if (t < D) w[4 + t] = A;
-    named_bar(2, 256);
-    if (t == 0) {
-      unsigned* cc = p.c_ih + (size_t)i * p.nh + h;
-      const unsigned old = atom_add_acq_rel(cc, 1u);
-      const int last = old == (unsigned)(nsp - 1);
-      if (last) *cc = 0;
-      sm_m[0] = last ? 1.f : 0.f;
-    }
-    named_bar(2, 256);
-    head_arrive = sm_m[0] != 0.f;
-    if (head_arrive && t < D) {
-      const float* w0 = p.ws_attn + (size_t)(u - sp) * (D + 4);
+  } else if (t < D) {
+    orow[t] = __float2bfloat16_rn(A / L);
+  }
+  named_bar(2, 256);
+  // one arrival per unit on the head's counter; the last unit of the head merges the splits
+  // of every sequence (split order) and publishes the head
+  if (t == 0) {
+    if (p.trace) DS_TR(TR_AT_END);
+    const unsigned old = atom_add_acq_rel(p.c_h + h, 1u);
+    const int last = old == (unsigned)(uph - 1);
+    if (last) p.c_h[h] = 0;
+    sm_m[0] = last ? 1.f : 0.f;
+  }
+  named_bar(2, 256);
+  const bool last = sm_m[0] != 0.f;
+  if (last) {
+    for (int i2 = 0; i2 < p.N; ++i2) {
+      const int ns = s_nc[i2];
+      if (ns < 2 || t >= D) continue;
+      const float* w0 = p.ws_attn + (size_t)(s_base[i2] + h * ns) * (D + 4);
       float MM = -INFINITY;
-      for (int k = 0; k < nsp; ++k) MM = fmaxf(MM, __ldcg(w0 + (size_t)k * (D + 4)));
+      for (int k = 0; k < ns; ++k) MM = fmaxf(MM, __ldcg(w0 + (size_t)k * (D + 4)));
       float LL = 0.f, AA = 0.f;
-      for (int k = 0; k < nsp; ++k) {
+      for (int k = 0; k < ns; ++k) {
         const float* wk = w0 + (size_t)k * (D + 4);
         const float ms = __ldcg(wk);
         const float f = ms == -INFINITY ? 0.f : exp2f(ms - MM);
         LL += __ldcg(wk + 1) * f;
         AA += __ldcg(wk + 4 + t) * f;
       }
-      orow[t] = __float2bfloat16_rn(AA / LL);
+      const int qs = p.seqs[i2].q_start;
+      p.o[(size_t)qs * H + h * D + t] = __float2bfloat16_rn(AA / LL);
     }
-  } else if (t < D) {
-    orow[t] = __float2bfloat16_rn(A / L);
-  }
-  named_bar(2, 256);  // o written (and sm reusable)
-  if (head_arrive && t == 0) {
-    if (p.trace) DS_TR(TR_AT_END);
-    const unsigned old = atom_add_acq_rel(p.c_h + h, 1u);
-    if (old == (unsigned)(p.N - 1)) {
-      p.c_h[h] = 0;
+    named_bar(2, 256);
+    if (t == 0) {
       publish(p.f_attn + h, tag);
       if (p.trace && h < 64) p.trace[(size_t)p.G * p.nl * 32 + (size_t)l * 256 + 128 + h] = gtimer();
     }
   }
+  named_bar(2, 256);  // sm reusable
 }
 
 // Sum of the np stream-K parts (in part order) of tile row ml for tokens n0 .. n0 + NC - 1,
@@ -786,8 +788,8 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
           while (i + 1 < p.N && s_base[i + 1] <= u) ++i;
           i = __shfl_sync(0xffffffffu, i, 0);
           const int nsp = __shfl_sync(0xffffffffu, s_nc[i], 0), r = u - __shfl_sync(0xffffffffu, s_base[i], 0);
-          if (p.hd == 128) ds_attn_unit<128>(p, l, tag, i, r / nsp, r % nsp, nsp, u, t256, s_att);
-          else ds_attn_unit<64>(p, l, tag, i, r / nsp, r % nsp, nsp, u, t256, s_att);
+          if (p.hd == 128) ds_attn_unit<128>(p, l, tag, i, r / nsp, r % nsp, nsp, u, t256, s_att, total / p.nh, s_nc, s_base);
+          else ds_attn_unit<64>(p, l, tag, i, r / nsp, r % nsp, nsp, u, t256, s_att, total / p.nh, s_nc, s_base);
         }
         if (t256 == 0) DS_TR(TR_E_ATTN);
       } else if (k == 1 || k == 3) {  // row-norm event 2l+1 (ffn) / 2l+2 (next attn or final)
