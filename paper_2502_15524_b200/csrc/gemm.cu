@@ -159,11 +159,14 @@ __global__ void __launch_bounds__(128, 1)
     } else if (p.epi == EPI_RESID) {
       bf16* o = reinterpret_cast<bf16*>(p.out) + (size_t)(n0 + c0) * p.ldo;
       const bf16* r = p.resid + (size_t)(n0 + c0) * p.ldr;
-      if (m < p.M)
+      if (m < p.M) {
+        float rv[CH];  // loads first: out may alias resid for the compiler
+#pragma unroll
+        for (int j = 0; j < CH; ++j) rv[j] = j < ncol ? __bfloat162float(__ldg(r + (size_t)j * p.ldr + m)) : 0.f;
 #pragma unroll
         for (int j = 0; j < CH; ++j)
-          if (j < ncol)
-            o[(size_t)j * p.ldo + m] = __float2bfloat16_rn(v[j] + __bfloat162float(r[(size_t)j * p.ldr + m]));
+          if (j < ncol) o[(size_t)j * p.ldo + m] = __float2bfloat16_rn(v[j] + rv[j]);
+      }
     } else {  // EPI_SILU_MUL: lanes 0-15 gate rows, 16-31 the matching up rows
       bf16* o = reinterpret_cast<bf16*>(p.out) + (size_t)(n0 + c0) * p.ldo;
       const int f = (m0 + warp * 32) / 2 + lane;
@@ -668,9 +671,14 @@ __global__ void __launch_bounds__(192, 1)
           } else if (p.epi == EPI_RESID) {
             bf16* o = reinterpret_cast<bf16*>(p.out) + (size_t)(n0 + c0) * p.ldo;
             const bf16* r = p.resid + (size_t)(n0 + c0) * p.ldr;
+            // all residual loads first (out may alias resid for the compiler: interleaving the
+            // loads with the stores would serialise 32 L2 round trips per chunk)
+            float rv[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) rv[j] = j < ncol ? __bfloat162float(__ldg(r + (size_t)j * p.ldr + m)) : 0.f;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (j < ncol) o[(size_t)j * p.ldo + m] = __float2bfloat16_rn(v[j] + __bfloat162float(r[(size_t)j * p.ldr + m]));
+              if (j < ncol) o[(size_t)j * p.ldo + m] = __float2bfloat16_rn(v[j] + rv[j]);
           } else {
             bf16* o = reinterpret_cast<bf16*>(p.out) + (size_t)(n0 + c0) * p.ldo;
             const int f = (m0 + quad * 32) / 2 + lane;
