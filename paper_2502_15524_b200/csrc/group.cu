@@ -155,6 +155,7 @@ struct hs_group {
   std::map<int, std::vector<cudaEvent_t>> ev_free;  // per device
   struct ProfAcc { uint64_t count = 0; double ms = 0, bytes = 0, flops = 0; };
   std::map<int, ProfAcc> prof_acc;
+  std::vector<void*> ipc_deferred;  // peer mappings of released stages, closed at destroy
 };
 
 namespace hs {
@@ -360,6 +361,8 @@ static hs_status validate_image(hs_group* g, const hs_image* im, uint64_t b, uin
 }
 
 // ------------------------------------------------------------------ create ---------------
+static hs_status open_peer_memory(hs_group* g, Stage& s);
+
 static hs_status create(const hs_model_cfg* cfg, const hs_plan* plan, const hs_image* image,
                         const hs_image* stage_images, const hs_kv_cfg* kv, const hs_comm* comm,
                         hs_group** out) {
@@ -469,6 +472,11 @@ static hs_status create(const hs_model_cfg* cfg, const hs_plan* plan, const hs_i
       s.comm = reinterpret_cast<uint8_t*>(p);
       s.ipc_comm_open = true;
     }
+    // a full-memory stage (a consolidation target) maps every peer's arena and KV pools now,
+    // before T0: opening large IPC allocations costs ~100 ms that must not land in the pause
+    if (me.full_memory)
+      for (int k = 0; k < pp; ++k)
+        if (k != g->owned_stage) HS_TRY(open_peer_memory(g.get(), g->st[k]));
     if (g->comm.barrier(g->comm.ctx) != 0) HS_FAIL(HS_E_STATE, "barrier failed");
   }
   *out = g.release();
@@ -1107,6 +1115,8 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
     HS_CUDA(cudaStreamSynchronize(s.copy));
   }
   if (g->spmd && g->comm.barrier(g->comm.ctx) != 0) HS_FAIL(HS_E_STATE, "barrier failed");
+  const auto t_drained = std::chrono::steady_clock::now();
+  auto t_copied = t_drained;
   Stage& T = g->st[tgt];
   if (T.owned) {
     DeviceGuard dg(T.device);
@@ -1123,7 +1133,7 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
     //    blocks of every live sequence for those layers, placed at the same block ids ("collect
     //    these blocks from all workers with a gather operation ... placed at different layers,
     //    according to which worker it comes from")
-    const uint64_t piece = 64ull << 10;
+    const uint64_t piece = 1ull << 20;
     std::vector<CopyDesc> list;
     auto add = [&](uint64_t src, uint64_t dst, uint64_t bytes) {
       for (uint64_t o = 0; o < bytes; o += piece) list.push_back({src + o, dst + o, std::min(piece, bytes - o)});
@@ -1181,6 +1191,7 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
     T.load_issued = true;
   }
   if (g->spmd && g->comm.barrier(g->comm.ctx) != 0) HS_FAIL(HS_E_STATE, "barrier failed");
+  t_copied = std::chrono::steady_clock::now();
   // 5. release the other stages ("other workers are terminated"); a stage
   //    sharing the target's device hands its streams over first
   for (int k : g->active)
@@ -1190,12 +1201,28 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
       T.owns_streams = true;
     }
   for (int k : g->active)
-    if (k != tgt) free_stage(g->st[k]);
+    if (k != tgt) {
+      Stage& S = g->st[k];
+      if (!S.owned && S.ipc_arena_open) {  // unmapping ~GBs costs ~100 ms: defer it to destroy
+        g->ipc_deferred.push_back(S.arena);
+        g->ipc_deferred.push_back(S.kv_mem);
+        S.ipc_arena_open = false;
+        S.arena = nullptr;
+        S.kv_mem = nullptr;
+      }
+      free_stage(S);
+    }
   g->active = {tgt};
   g->st[tgt].lb = 0;
   g->st[tgt].le = c.n_layers;
   g->plan.pp = 1;
   stats.pause_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_enter).count();
+  if (getenv("HS_DEBUG_CONS"))
+    fprintf(stderr, "[hs] consolidate: drain %.1f ms, copy-list build+copy %.1f ms, free %.1f ms, total %.1f ms\n",
+            1e3 * std::chrono::duration<double>(t_drained - t_enter).count(),
+            1e3 * std::chrono::duration<double>(t_copied - t_drained).count(),
+            1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t_copied).count(),
+            1e3 * stats.pause_seconds);
   if (out) *out = stats;
   return HS_OK;
 }
@@ -1443,6 +1470,8 @@ extern "C" hs_status hs_group_destroy(hs_group* g) {
   }
   for (auto& s : g->st)
     if (!s.owned) free_stage(s);
+  for (void* p : g->ipc_deferred)
+    if (p) cudaIpcCloseMemHandle(p);
   for (auto& s : g->st)
     if (s.owned) free_stage(s);
   delete g;
