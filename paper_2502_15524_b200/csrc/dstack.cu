@@ -615,8 +615,10 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
         const int s = i % C::STAGES;
         const uint32_t par = ((i / C::STAGES) & 1) ^ 1;
         unsigned long long t0 = 0;
+        unsigned long long tw = 0;  // a dependency stall (not steady streaming): prefetch into L2
         for (unsigned it = 0; !mbar_test(&empty[s], par); ++it) {
-          if (pf_ok && j < i + p.pf_dist) {
+          if (p.pf_dist > 0 && tw == 0) tw = gtimer();
+          if (pf_ok && j < i + p.pf_dist && gtimer() - tw > 1500) {
             if (j >= i) tma_prefetch_3d(wm[pf.k], (pf.x % p.nkb[pf.k]) * 64, (pf.x / p.nkb[pf.k]) * 128, pf.l);
             pf_ok = ds_it_next(p, pf);
             ++j;

@@ -951,6 +951,12 @@ hs_status gemm(const GemmArgs& a, cudaStream_t st) {
     {
       const long long c128 = cdiv((long long)mt * cdiv(a.N, 128), G) * 128;
       const long long c256 = cdiv((long long)mt * cdiv(a.N, 256), G) * 256;
+      static int force = [] {
+        const char* e = getenv("HS_TP_BN");
+        return e ? atoi(e) : 0;
+      }();
+      if (force == 256) return launch_tp<256>(a, st);
+      if (force == 128) return launch_tp<128>(a, st);
       return c256 < c128 ? launch_tp<256>(a, st) : launch_tp<128>(a, st);
     }
   }
