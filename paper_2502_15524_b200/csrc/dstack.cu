@@ -438,9 +438,6 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
     const int np = sk_owner((long long)(t + 1) * nkb - 1, W, Gk) - first + 1;
     const int part = blockIdx.x - first;
     float* tws = p.ws[k] + (size_t)t * p.maxp[k] * BN * 128;
-    // early look at the tile's arrival counter (overlaps the drain): if every other part has
-    // already arrived this CTA is the last one and needs no atomic round trip
-    const unsigned pre = (et == 0 && np > 1) ? ld_acquire(&p.c_tile[k][t]) : 0u;
     {
       float* dst = tws + (size_t)part * BN * 128 + ml;
       const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + buf * BN;
@@ -463,11 +460,8 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
     cur += kb_hi - kb_lo;
     named_bar(1, 128);
     if (et == 0) {
-      int last;
-      if (pre == (unsigned)(np - 1)) {  // the others' partials were released before (acquired above)
-        last = 1;
-        if (np > 1) p.c_tile[k][t] = 0;
-      } else {
+      int last = 1;
+      if (np > 1) {  // a tile held by one CTA needs no arrival
         const unsigned old = atom_add_acq_rel(&p.c_tile[k][t], 1u);
         last = old == (unsigned)(np - 1);
         if (last) p.c_tile[k][t] = 0;
