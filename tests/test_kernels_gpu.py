@@ -226,3 +226,17 @@ def test_embed_and_span_copy_bit_exact():
     torch.cuda.synchronize()
     A, B = a.cpu().numpy().reshape(40, span), b.cpu().numpy().reshape(40, span)
     assert np.array_equal(B[:25], A[perm]) and not B[25:].any()
+
+
+def test_tmem_a_operand_probe():
+    """tcgen05.cp (smem -> TMEM) + tcgen05.mma with A from TMEM equals the shared-memory A path
+    bit for bit, and both equal the fp32 reference (the A-in-TMEM staging of the decode stack's
+    deep weight ring)."""
+    torch.manual_seed(0)
+    K = 256
+    A = (torch.randn(128, K, device="cuda") * 0.1).to(torch.bfloat16)
+    B = torch.randn(16, K, device="cuda").to(torch.bfloat16)
+    ss, ts = hs.tmem_a_gemm(A, B)
+    ref = (B.float() @ A.float().t())
+    assert torch.allclose(ss, ref, rtol=1e-4, atol=1e-4), (ss - ref).abs().max()
+    assert torch.equal(ss, ts), (ss - ts).abs().max()
