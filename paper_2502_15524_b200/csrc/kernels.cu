@@ -240,11 +240,12 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(
   PDL_WAIT();
   constexpr int CH = D / 8;  // 16-byte chunks per row
   constexpr int KS = D / 16; // k-steps over head_dim
-  __shared__ __align__(128) uint4 Ks[PF_KC * CH];
-  __shared__ __align__(128) uint4 Vs[PF_KC * CH];
+  // double-buffered K / V chunks (dynamic smem): chunk t+1 streams in (cp.async) while chunk t
+  // is multiplied
+  extern __shared__ __align__(128) uint4 kv_smem[];
   const SeqDesc s = seqs[blockIdx.z];
   const int head = blockIdx.y;
-  const int qt0 = blockIdx.x * PF_Q;
+  const int qt0 = (gridDim.x - 1 - blockIdx.x) * PF_Q;  // longest (causal) query tiles first
   if (qt0 >= s.n_q) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tig = lane & 3;
@@ -270,32 +271,51 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(
   float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
   const int n_keys = s.pos0 + min(qt0 + PF_Q, s.n_q);
   const int* tab = tables + (size_t)s.table * max_blocks;
-  const uint32_t ks_base = static_cast<uint32_t>(__cvta_generic_to_shared(Ks));
-  const uint32_t vs_base = static_cast<uint32_t>(__cvta_generic_to_shared(Vs));
   const int warp_max_pos = s.pos0 + min(qt0 + warp * 16 + 15, s.n_q - 1);
-  for (int kc = 0; kc < n_keys; kc += PF_KC) {
-    __syncthreads();
+  // gather K, V rows (D * 2 bytes each) of chunk kc into buffer bb, swizzled: 16-byte chunk c
+  // of row r at c ^ (r & 7); rows past the keys are zero-filled (cp.async src-size 0)
+  auto issue = [&](int bb, int kc) {
+    uint4* Kd = kv_smem + (size_t)bb * 2 * PF_KC * CH;
+    uint4* Vd = Kd + PF_KC * CH;
     const int nk = min(PF_KC, n_keys - kc);
-    // gather K, V rows (256 B / 128 B each) into swizzled smem: chunk c of row r at c ^ (r & 7)
     for (int idx = threadIdx.x; idx < PF_KC * CH; idx += 128) {
       const int r = idx / CH, c = idx % CH;
-      uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
+      const bf16* ks = pool;
+      int bytes = 0;
       if (r < nk) {
         const int j = kc + r;
         const int b = tab[j >> 4];
         if (b >= 0 && b < nblocks) {
-          const size_t base = ((((size_t)b * 2) * nh + head) * 16 + (j & 15)) * D;
-          kv = reinterpret_cast<const uint4*>(pool + base)[c];
-          vv = reinterpret_cast<const uint4*>(pool + base + (size_t)nh * 16 * D)[c];
+          ks = pool + ((((size_t)b * 2) * nh + head) * 16 + (j & 15)) * D + c * 8;
+          bytes = 16;
         } else if (c == 0) {
           flag_bad(4u);
         }
       }
-      Ks[r * CH + (c ^ (r & 7))] = kv;
-      Vs[r * CH + (c ^ (r & 7))] = vv;
+      const uint32_t dk = static_cast<uint32_t>(__cvta_generic_to_shared(Kd + r * CH + (c ^ (r & 7))));
+      const uint32_t dv = static_cast<uint32_t>(__cvta_generic_to_shared(Vd + r * CH + (c ^ (r & 7))));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dk), "l"(ks), "r"(bytes) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dv), "l"(ks + (size_t)nh * 16 * D), "r"(bytes)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  issue(0, 0);
+  for (int kc = 0, it = 0; kc < n_keys; kc += PF_KC, ++it) {
+    const int nk = min(PF_KC, n_keys - kc);
+    if (kc + PF_KC < n_keys) {
+      issue((it + 1) & 1, kc + PF_KC);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
-    if (kc > warp_max_pos) continue;  // whole chunk in this warp's causal future
+    const uint32_t ks_base = static_cast<uint32_t>(__cvta_generic_to_shared(kv_smem + (size_t)(it & 1) * 2 * PF_KC * CH));
+    const uint32_t vs_base = ks_base + PF_KC * CH * 16;
+    if (kc > warp_max_pos) {  // whole chunk in this warp's causal future
+      __syncthreads();
+      continue;
+    }
     // S = Q K^T : 16 x 64 per warp (8 n-tiles of 8 keys)
     float sc[8][4];
 #pragma unroll
@@ -375,6 +395,7 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(
         mma_bf16_16816(acc[dd + 1], pl[kk], b2, b3);
       }
     }
+    __syncthreads();  // buffer (it & 1) is refilled by the next iteration's issue
   }
   // finalize: quad-reduce the row sums, normalise, store bf16
   l_a += __shfl_xor_sync(0xffffffffu, l_a, 1);
@@ -398,8 +419,17 @@ void launch_attn_prefill(const bf16* q, const bf16* pool, const SeqDesc* seqs, i
                          const int* tables, int max_blocks, bf16* o, int nh, int d, int nblocks, cudaStream_t st) {
   count_launch();
   dim3 grid((max_nq + PF_Q - 1) / PF_Q, nh, n_seqs);
-  if (d == 128) launchk(attn_prefill_kernel<128>, grid, 128, 0, st, q, pool, seqs, tables, max_blocks, o, nh, nblocks);
-  else launchk(attn_prefill_kernel<64>, grid, 128, 0, st, q, pool, seqs, tables, max_blocks, o, nh, nblocks);
+  const size_t smem = (size_t)2 * 2 * PF_KC * d * 2;  // 2 buffers x (K, V) x 64 rows x d bf16
+  static bool attr[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !attr[dev]) {
+    cudaFuncSetAttribute(attn_prefill_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 2 * PF_KC * 128 * 2);
+    cudaFuncSetAttribute(attn_prefill_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 2 * PF_KC * 64 * 2);
+    attr[dev] = true;
+  }
+  if (d == 128) launchk(attn_prefill_kernel<128>, grid, 128, smem, st, q, pool, seqs, tables, max_blocks, o, nh, nblocks);
+  else launchk(attn_prefill_kernel<64>, grid, 128, smem, st, q, pool, seqs, tables, max_blocks, o, nh, nblocks);
 }
 
 // Decode (one query per sequence), latency-oriented: CTA = (head, seq, split), 16 warps; warp
