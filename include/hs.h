@@ -248,8 +248,10 @@ hs_status hs_prefill(hs_group* g, int32_t n_seqs, const int64_t* seq_ids,
 
 /* One greedy decode step for n_seqs live sequences: in_tokens[i] is appended at position
  * ctx_i (in_tokens == NULL => the tokens produced by the previous prefill/decode call for
- * the same seq_ids, fed back on the device).  Errors as hs_prefill; HS_E_INVAL for a
- * sequence never prefilled. */
+ * the same seq_ids, fed back on the device).  Each stage runs all its layers in one
+ * persistent kernel launch (the decode stack, n_seqs <= 64; HS_DSTACK=0 or larger batches:
+ * five kernels per layer), then hands off / samples.  Errors as hs_prefill; HS_E_INVAL for
+ * a sequence never prefilled. */
 hs_status hs_decode_step(hs_group* g, int32_t n_seqs, const int64_t* seq_ids,
                          const int32_t* in_tokens, int32_t* out_tokens, float* out_logits);
 

@@ -132,7 +132,7 @@ struct DsCfg {
   static constexpr int SMEM = STAGES * STAGE_BYTES + VALS_BYTES + ROPE_BYTES + ATT_BYTES + 1024 + MISC;
 };
 
-__device__ __constant__ unsigned p_backoff_ns = 128;
+__device__ __constant__ unsigned p_backoff_ns = 256;
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
@@ -972,7 +972,7 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
     static bool bo_set[64] = {};
     if (s->device < 64 && !bo_set[s->device]) {
       const char* e = getenv("HS_DSTACK_BACKOFF");
-      const unsigned ns = e ? (unsigned)atoi(e) : 128u;
+      const unsigned ns = e ? (unsigned)atoi(e) : 256u;
       HS_CUDA(cudaMemcpyToSymbol(p_backoff_ns, &ns, sizeof(ns)));
       bo_set[s->device] = true;
     }

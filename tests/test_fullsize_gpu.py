@@ -96,3 +96,23 @@ def test_7b_logits_vs_oracle_sampled(image):
     print("7B max|dlogit| per step", errs, "floor", floor, "tol", tol)
     assert max(errs) <= tol, (errs, floor)
     g.destroy()
+
+
+def test_7b_pp8_equals_pp1_then_consolidates(image):
+    """PP = 8 (the scaling run's largest degree; 4 layers per stage, 8 stages on one GPU here):
+    prefill and decode bitwise equal to PP = 1, consolidation into stage 0, decode continues
+    bitwise equal."""
+    prompt = hsgen.prompts(1, 512, CFG["vocab"])
+    g1, g8 = group(image, 1), group(image, 8)
+    t1, l1 = g1.prefill([0], prompt, want_logits=True)
+    t8, l8 = g8.prefill([0], prompt, want_logits=True)
+    assert np.array_equal(t1, t8) and np.array_equal(l1, l8)
+    for _ in range(4):
+        a, b = g1.decode_step([0], want_logits=True), g8.decode_step([0], want_logits=True)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    g8.consolidate(0)
+    for _ in range(2):
+        a, b = g1.decode_step([0], want_logits=True), g8.decode_step([0], want_logits=True)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    g1.destroy()
+    g8.destroy()
