@@ -681,12 +681,8 @@ __global__ void __launch_bounds__(192, 1)
               if (j < ncol) o[(size_t)j * p.ldo + m] = __float2bfloat16_rn(v[j] + rv[j]);
           } else {
             bf16* o = reinterpret_cast<bf16*>(p.out) + (size_t)(n0 + c0) * p.ldo;
-            const int f = (m0 + quad * 32) / 2 + lane;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float u = __shfl_xor_sync(0xffffffffu, v[j], 16);
-              if (lane < 16 && j < ncol) o[(size_t)j * p.ldo + f] = __float2bfloat16_rn(silu_f(v[j]) * u);
-            }
+            const int f = (m0 + quad * 32) / 2 + (lane & 15);
+            silu_mul_store32(v, lane, o + f, (size_t)p.ldo, ncol);
           }
         }
       }
@@ -779,6 +775,7 @@ bool pdl_enabled() {
 }
 
 static const int kBN[] = {16, 32, 64, 128, 256};
+static constexpr double kTp2Rate128 = 0.9, kTp2Rate256 = 1.6;  // per-SM rate vs gemm_tp_kernel<128> (measured r01)
 int gemm_bn_count() { return 5; }
 int gemm_bn_value(int i) { return kBN[i]; }
 int gemm_bn(int N) {
@@ -927,6 +924,222 @@ static hs_status launch_tp(const GemmArgs& a, cudaStream_t st) {
   return HS_OK;
 }
 
+// ------------------------------------------------------------------ 2-SM persistent (prefill)
+// CTA pair (cluster of 2, tcgen05 cta_group::2): a 256 x 256 output tile per pair, M = 256 rows
+// of weights (128 per CTA) x N = 256 tokens (128 per CTA's shared memory); the leader CTA issues
+// the MMAs, both CTAs' TMA loads complete on the leader's barrier, the MMA commits multicast
+// to both CTAs' "empty" / "accumulator full" barriers, and each CTA drains its own 128 TMEM lanes
+// (rows) x 256 columns.  Per SM a k-block moves 32 KB for 4.2 MFLOP (2x the single-CTA 128 x 256
+// tile): prefill GEMMs are bound by how fast an SM ingests operands, not by the tensor pipe.
+template <int BN>
+struct Tp2Cfg {
+  static constexpr int A_BYTES = 128 * 64 * 2;
+  static constexpr int B_BYTES = (BN / 2) * 64 * 2;  // this CTA's half of the BN-token tile
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = BN >= 256 ? 6 : 8;
+  static constexpr int TMEM_COLS = 2 * BN;           // two BN-column accumulators
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int BN>
+__global__ void __launch_bounds__(192, 1)
+    gemm_tp2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TpParams p) {
+  using C = Tp2Cfg<BN>;
+  PDL_LAUNCH();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int tiles = p.m_tiles * p.n_tiles;  // m_tiles counts 256-row pairs here
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 8); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"((uint32_t)C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();  // both CTAs' barriers initialised before any remote arrive / TMA
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer (both CTAs): this CTA's 128 weight rows and 128 tokens
+      PDL_WAIT();
+      int i = 0;
+      for (int t = cid; t < tiles; t += ncl) {
+        const int m0 = (t / p.n_tiles) * 256 + (int)rank * 128, n0 = (t % p.n_tiles) * BN + (int)rank * (BN / 2);
+        for (int kb = 0; kb < p.nkb; ++kb, ++i) {
+          const int s = i % C::STAGES;
+          mbar_wait(&empty[s], ((i / C::STAGES) & 1) ^ 1);
+          uint8_t* sa = smem + s * C::STAGE_BYTES;
+          // bytes complete on the leader's barrier (peer bit cleared); the leader arms it for both
+          const uint32_t bar = smem_u32(&full[s]) & 0xFEFFFFFFu;
+          if (leader) mbar_expect_tx(&full[s], 2 * C::STAGE_BYTES);
+          asm volatile(
+              "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(sa)),
+              "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(bar), "r"(kb * 64), "r"(m0)
+              : "memory");
+          asm volatile(
+              "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(sa + C::A_BYTES)),
+              "l"(reinterpret_cast<uint64_t>(&tmB)), "r"(bar), "r"(kb * 64), "r"(n0)
+              : "memory");
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // MMA issuer (leader only): M = 256 across the pair, N = 256
+      constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                 ((uint32_t)(256 >> 4) << 24);
+      int i = 0, lt = 0;
+      for (int t = cid; t < tiles; t += ncl, ++lt) {
+        const int buf = lt & 1;
+        mbar_wait(&tempty[buf], ((lt >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + buf * BN;
+        for (int kb = 0; kb < p.nkb; ++kb, ++i) {
+          const int s = i % C::STAGES;
+          mbar_wait(&full[s], (i / C::STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint8_t* sa = smem + s * C::STAGE_BYTES;
+          const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + C::A_BYTES);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
+            asm volatile(
+                "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, q;\n\t}" ::"r"(acc),
+                "l"(da + 2 * k), "l"(db + 2 * k), "r"(idesc), "r"(accum));
+          }
+          asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                       ::"r"(smem_u32(&empty[s])), "h"((uint16_t)3) : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                     ::"r"(smem_u32(&tfull[buf])), "h"((uint16_t)3) : "memory");
+      }
+    }
+  } else {
+    PDL_WAIT();
+    const int quad = warp & 3;
+    int lt = 0;
+    for (int t = cid; t < tiles; t += ncl, ++lt) {
+      const int buf = lt & 1;
+      const int m0 = (t / p.n_tiles) * 256 + (int)rank * 128, n0 = (t % p.n_tiles) * BN;
+      mbar_wait(&tfull[buf], (lt >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int m = m0 + quad * 32 + lane;
+      const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16) + buf * BN;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(trow + c0, v);
+        if (n0 + c0 < p.N) {
+          const int ncol = min(32, p.N - n0 - c0);
+          if (p.epi == EPI_F32) {
+            float* o = reinterpret_cast<float*>(p.out) + (size_t)(n0 + c0) * p.ldo;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < ncol) o[(size_t)j * p.ldo + m] = v[j];
+          } else if (p.epi == EPI_BF16) {
+            bf16* o = reinterpret_cast<bf16*>(p.out) + (size_t)(n0 + c0) * p.ldo;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < ncol) o[(size_t)j * p.ldo + m] = __float2bfloat16_rn(v[j]);
+          } else if (p.epi == EPI_RESID) {
+            bf16* o = reinterpret_cast<bf16*>(p.out) + (size_t)(n0 + c0) * p.ldo;
+            const bf16* r = p.resid + (size_t)(n0 + c0) * p.ldr;
+            float rv[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) rv[j] = j < ncol ? __bfloat162float(__ldg(r + (size_t)j * p.ldr + m)) : 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < ncol) o[(size_t)j * p.ldo + m] = __float2bfloat16_rn(v[j] + rv[j]);
+          } else {
+            bf16* o = reinterpret_cast<bf16*>(p.out) + (size_t)(n0 + c0) * p.ldo;
+            const int f = (m0 + quad * 32) / 2 + (lane & 15);
+            silu_mul_store32(v, lane, o + f, (size_t)p.ldo, ncol);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      // release the accumulator on the leader's barrier (both CTAs' 4 epilogue warps)
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf]) & 0xFEFFFFFFu)
+                     : "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)C::TMEM_COLS));
+}
+
+template <int BN>
+static hs_status launch_tp2(const GemmArgs& a, cudaStream_t st) {
+  using C = Tp2Cfg<BN>;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static bool attr_set[64] = {};
+  if (dev < 64 && !attr_set[dev]) {
+    HS_CUDA(cudaFuncSetAttribute(gemm_tp2_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set[dev] = true;
+  }
+  int bi = 0;
+  while (kBN[bi] != BN / 2) ++bi;
+  if (a.B[bi].box_rows != BN / 2) HS_FAIL(HS_E_INVAL, "TMA box mismatch");
+  TpParams p{};
+  p.M = a.M; p.N = a.N; p.nkb = a.K / 64; p.m_tiles = a.M / 256; p.n_tiles = (int)cdiv(a.N, BN);
+  p.epi = a.epi; p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr;
+  const int tiles = p.m_tiles * p.n_tiles;
+  const int pairs = std::min(tiles, num_sms(dev) / 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  int na = 1;
+  if (pdl_enabled()) {
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    na = 2;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  HS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tp2_kernel<BN>, a.A->map, a.B[bi].map, p));
+  count_launch();
+  return HS_OK;
+}
+
 void launch_rownorm_decode(const bf16* x, const bf16* w, bf16* y, int T, int H, float eps, cudaStream_t st) {
   launchk(rownorm_kernel, T, 128, 0, st, x, w, y, H, eps);
   count_launch();
@@ -957,6 +1170,21 @@ hs_status gemm(const GemmArgs& a, cudaStream_t st) {
       }();
       if (force == 256) return launch_tp<256>(a, st);
       if (force == 128) return launch_tp<128>(a, st);
+      static int tp2 = [] {
+        const char* e = getenv("HS_TP2");
+        return (e && e[0] == '0') ? 0 : 1;
+      }();
+      if (tp2 && a.M % 256 == 0 && force != 1) {
+        // cost = waves x 128x128 tile-equivalents per SM / relative per-SM rate (measured:
+        // the CTA pair halves each SM's operand bytes per flop); min over the three kernels
+        const double w128 = (double)cdiv((long long)mt * cdiv(a.N, 128), G);
+        const double c2_128 = (double)cdiv((long long)(a.M / 256) * cdiv(a.N, 128), G / 2) / kTp2Rate128;
+        const double c2_256 = (double)cdiv((long long)(a.M / 256) * cdiv(a.N, 256), G / 2) * 2.0 / kTp2Rate256;
+        if (force == 2128) return launch_tp2<128>(a, st);
+        if (force == 2256) return launch_tp2<256>(a, st);
+        if (c2_128 < w128 && c2_128 <= c2_256) return launch_tp2<128>(a, st);
+        if (c2_256 < w128) return launch_tp2<256>(a, st);
+      }
       return c256 < c128 ? launch_tp<256>(a, st) : launch_tp<128>(a, st);
     }
   }

@@ -115,6 +115,21 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
 
+// SiLU(gate) * up for 32 token columns held by a warp (lanes 0-15: gate rows, lanes 16-31: the
+// matching up rows): lane l < 16 produces columns 0-15 and lane l + 16 columns 16-31 of the
+// same output feature, so each lane evaluates 16 SiLUs instead of 32.  o = &out[col 0][feature].
+__device__ __forceinline__ void silu_mul_store32(const float* v, int lane, __nv_bfloat16* o, size_t ldo, int ncol) {
+  const bool hi = lane >= 16;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const float other = __shfl_xor_sync(0xffffffffu, hi ? v[q] : v[16 + q], 16);
+    const float g = hi ? other : v[q];
+    const float u = hi ? v[16 + q] : other;
+    const int j = hi ? 16 + q : q;
+    if (j < ncol) o[(size_t)j * ldo] = __float2bfloat16_rn(silu_f(g) * u);
+  }
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
