@@ -546,6 +546,8 @@ struct TpParams {
   int ldo;
   const bf16* resid;
   int ldr;
+  int splits = 1, kbps = 0;  // split-K (tp2 only): work item = tile * splits + split
+  float* ws = nullptr;       // fp32 partials [split][N][M] when splits > 1
 };
 
 template <int BN>
@@ -967,7 +969,7 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-  const int tiles = p.m_tiles * p.n_tiles;  // m_tiles counts 256-row pairs here
+  const int tiles = p.m_tiles * p.n_tiles * p.splits;  // work items; m_tiles counts 256-row pairs
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -989,9 +991,11 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {  // producer (both CTAs): this CTA's 128 weight rows and 128 tokens
       PDL_WAIT();
       int i = 0;
-      for (int t = cid; t < tiles; t += ncl) {
+      for (int w = cid; w < tiles; w += ncl) {
+        const int t = w / p.splits, sp = w % p.splits;
+        const int kb0 = sp * p.kbps, kb1 = min(p.nkb, kb0 + p.kbps);
         const int m0 = (t / p.n_tiles) * 256 + (int)rank * 128, n0 = (t % p.n_tiles) * BN + (int)rank * (BN / 2);
-        for (int kb = 0; kb < p.nkb; ++kb, ++i) {
+        for (int kb = kb0; kb < kb1; ++kb, ++i) {
           const int s = i % C::STAGES;
           mbar_wait(&empty[s], ((i / C::STAGES) & 1) ^ 1);
           uint8_t* sa = smem + s * C::STAGE_BYTES;
@@ -1016,12 +1020,14 @@ __global__ void __launch_bounds__(192, 1)
       constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                                  ((uint32_t)(256 >> 4) << 24);
       int i = 0, lt = 0;
-      for (int t = cid; t < tiles; t += ncl, ++lt) {
+      for (int w = cid; w < tiles; w += ncl, ++lt) {
+        const int sp = w % p.splits;
+        const int kb0 = sp * p.kbps, kb1 = min(p.nkb, kb0 + p.kbps);
         const int buf = lt & 1;
         mbar_wait(&tempty[buf], ((lt >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t acc = tmem + buf * BN;
-        for (int kb = 0; kb < p.nkb; ++kb, ++i) {
+        for (int kb = kb0; kb < kb1; ++kb, ++i) {
           const int s = i % C::STAGES;
           mbar_wait(&full[s], (i / C::STAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -1029,7 +1035,7 @@ __global__ void __launch_bounds__(192, 1)
           const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + C::A_BYTES);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
+            const uint32_t accum = (kb > kb0 || k > 0) ? 1u : 0u;
             asm volatile(
                 "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
                 "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, q;\n\t}" ::"r"(acc),
@@ -1046,7 +1052,8 @@ __global__ void __launch_bounds__(192, 1)
     PDL_WAIT();
     const int quad = warp & 3;
     int lt = 0;
-    for (int t = cid; t < tiles; t += ncl, ++lt) {
+    for (int w = cid; w < tiles; w += ncl, ++lt) {
+      const int t = w / p.splits, sp = w % p.splits;
       const int buf = lt & 1;
       const int m0 = (t / p.n_tiles) * 256 + (int)rank * 128, n0 = (t % p.n_tiles) * BN;
       mbar_wait(&tfull[buf], (lt >> 1) & 1);
@@ -1059,7 +1066,12 @@ __global__ void __launch_bounds__(192, 1)
         tmem_ld32(trow + c0, v);
         if (n0 + c0 < p.N) {
           const int ncol = min(32, p.N - n0 - c0);
-          if (p.epi == EPI_F32) {
+          if (p.splits > 1) {  // fp32 partial of this split (reduced by splitk_reduce_kernel)
+            float* o = p.ws + ((size_t)sp * p.N + n0 + c0) * p.M;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < ncol) o[(size_t)j * p.M + m] = v[j];
+          } else if (p.epi == EPI_F32) {
             float* o = reinterpret_cast<float*>(p.out) + (size_t)(n0 + c0) * p.ldo;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
@@ -1100,7 +1112,7 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 template <int BN>
-static hs_status launch_tp2(const GemmArgs& a, cudaStream_t st) {
+static hs_status launch_tp2(const GemmArgs& a, cudaStream_t st, int splits = 1) {
   using C = Tp2Cfg<BN>;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1115,7 +1127,12 @@ static hs_status launch_tp2(const GemmArgs& a, cudaStream_t st) {
   TpParams p{};
   p.M = a.M; p.N = a.N; p.nkb = a.K / 64; p.m_tiles = a.M / 256; p.n_tiles = (int)cdiv(a.N, BN);
   p.epi = a.epi; p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr;
-  const int tiles = p.m_tiles * p.n_tiles;
+  p.kbps = (int)cdiv(p.nkb, splits);
+  p.splits = (int)cdiv(p.nkb, p.kbps);
+  p.ws = a.workspace;
+  if (p.splits > 1 && (!a.workspace || (uint64_t)p.splits * a.N * a.M * 4 > a.workspace_bytes))
+    HS_FAIL(HS_E_INVAL, "split-K workspace too small");
+  const int tiles = p.m_tiles * p.n_tiles * p.splits;
   const int pairs = std::min(tiles, num_sms(dev) / 2);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs);
@@ -1137,6 +1154,13 @@ static hs_status launch_tp2(const GemmArgs& a, cudaStream_t st) {
   cfg.numAttrs = na;
   HS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tp2_kernel<BN>, a.A->map, a.B[bi].map, p));
   count_launch();
+  if (p.splits > 1) {
+    dim3 g2(cdiv(a.M, 256), a.N);
+    launchk(splitk_reduce_kernel, g2, 256, 0, st, (const float*)a.workspace, p.splits, a.M, a.N, a.epi, a.out, a.ldo,
+            a.resid, a.ldr);
+    count_launch();
+    HS_CUDA(cudaGetLastError());
+  }
   return HS_OK;
 }
 
@@ -1182,8 +1206,20 @@ hs_status gemm(const GemmArgs& a, cudaStream_t st) {
         const double c2_256 = (double)cdiv((long long)(a.M / 256) * cdiv(a.N, 256), G / 2) * 2.0 / kTp2Rate256;
         if (force == 2128) return launch_tp2<128>(a, st);
         if (force == 2256) return launch_tp2<256>(a, st);
-        if (c2_128 < w128 && c2_128 <= c2_256) return launch_tp2<128>(a, st);
-        if (c2_256 < w128) return launch_tp2<256>(a, st);
+        // few pair tiles (M = 4096): split K over the pairs, fp32 partials + one reduction pass
+        int best_s = 1;
+        double best = c2_256;
+        const long long pairs256 = (long long)(a.M / 256) * cdiv(a.N, 256);
+        // only when the pairs fill less than half the clusters and K is long (down-proj): the
+        // reduction's traffic (S x N x M x 4 B) outweighs the gain otherwise (measured)
+        for (int sk = 2; sk <= 4 && pairs256 * 2 <= G / 2 && a.K / 64 >= 128; ++sk) {
+          if (!a.workspace || (uint64_t)sk * a.N * a.M * 4 > a.workspace_bytes) break;
+          const double c = (double)cdiv(pairs256 * sk, G / 2) * 2.0 / kTp2Rate256 / sk + 0.1 * sk;
+          if (c < best) { best = c; best_s = sk; }
+        }
+        if (force >= 22560 && force <= 22564) return launch_tp2<256>(a, st, force - 22560);
+        if (c2_128 < w128 && c2_128 <= best) return launch_tp2<128>(a, st);
+        if (best < w128) return launch_tp2<256>(a, st, best_s);
       }
       return c256 < c128 ? launch_tp<256>(a, st) : launch_tp<128>(a, st);
     }
