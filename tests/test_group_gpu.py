@@ -303,11 +303,11 @@ def test_scale_up_every_stage_becomes_an_endpoint(image, oracle_run):
     g1.destroy()
 
 
-@pytest.mark.parametrize("n_seqs,long_ctx", [(1, 1000), (12, 0), (40, 0), (70, 0)])
+@pytest.mark.parametrize("n_seqs,long_ctx", [(1, 1000), (12, 0), (24, 0), (40, 0), (70, 0)])
 def test_decode_stack_batches_and_long_context(image, oracle_run, n_seqs, long_ctx):
     """The decode-stack kernel (every layer of the stage in one launch) against the oracle,
     teacher-forced: one sequence whose context crosses several attention splits (merged in
-    split order), a 12-sequence batch (tile width 16) and a 40-sequence batch (tile width 64),
+    split order), 12-, 24- and 40-sequence batches (tile widths 16, 32, 64),
     varied prompt lengths; PP = 2 on one GPU so the stage boundary is crossed too.  70 sequences
     exceed the decode stack's 64-token tile: the per-kernel decode path runs instead."""
     W = Weights(CFG)
