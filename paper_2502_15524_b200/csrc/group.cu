@@ -751,6 +751,7 @@ struct Chunk {
 static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int64_t>& ids,
                           const std::vector<int>& host_tokens, bool feedback, int32_t* out_tokens,
                           float* out_logits) {
+  const auto t_call = std::chrono::steady_clock::now();
   const hs_model_cfg& c = g->cfg;
   const int first = g->active.front(), last = g->active.back();
   // ---- chunking of prefill: depends on the shapes only (never on the number of stages), so
@@ -957,6 +958,7 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
     s.called = true;
   }
   // wait for the result on the stage(s) this process owns
+  const auto t_enq = std::chrono::steady_clock::now();
   const int n = m0.n;
   int err = 0;
   bool got = false;
@@ -989,6 +991,13 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
     }
   }
   g->last_ids = ids;
+  static const bool dbg = getenv("HS_DEBUG_CALL") != nullptr;
+  if (dbg) {
+    const auto t_end = std::chrono::steady_clock::now();
+    fprintf(stderr, "[hs] call stage %d: enqueue %.1f us, wait %.1f us\n", g->owned_stage,
+            1e6 * std::chrono::duration<double>(t_enq - t_call).count(),
+            1e6 * std::chrono::duration<double>(t_end - t_enq).count());
+  }
   return HS_OK;
 }
 
