@@ -282,6 +282,14 @@ __device__ __forceinline__ void ds_attn_unit(const DsParams& p, int l, unsigned 
     if (bi >= 32) blk = tab[b];
     if (blk < 0 || blk >= p.nblocks) blk = 0;
     const bf16* kb = pool + (((size_t)blk * 2 * p.nh + h) * 16) * D + lane * E;
+    if (b + DS_AWARPS < b1 && bi + 1 < 32) {  // the warp's next block into L2 (no registers held)
+      int nblk = __shfl_sync(0xffffffffu, my_blk, bi + 1);
+      if (nblk < 0 || nblk >= p.nblocks) nblk = 0;
+      const char* row = reinterpret_cast<const char*>(pool + (((size_t)nblk * 2 * p.nh + h) * 16 + (lane & 15)) * D +
+                                                      (lane >= 16 ? vstride : 0));
+#pragma unroll
+      for (int ln = 0; ln < D * 2; ln += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + ln));
+    }
     VT kr[16], vr[16];
 #pragma unroll
     for (int jj = 0; jj < 16; ++jj) {
