@@ -791,6 +791,15 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
     for (int step = 0; step < 4 * p.nl; ++step) {
       const int l = step >> 2, k = step & 3;
       const unsigned tag = p.tag0 + l;
+      if (k == 0 && t256 < 2) {  // this CTA's column slices of the layer's two norm vectors into L2
+        const bf16* w = t256 == 0 ? p.ffn_norm + (size_t)l * p.norm_stride
+                                  : (l + 1 < p.nl ? p.attn_norm + (size_t)(l + 1) * p.norm_stride : p.final_norm);
+        if (w) {
+          const int n8 = p.H >> 3;
+          const int c0 = (int)((long long)blockIdx.x * n8 / p.G), c1 = (int)((long long)(blockIdx.x + 1) * n8 / p.G);
+          for (int c = c0 & ~7; c < c1; c += 8) asm volatile("prefetch.global.L2 [%0];" ::"l"(w + (size_t)c * 8));
+        }
+      }
       if (epi) seg = ds_segments<BN, NC>(p, k, l, tag, seg, tmem, tfull, tempty, vals, flag, t256, lane, quad,
                                      s_pos, s_slot, s_rope);
       if (t256 == 0) DS_TR(TR_E_QKV + (k == 0 ? 0 : k == 1 ? 2 : k == 2 ? 4 : 5));
