@@ -13,10 +13,12 @@
 //                    the last CTA to finish a tile sums the parts in part order (deterministic)
 //                    and applies the fused epilogue (RoPE + paged KV write | residual | SiLU*up),
 //                    then publishes the tile's flag.
-//   warps 4-11     : decode attention (one warp per (sequence, head, KV chunk) item) and the
-//                    row RMSNorms (done by the CTA that completes the last O / down tile).
-// Flags carry tags (launch number << 8 | layer + 1) and are compared wrap-safe, so nothing is
-// reset between steps; arrival counters are reset by their last arriver.
+//   warps 4-11     : decode attention (units of (sequence, head, KV split) per CTA, one
+//                    16-token block per warp at a time, next block prefetched into L2) and
+//                    every CTA's column slice of each row RMSNorm.
+// Flags carry tags (launch number << 8 | layer + 1) and are compared wrap-safe, the row and
+// norm counters are cumulative with per-launch bases, so nothing is reset between steps;
+// per-tile arrival counters are reset by their last arriver.
 //
 // Numerics follow the per-kernel path: fp32 accumulation in TMEM, partial sums
 // added in part order, bf16 rounding at the same points (q/k/v, RoPE outputs, attention output,
@@ -55,7 +57,6 @@ struct DsParams {
   const SeqDesc* seqs;
   const float2* rope;
   int ch;
-  int pf_dist;  // weight k-blocks prefetched into L2 ahead of the ring
   float* ws_attn;
   unsigned *c_tile[4], *c_ih, *c_h, *f_qkv, *f_attn, *f_gu;
   // distributed row norms: residual tiles publish sum-of-squares partials ssq[tile][64] and
@@ -615,40 +616,17 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---- weight producer (independent of every earlier kernel and flag)
-      // While the ring is full (the MMA waits for activations) the producer keeps HBM busy by
-      // prefetching the next items into L2, up to pf_dist items ahead of the ring.
       const CUtensorMap* wm[4] = {&tw0, &tw1, &tw2, &tw3};
-      DsIt ld, pf;
-      bool ld_ok = ds_it_begin(p, ld), pf_ok = ld_ok;
-      pf = ld;
-      int i = 0, j = 0;
-      while (ld_ok) {
+      DsIt ld;
+      bool ld_ok = ds_it_begin(p, ld);
+      for (int i = 0; ld_ok; ++i) {
         const int s = i % C::STAGES;
-        const uint32_t par = ((i / C::STAGES) & 1) ^ 1;
-        unsigned long long t0 = 0;
-        unsigned long long tw = 0;  // a dependency stall (not steady streaming): prefetch into L2
-        for (unsigned it = 0; !mbar_test(&empty[s], par); ++it) {
-          if (p.pf_dist > 0 && tw == 0) tw = gtimer();
-          if (pf_ok && j < i + p.pf_dist && gtimer() - tw > 1500) {
-            if (j >= i) tma_prefetch_3d(wm[pf.k], (pf.x % p.nkb[pf.k]) * 64, (pf.x / p.nkb[pf.k]) * 128, pf.l);
-            pf_ok = ds_it_next(p, pf);
-            ++j;
-          } else if ((it & 1023) == 1023) {
-            if (t0 == 0) t0 = gtimer();
-            else if (gtimer() - t0 > 4000000000ull) __trap();
-          }
-        }
-        if (j <= i) {  // keep the prefetch cursor ahead of the load cursor
-          pf = ld;
-          pf_ok = ds_it_next(p, pf);
-          j = i + 1;
-        }
+        mbar_wait(&empty[s], ((i / C::STAGES) & 1) ^ 1);
         const int l = ld.l, k = ld.k, x = ld.x;
         if (x == ld.beg && p.trace) DS_TR(k == 0 ? TR_A0 : TR_A1 + k - 1);
         mbar_expect_tx(&full[s], C::A_BYTES);
         tma_load_3d(wm[k], &full[s], smem + s * C::STAGE_BYTES, (x % p.nkb[k]) * 64, (x / p.nkb[k]) * 128, l);
         ld_ok = ds_it_next(p, ld);
-        ++i;
       }
     }
   } else if (warp == 1) {
@@ -981,11 +959,6 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
   }
   p.ws_attn = s->ws_attn;
   {
-    static int pf = [] {
-      const char* e = getenv("HS_DSTACK_PF");
-      return e ? atoi(e) : 0;  // measured: L2 prefetch ahead of the ring only slows the step (r01)
-    }();
-    p.pf_dist = pf;
     static bool bo_set[64] = {};
     if (s->device < 64 && !bo_set[s->device]) {
       const char* e = getenv("HS_DSTACK_BACKOFF");
