@@ -52,6 +52,8 @@ GEMM_CASES = [  # (M, K, N)
     (768, 256, 300), (256, 768, 1100), (128, 64, 5),
     (2048, 4096, 7), (1536, 2048, 64), (4096, 11008, 3),  # stream-K (decode) path when ws is given
     (4096, 4096, 128), (2048, 1024, 200),                 # prefill chunks: tiled split-K / persistent
+    (12288, 1024, 512), (22016, 1024, 300),               # CTA-pair kernel (256 x 256 tiles, ragged N)
+    (4096, 8192, 512),                                    # CTA pairs with split-K + reduction (ws given)
 ]
 
 
