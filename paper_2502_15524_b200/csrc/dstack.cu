@@ -126,11 +126,12 @@ struct DsCfg {
   static constexpr int VALS_BYTES = 128 * BN * 4;  // tile values for the RoPE pairing
   static constexpr int ROPE_BYTES = BN * 64 * 8;   // cos/sin of the call's positions (head_dim <= 128)
   static constexpr int ATT_BYTES = (2 * 8 + 8 * 128) * 4 + 128;  // attention warp merge
+  static constexpr int XN_BYTES = BN <= 16 ? 10240 : 0;  // single-sequence decode: the normalised row (H <= 5120)
   static constexpr int MISC = 2048;
-  static constexpr int FIT = (232448 - 1024 - MISC - VALS_BYTES - ROPE_BYTES - ATT_BYTES) / STAGE_BYTES;
+  static constexpr int FIT = (232448 - 1024 - MISC - VALS_BYTES - ROPE_BYTES - ATT_BYTES - XN_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = FIT > 12 ? 12 : FIT;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + VALS_BYTES + ROPE_BYTES + ATT_BYTES + 1024 + MISC;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + VALS_BYTES + ROPE_BYTES + ATT_BYTES + XN_BYTES + 1024 + MISC;
 };
 
 __device__ __constant__ unsigned p_backoff_ns = 256;
@@ -584,7 +585,8 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
   float* vals = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES);
   float2* s_rope = reinterpret_cast<float2*>(smem + C::STAGES * C::STAGE_BYTES + C::VALS_BYTES);
   float* s_att = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + C::VALS_BYTES + C::ROPE_BYTES);
-  uint8_t* misc = smem + C::STAGES * C::STAGE_BYTES + C::VALS_BYTES + C::ROPE_BYTES + C::ATT_BYTES;
+  uint4* s_xn = reinterpret_cast<uint4*>(smem + C::STAGES * C::STAGE_BYTES + C::VALS_BYTES + C::ROPE_BYTES + C::ATT_BYTES);
+  uint8_t* misc = smem + C::STAGES * C::STAGE_BYTES + C::VALS_BYTES + C::ROPE_BYTES + C::ATT_BYTES + C::XN_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(misc);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
@@ -676,10 +678,74 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
         int beg, end, Gk;
         ds_range(blockIdx.x, W, G, beg, end, Gk);
         if (beg == end) continue;
-        if (k == 0 || k == 2) {  // the row norm feeding this GEMM: every CTA's slice written
+        if constexpr (NC == 1) {
+          if (k == 0 || k == 2) {
+            // single-sequence decode: this warp normalises the row itself (tile partial sums ->
+            // rs, then bf16(x * rs * w) into shared memory) and writes each k-block's activation
+            // tile straight into its ring slot: no global round trip, no TMA for these phases
+            const int T = p.H / 128, n8 = p.H >> 3;
+            if (lane == 0) wait_tag(p.c_rows, p.base_rows + (unsigned)T * (unsigned)(2 * l + (k == 0 ? 1 : 2)));
+            __syncwarp();
+            if (p.trace && lane == 0) DS_TR(k);
+            const bf16* src = k == 0 ? (l == 0 ? p.x_in : p.x) : p.hbuf;
+            const uint4* x4 = reinterpret_cast<const uint4*>(src);
+            const uint4* w4 = reinterpret_cast<const uint4*>(k == 0 ? p.attn_norm + (size_t)l * p.norm_stride
+                                                                    : p.ffn_norm + (size_t)l * p.norm_stride);
+            float acc = 0.f;
+            for (int tt = lane; tt < T; tt += 32) acc += __ldcg(p.ssq + (size_t)tt * DS_MAXSEQ);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            const float rs = 1.0f / sqrtf(acc / (float)p.H + p.eps);
+            for (int c0 = 0; c0 < n8; c0 += 256) {
+              uint4 xv[8], wv[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const int c = c0 + j * 32 + lane;
+                if (c < n8) { xv[j] = __ldcg(x4 + c); wv[j] = __ldg(w4 + c); }
+              }
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const int c = c0 + j * 32 + lane;
+                if (c < n8) {
+                  uint4 o;
+                  const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&xv[j]);
+                  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&wv[j]);
+                  __nv_bfloat162* rr = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) {
+                    const float2 xa = __bfloat1622float2(a[q]), g = __bfloat1622float2(b[q]);
+                    rr[q] = __floats2bfloat162_rn(xa.x * rs * g.x, xa.y * rs * g.y);
+                  }
+                  s_xn[c] = o;
+                }
+              }
+            }
+            __syncwarp();
+            // token row 0 of each k-block's tile (rows >= N are never drained); 4 k-blocks per
+            // warp pass, 8 lanes (128 bytes) each
+            const int grp = lane >> 3, gl = lane & 7;
+            for (int x0 = beg; x0 < end; x0 += 4, i += 4) {
+              const int x = x0 + grp, ii = i + grp;
+              const bool mine = x < end;
+              const int s = ii % C::STAGES;
+              if (mine && gl == 0) mbar_wait(&empty[s], ((ii / C::STAGES) & 1) ^ 1);
+              __syncwarp();
+              if (mine) {
+                uint4* dst = reinterpret_cast<uint4*>(smem + s * C::STAGE_BYTES + C::A_BYTES);
+                dst[gl] = s_xn[(x % nkb) * 8 + gl];  // row 0: 16-byte chunk c at c ^ 0
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              }
+              __syncwarp();
+              if (mine && gl == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+            }
+            i -= (4 - (end - beg) % 4) % 4;  // the last pass may have covered fewer than 4 k-blocks
+            continue;
+          }
+        } else if (k == 0 || k == 2) {  // the row norm feeding this GEMM: every CTA's slice written
           if (lane == 0) wait_tag(p.c_norm, p.base_norm + (unsigned)(2 * l + (k == 0 ? 1 : 2)) * (unsigned)G);
           __syncwarp();
         }
+
         for (int x0 = beg; x0 < end; x0 += 32) {
           const int cnt = min(32, end - x0);
           const int kbl = (x0 + lane) % nkb;
@@ -762,7 +828,7 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
         if (t256 == 0) red_release_add(p.c_rows, 1u);
       }
       ds_wait_count(p.c_rows, p.base_rows + (unsigned)T, t256);
-      ds_norm_slice(p, p.x_in, p.attn_norm, p.nrm, t256, s_att);
+      ds_norm_slice(p, p.x_in, p.attn_norm, NC == 1 ? nullptr : p.nrm, t256, s_att);  // NC == 1: the B producer normalises
       const int l = 0;
       if (t256 == 0) DS_TR(TR_E_NA);
     }
@@ -797,9 +863,9 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
         ds_wait_count(p.c_rows, p.base_rows + (unsigned)T * (ev + 1), t256);
         if (t256 == 0) DS_TR(k == 1 ? TR_O_LAST : TR_D_LAST);
         if (k == 1)
-          ds_norm_slice(p, p.hbuf, p.ffn_norm + (size_t)l * p.norm_stride, p.nrm, t256, s_att);
+          ds_norm_slice(p, p.hbuf, p.ffn_norm + (size_t)l * p.norm_stride, NC == 1 ? nullptr : p.nrm, t256, s_att);
         else if (l + 1 < p.nl)
-          ds_norm_slice(p, p.x, p.attn_norm + (size_t)(l + 1) * p.norm_stride, p.nrm, t256, s_att);
+          ds_norm_slice(p, p.x, p.attn_norm + (size_t)(l + 1) * p.norm_stride, NC == 1 ? nullptr : p.nrm, t256, s_att);
         else
           ds_norm_slice(p, p.x, p.final_norm, p.final_norm ? p.fin : nullptr, t256, s_att);
         if (t256 == 0) DS_TR(k == 1 ? TR_E_NF : TR_E_NA);
