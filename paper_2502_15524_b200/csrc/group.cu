@@ -764,7 +764,11 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
   if (!m0.decode) {
     int min_len = 1 << 30;
     for (int i = 0; i < m0.n; ++i) min_len = std::min(min_len, g->seqs[ids[i]].ctx);
-    nchunks = std::max(1, std::min<int>({kMaxChunks, min_len / 16, m0.T / kChunkTokens}));
+    static const int chunk_tokens = [] {
+      const char* e = getenv("HS_CHUNK_TOKENS");
+      return e && atoi(e) > 0 ? atoi(e) : kChunkTokens;
+    }();
+    nchunks = std::max(1, std::min<int>({kMaxChunks, min_len / 16, m0.T / chunk_tokens}));
   }
   std::vector<int> dctx;  // decode: keys per sequence after this step (decode-stack item split)
   if (m0.decode)
