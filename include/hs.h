@@ -100,7 +100,10 @@ typedef struct {
 /* A (slice of a) host image: data covers image bytes [data_offset, data_offset+data_bytes).
  * data should be pinned (cudaHostAlloc / cudaHostRegister); pageable memory works but the
  * copy engine then cannot stream it asynchronously.  Caller-owned; must stay valid until
- * every load issued from it has completed (hs_stage_load_stats) or the group is destroyed. */
+ * every load issued from it has completed (hs_stage_load_stats) and every prefill issued
+ * while that load was in flight has returned (a prefill reads its prompt's embedding rows
+ * from a pinned, device-mapped image while the table is still streaming), or until the group
+ * is destroyed. */
 typedef struct {
   const hs_image_header* header;
   const void* data;
@@ -220,8 +223,9 @@ hs_status hs_group_create(const hs_model_cfg* cfg, const hs_plan* plan,
                           const hs_image* image, const hs_image* stage_images,
                           const hs_kv_cfg* kv, const hs_comm* comm, hs_group** out);
 
-/* Issues the chunked H2D load of a stage's slice (critical order: embedding, layers b..e-1
- * in order, final norm + lm_head last) and returns immediately; each layer's readiness
+/* Issues the chunked H2D load of a stage's slice (critical order: layers b..e-1 in order,
+ * final norm + lm_head, then the embedding table, which only decode steps wait for; with an
+ * unmapped image the embedding goes first) and returns immediately; each layer's readiness
  * event is recorded after its last chunk.  chunk_bytes = 0 => 32 MiB.  Calling it again
  * re-loads (used by benchmarks).  In SPMD mode only the owned stage is issued; stage = -1
  * means "every stage this process owns".  Errors: HS_E_INVAL, HS_E_CUDA. */

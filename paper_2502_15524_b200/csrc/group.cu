@@ -106,6 +106,7 @@ struct Stage {
   TmaMat lm;
   TmaMat b_nrm[5], b_o[5], b_act[5], b_fin[5];
   const hs_image* img = nullptr;
+  const bf16* host_embed = nullptr;  // device-accessible (UVA-mapped) embedding table in the host image
   // decode stack (dstack.h): workspace + layered weight maps of the current layer range
   DstackState* ds = nullptr;
   TmaMat ds_w[4];
@@ -503,10 +504,22 @@ static hs_status load_stage(hs_group* g, int k, uint64_t chunk) {
   };
   s.loaded_bytes = 0;
   HS_CUDA(cudaEventRecord(s.ev_l0, s.copy));
-  // critical order: embedding, layers b..e-1, final norm + lm_head (R4)
-  if (s.lb == 0 && k == g->active.front()) HS_TRY(copy_region(h.embed_off, h.embed_bytes, s.ev_embed));
+  // critical order: layers b..e-1, final norm + lm_head, then the embedding table (R4).
+  // The prefill reads its prompt's embedding rows straight from the pinned image (UVA-mapped),
+  // so the 262 MB table (7B) is not on the TTFT path; decode steps wait for it.  Without a
+  // mapped image the table goes first.
+  const bool embed_here = s.lb == 0 && k == g->active.front();
+  s.host_embed = nullptr;
+  if (embed_here && !getenv("HS_EMBED_FIRST")) {
+    void* dp = nullptr;
+    const void* hp = src + (h.embed_off - s.img->data_offset);
+    if (cudaHostGetDevicePointer(&dp, const_cast<void*>(hp), 0) == cudaSuccess) s.host_embed = static_cast<const bf16*>(dp);
+    else cudaGetLastError();
+  }
+  if (embed_here && !s.host_embed) HS_TRY(copy_region(h.embed_off, h.embed_bytes, s.ev_embed));
   for (int l = s.lb; l < s.le; ++l) HS_TRY(copy_region(h.layer_off[l], h.layer_bytes, s.ev_layer[l]));
   if (s.le == c.n_layers) HS_TRY(copy_region(h.final_off, h.final_bytes, s.ev_final));
+  if (embed_here && s.host_embed) HS_TRY(copy_region(h.embed_off, h.embed_bytes, s.ev_embed));
   HS_CUDA(cudaEventRecord(s.ev_l1, s.copy));
   s.load_issued = true;
   return HS_OK;
@@ -862,8 +875,12 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
     // stage input of chunk cidx: embedding (first stage) or the hand-off buffer
     auto stage_input = [&](int cidx) -> hs_status {
       if (is_first) {
-        if (cidx == 0 && s.lb == 0) HS_CUDA(cudaStreamWaitEvent(st, s.ev_embed, 0));
         const bf16* E = reinterpret_cast<const bf16*>(s.wptr(g->hdr.embed_off));
+        // prefill while the table is still streaming: read the prompt's rows from the image
+        const bool from_host = !dec && s.host_embed && cudaEventQuery(s.ev_embed) == cudaErrorNotReady;
+        cudaGetLastError();
+        if (from_host) E = s.host_embed;
+        else if (cidx == 0 && s.lb == 0) HS_CUDA(cudaStreamWaitEvent(st, s.ev_embed, 0));
         const int* d_tok = reinterpret_cast<const int*>(meta_of(cidx) + ch[cidx].m.o_tok);
         if (feedback) {
           ProfScope ps(g, s, PK_WAIT, dec, 0, 0);
