@@ -475,7 +475,8 @@ static hs_status create(const hs_model_cfg* cfg, const hs_plan* plan, const hs_i
     }
     // a full-memory stage (a consolidation target) maps every peer's arena and KV pools now,
     // before T0: opening large IPC allocations costs ~100 ms that must not land in the pause
-    if (me.full_memory)
+    static const bool late_open = getenv("HS_CONS_LATE_OPEN") != nullptr;  // debug: map at consolidation
+    if (me.full_memory && !late_open)
       for (int k = 0; k < pp; ++k)
         if (k != g->owned_stage) HS_TRY(open_peer_memory(g.get(), g->st[k]));
     if (g->comm.barrier(g->comm.ctx) != 0) HS_FAIL(HS_E_STATE, "barrier failed");
@@ -1163,7 +1164,10 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
     //    blocks of every live sequence for those layers, placed at the same block ids ("collect
     //    these blocks from all workers with a gather operation ... placed at different layers,
     //    according to which worker it comes from")
-    const uint64_t piece = 1ull << 20;
+    static const uint64_t piece = [] {
+      const char* e = getenv("HS_CONS_PIECE_KB");
+      return (e && atoi(e) > 0 ? (uint64_t)atoi(e) : 1024ull) << 10;
+    }();
     std::vector<CopyDesc> list;
     auto add = [&](uint64_t src, uint64_t dst, uint64_t bytes) {
       for (uint64_t o = 0; o < bytes; o += piece) list.push_back({src + o, dst + o, std::min(piece, bytes - o)});
@@ -1197,6 +1201,15 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
     if (!list.empty()) {
       HS_CUDA(cudaMalloc(&d_list, list.size() * sizeof(CopyDesc)));
       HS_CUDA(cudaMemcpy(d_list, list.data(), list.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+    }
+    if (getenv("HS_DEBUG_CONS_SYNC")) {
+      cudaError_t pe = cudaDeviceSynchronize();
+      if (pe != cudaSuccess) HS_FAIL(HS_E_CUDA, "consolidate: fault before the copy list: %s", cudaGetErrorString(pe));
+      for (auto& d : list) {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, reinterpret_cast<void*>(d.src)) != cudaSuccess || at.devicePointer == nullptr)
+          HS_FAIL(HS_E_CUDA, "consolidate: unmapped source 0x%llx", (unsigned long long)d.src);
+      }
     }
     HS_CUDA(cudaEventRecord(e0, s2));
     launch_copy_list(d_list, (int)list.size(), 8 * num_sms(T.device), s2);
