@@ -1126,6 +1126,11 @@ static hs_status open_peer_memory(hs_group* g, Stage& s) {
   HS_CUDA(cudaIpcOpenMemHandle(&p, s.share.kv, cudaIpcMemLazyEnablePeerAccess));
   s.kv_mem = reinterpret_cast<uint8_t*>(p);
   s.ipc_arena_open = true;
+  for (void* q : {static_cast<void*>(s.arena), static_cast<void*>(s.kv_mem)}) {  // mapped as device memory
+    cudaPointerAttributes at{};
+    HS_CUDA(cudaPointerGetAttributes(&at, q));
+    if (at.type != cudaMemoryTypeDevice) HS_FAIL(HS_E_CUDA, "peer mapping %p is not device memory", q);
+  }
   return HS_OK;
 }
 

@@ -735,7 +735,9 @@ __global__ void __launch_bounds__(256) copy_list_kernel(const CopyDesc* __restri
 void launch_copy_list(const CopyDesc* d, int n, int ctas, cudaStream_t st) {
   if (n <= 0) return;
   count_launch();
-  launchk(copy_list_kernel, ctas < n ? ctas : n, 256, 0, st, d, n);
+  // plain launch (no programmatic serialisation): a one-off bulk copy has nothing to overlap,
+  // and it reads peer mappings opened by another process
+  copy_list_kernel<<<ctas < n ? ctas : n, 256, 0, st>>>(d, n);
 }
 
 // Small copies between mapped pinned host memory and device memory done by SMs, so they never
