@@ -1,5 +1,5 @@
-"""SPMD mode (one process per GPU, the product's multi-GPU launch): parity of the 2-rank
-pipeline and of its consolidation against the oracle, on BASELINE config 1 (tiny decoder, two
+"""SPMD mode (one process per GPU, the product's multi-GPU launch): parity of the 2- and
+4-rank pipeline and of its consolidation against the oracle, on BASELINE config 1 (tiny decoder, two
 32-token prompts), teacher-forced, with the group created / run / consolidated / destroyed three
 times in a row (repeated CUDA IPC export, mapping and release, as bench.py does per step).
 Same acceptance as tests/test_group_gpu.py: max |logit - oracle| <= TOL on every step, and the
@@ -41,19 +41,21 @@ def oracle_hist():
     return hist, max(2e-2, 1.5 * max(floor))
 
 
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-def test_spmd_two_ranks_pipeline_and_consolidation(oracle_hist, tmp_path):
+@pytest.mark.parametrize("world", [2, 4])
+def test_spmd_pipeline_and_consolidation(oracle_hist, tmp_path, world):
+    if not torch.cuda.is_available() or torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
     hist, tol = oracle_hist
     teacher = tmp_path / "teacher.npy"
     np.save(teacher, np.stack([h[0] for h in hist]).astype(np.int32))
     out = str(tmp_path / "res")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(29400 + os.getpid() % 500),
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
+           "--master-addr", "127.0.0.1", "--master-port", str(29400 + os.getpid() % 500 + world),
            os.path.join(HERE, "spmd_worker.py"), str(teacher), out]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-4000:]
     r0 = np.load(out + ".0.npz")
-    r1 = np.load(out + ".1.npz")
+    r1 = np.load(out + f".{world - 1}.npz")  # the last stage returns the logits before consolidation
     for r in range(ROUNDS):
         assert r0[f"r{r}_cons_bytes"][0] > 0 and r0[f"r{r}_cons_bytes"][1] > 0
         for step in range(POST + 1):
