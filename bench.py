@@ -215,9 +215,9 @@ def run_ours(args):
                 r["decode2_dev"] = dev2 / 1e3
             r["prof"] = g.profile_read(reset=True) if profile else {}
             barrier()
+            g.destroy()  # closes this rank's peer mappings (collective) before the endpoints free
             for e in eps:
                 e.destroy()
-            g.destroy()
             state["g"] = None
             return r
         if consolidate:

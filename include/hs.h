@@ -299,6 +299,11 @@ hs_status hs_consolidate(hs_group* g, int32_t target_stage, hs_consolidate_stats
 hs_status hs_scale_up(hs_group* g, const int32_t* seq_owner, int32_t n_live, hs_group** out,
                       hs_consolidate_stats* stats);
 
+/* Frees everything the group owns.  SPMD: collective (every rank calls it on the same group);
+ * the ranks close their CUDA-IPC mappings of peer memory, meet at hs_comm.barrier, then free
+ * their own memory, so no exporter frees a region a peer still maps.  After hs_scale_up,
+ * destroy the emptied group (which holds the peer mappings) before the endpoints.
+ * A dead group (HS_E_CUDA) skips the barrier.  NULL is a no-op. */
 hs_status hs_group_destroy(hs_group* g);
 const char* hs_last_error(void);
 

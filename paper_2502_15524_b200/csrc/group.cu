@@ -1520,6 +1520,10 @@ extern "C" hs_status hs_group_destroy(hs_group* g) {
     if (!s.owned) free_stage(s);
   for (void* p : g->ipc_deferred)
     if (p) cudaIpcCloseMemHandle(p);
+  // SPMD: every importer closes its mappings of a peer's arena / KV / comm block before that
+  // peer frees them (an exporter's cudaFree ahead of an importer's close is undefined), so the
+  // ranks meet here between the closes above and the frees below.  A dead group skips it.
+  if (g->spmd && !g->dead && g->comm.barrier) g->comm.barrier(g->comm.ctx);
   for (auto& s : g->st)
     if (s.owned) free_stage(s);
   delete g;
