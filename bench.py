@@ -237,6 +237,7 @@ def run_ours(args):
                 r["decode2_dev"] = dev2 / 1e3
         r["prof"] = g.profile_read(reset=True) if profile else {}
         if consolidate:
+            g.release_peer_memory()  # collective: the sources' released HBM is freed here
             barrier()
             g.destroy()
             state["g"] = None

@@ -299,6 +299,15 @@ hs_status hs_consolidate(hs_group* g, int32_t target_stage, hs_consolidate_stats
 hs_status hs_scale_up(hs_group* g, const int32_t* seq_owner, int32_t n_live, hs_group** out,
                       hs_consolidate_stats* stats);
 
+/* SPMD, collective: frees the HBM that consolidation released on the non-target ranks.  The
+ * released stages' arena / KV / comm memory is exported to peers over CUDA IPC, and an exporter
+ * may free it only after every importer has closed its mapping (closing multi-GB mappings costs
+ * ~100 ms, so hs_consolidate defers it off the decode pause).  Each rank closes its deferred
+ * mappings, meets at hs_comm.barrier, then frees its released memory.  Call it after
+ * hs_consolidate once the pause no longer matters (hs_group_destroy does it too).  No-op in
+ * local mode and when nothing is pending.  Errors: HS_E_INVAL (NULL), HS_E_STATE (barrier). */
+hs_status hs_release_peer_memory(hs_group* g);
+
 /* Frees everything the group owns.  SPMD: collective (every rank calls it on the same group);
  * the ranks close their CUDA-IPC mappings of peer memory, meet at hs_comm.barrier, then free
  * their own memory, so no exporter frees a region a peer still maps.  After hs_scale_up,

@@ -157,6 +157,9 @@ struct hs_group {
   struct ProfAcc { uint64_t count = 0; double ms = 0, bytes = 0, flops = 0; };
   std::map<int, ProfAcc> prof_acc;
   std::vector<void*> ipc_deferred;  // peer mappings of released stages, closed at destroy
+  // SPMD: this rank's exported arena / KV / comm memory of a released stage, freed only after
+  // every importer has closed its mapping (hs_release_peer_memory or destroy)
+  std::vector<std::pair<int, void*>> exp_deferred;  // (device, pointer)
 };
 
 namespace hs {
@@ -1251,12 +1254,19 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
   for (int k : g->active)
     if (k != tgt) {
       Stage& S = g->st[k];
-      if (!S.owned && S.ipc_arena_open) {  // unmapping ~GBs costs ~100 ms: defer it to destroy
+      if (!S.owned && S.ipc_arena_open) {  // unmapping ~GBs costs ~100 ms: defer it
         g->ipc_deferred.push_back(S.arena);
         g->ipc_deferred.push_back(S.kv_mem);
         S.ipc_arena_open = false;
         S.arena = nullptr;
         S.kv_mem = nullptr;
+      }
+      if (S.owned && g->spmd) {  // exported: peers may still map it; freed at the release point
+        for (void* p : {static_cast<void*>(S.arena), static_cast<void*>(S.kv_mem), static_cast<void*>(S.comm)})
+          if (p) g->exp_deferred.push_back({S.device, p});
+        S.arena = nullptr;
+        S.kv_mem = nullptr;
+        S.comm = nullptr;
       }
       free_stage(S);
     }
@@ -1503,6 +1513,27 @@ extern "C" hs_status hs_scale_up(hs_group* g, const int32_t* seq_owner, int32_t 
   return r;
 }
 
+// Collective (SPMD): close this rank's mappings of released peers' memory, meet, then free this
+// rank's exported memory of released stages.  Safe to call any number of times.
+static hs_status release_peer_memory(hs_group* g, bool barrier) {
+  for (void* p : g->ipc_deferred)
+    if (p) cudaIpcCloseMemHandle(p);
+  g->ipc_deferred.clear();
+  if (barrier && g->spmd && g->comm.barrier && g->comm.barrier(g->comm.ctx) != 0)
+    HS_FAIL(HS_E_STATE, "barrier failed");
+  for (auto& dp : g->exp_deferred) {
+    DeviceGuard dg(dp.first);
+    cudaFree(dp.second);
+  }
+  g->exp_deferred.clear();
+  return HS_OK;
+}
+
+extern "C" hs_status hs_release_peer_memory(hs_group* g) {
+  if (!g) HS_FAIL(HS_E_INVAL, "null group");
+  return release_peer_memory(g, !g->dead);
+}
+
 extern "C" hs_status hs_group_destroy(hs_group* g) {
   if (!g) return HS_OK;
   for (auto& s : g->st) {
@@ -1518,12 +1549,10 @@ extern "C" hs_status hs_group_destroy(hs_group* g) {
   }
   for (auto& s : g->st)
     if (!s.owned) free_stage(s);
-  for (void* p : g->ipc_deferred)
-    if (p) cudaIpcCloseMemHandle(p);
   // SPMD: every importer closes its mappings of a peer's arena / KV / comm block before that
   // peer frees them (an exporter's cudaFree ahead of an importer's close is undefined), so the
-  // ranks meet here between the closes above and the frees below.  A dead group skips it.
-  if (g->spmd && !g->dead && g->comm.barrier) g->comm.barrier(g->comm.ctx);
+  // ranks meet between the closes and the frees.  A dead group skips the barrier.
+  release_peer_memory(g, !g->dead);
   for (auto& s : g->st)
     if (s.owned) free_stage(s);
   delete g;

@@ -117,7 +117,7 @@ SYMBOLS = ["hs_image_layout", "hs_plan_stages", "hs_predict_ttft_eq1", "hs_predi
            "hs_k_gemm", "hs_k_rmsnorm", "hs_k_rope_kv", "hs_k_attention", "hs_k_argmax", "hs_k_embed",
            "hs_k_span_copy", "hs_debug_gemm_trace", "hs_debug_dstack_trace", "hs_debug_tmem_a_gemm", "hs_plan_auto", "hs_links_create", "hs_links_admit",
            "hs_links_settle", "hs_links_complete", "hs_links_pending", "hs_links_destroy",
-           "hs_load_background_async", "hs_scale_up"]
+           "hs_load_background_async", "hs_scale_up", "hs_release_peer_memory"]
 
 _lib = None
 
@@ -151,6 +151,7 @@ def lib():
     L.hs_release_seq.argtypes = [VP, C.c_int64]
     L.hs_consolidate.argtypes = [VP, I32, P(ConsolidateStats)]
     L.hs_group_destroy.argtypes = [VP]
+    L.hs_release_peer_memory.argtypes = [VP]
     L.hs_group_info.argtypes = [VP, P(I32), P(I32)]
     L.hs_debug_read_kv.argtypes = [VP, C.c_int64, I32, I32, I32, VP]
     L.hs_debug_read_weights.argtypes = [VP, I32, U64, U64, VP]
@@ -386,6 +387,11 @@ class Group:
         s = ConsolidateStats()
         check(lib().hs_consolidate(self.h, target, C.byref(s)))
         return s
+
+    def release_peer_memory(self):
+        """SPMD, collective: free the HBM consolidation released on the non-target ranks (after
+        every rank has closed its peer mappings of it)."""
+        check(lib().hs_release_peer_memory(self.h))
 
     def scale_up(self, seq_owner=None):
         """Every stage becomes a standalone endpoint; returns (list of Group, stats).  This group

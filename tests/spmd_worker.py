@@ -54,6 +54,8 @@ def main():
                 out[f"r{r}_log{step}"] = logits.copy()
         st = g.consolidate(0)
         out[f"r{r}_cons_bytes"] = np.array([st.weight_bytes, st.kv_bytes])
+        if r % 2 == 0:  # the sources free their HBM before the target decodes on (else: at destroy)
+            g.release_peer_memory()
         if rank == 0:
             for step in range(PRE + 1, POST + 1):
                 toks, logits = g.decode_step([0, 1], teacher[step - 1], want_logits=True)
