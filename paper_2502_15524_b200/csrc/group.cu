@@ -160,6 +160,9 @@ struct hs_group {
   // SPMD: this rank's exported arena / KV / comm memory of a released stage, freed only after
   // every importer has closed its mapping (hs_release_peer_memory or destroy)
   std::vector<std::pair<int, void*>> exp_deferred;  // (device, pointer)
+  // SPMD: the rest of a released stage's teardown (buffers, streams, events, comm mapping) also
+  // waits for the release point, so consolidation's pause makes no driver free/unmap calls
+  std::vector<hs::Stage> stage_deferred;
 };
 
 namespace hs {
@@ -1268,7 +1271,12 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
         S.kv_mem = nullptr;
         S.comm = nullptr;
       }
-      free_stage(S);
+      if (g->spmd) {
+        g->stage_deferred.push_back(S);
+        S = Stage{};
+      } else {
+        free_stage(S);
+      }
     }
   g->active = {tgt};
   g->st[tgt].lb = 0;
@@ -1519,6 +1527,8 @@ static hs_status release_peer_memory(hs_group* g, bool barrier) {
   for (void* p : g->ipc_deferred)
     if (p) cudaIpcCloseMemHandle(p);
   g->ipc_deferred.clear();
+  for (Stage& s : g->stage_deferred)  // importer side first: closes the comm mapping
+    if (!s.owned) free_stage(s);
   if (barrier && g->spmd && g->comm.barrier && g->comm.barrier(g->comm.ctx) != 0)
     HS_FAIL(HS_E_STATE, "barrier failed");
   for (auto& dp : g->exp_deferred) {
@@ -1526,6 +1536,9 @@ static hs_status release_peer_memory(hs_group* g, bool barrier) {
     cudaFree(dp.second);
   }
   g->exp_deferred.clear();
+  for (Stage& s : g->stage_deferred)
+    if (s.owned) free_stage(s);
+  g->stage_deferred.clear();
   return HS_OK;
 }
 
