@@ -1158,7 +1158,7 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
   }
   if (g->spmd && g->comm.barrier(g->comm.ctx) != 0) HS_FAIL(HS_E_STATE, "barrier failed");
   const auto t_drained = std::chrono::steady_clock::now();
-  auto t_copied = t_drained;
+  auto t_copied = t_drained, t_listed = t_drained, t_synced = t_drained;
   Stage& T = g->st[tgt];
   if (T.owned) {
     DeviceGuard dg(T.device);
@@ -1213,6 +1213,7 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
       HS_CUDA(cudaMalloc(&d_list, list.size() * sizeof(CopyDesc)));
       HS_CUDA(cudaMemcpy(d_list, list.data(), list.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
     }
+    t_listed = std::chrono::steady_clock::now();
     if (getenv("HS_DEBUG_CONS_SYNC")) {
       cudaError_t pe = cudaDeviceSynchronize();
       if (pe != cudaSuccess) HS_FAIL(HS_E_CUDA, "consolidate: fault before the copy list: %s", cudaGetErrorString(pe));
@@ -1229,6 +1230,7 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
     float ms = 0;
     HS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     stats.seconds = ms / 1e3;
+    t_synced = std::chrono::steady_clock::now();
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaEventDestroy(e2);
@@ -1284,9 +1286,13 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
   g->plan.pp = 1;
   stats.pause_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_enter).count();
   if (getenv("HS_DEBUG_CONS"))
-    fprintf(stderr, "[hs] consolidate: drain %.1f ms, copy-list build+copy %.1f ms, free %.1f ms, total %.1f ms\n",
+    fprintf(stderr, "[hs] consolidate: drain %.1f ms, copy-list build+copy %.1f ms (list %.1f, copy %.1f, "
+            "barrier %.1f), free %.1f ms, total %.1f ms\n",
             1e3 * std::chrono::duration<double>(t_drained - t_enter).count(),
             1e3 * std::chrono::duration<double>(t_copied - t_drained).count(),
+            1e3 * std::chrono::duration<double>(t_listed - t_drained).count(),
+            1e3 * std::chrono::duration<double>(t_synced - t_listed).count(),
+            1e3 * std::chrono::duration<double>(t_copied - t_synced).count(),
             1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t_copied).count(),
             1e3 * stats.pause_seconds);
   if (out) *out = stats;
