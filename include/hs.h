@@ -303,16 +303,20 @@ hs_status hs_scale_up(hs_group* g, const int32_t* seq_owner, int32_t n_live, hs_
  * released stages' arena / KV / comm memory is exported to peers over CUDA IPC, and an exporter
  * may free it only after every importer has closed its mapping (closing multi-GB mappings costs
  * ~100 ms, so hs_consolidate defers it off the decode pause).  Each rank closes its deferred
- * mappings, meets at hs_comm.barrier, then frees its released memory.  Call it after
- * hs_consolidate once the pause no longer matters (hs_group_destroy does it too).  No-op in
- * local mode and when nothing is pending.  Errors: HS_E_INVAL (NULL), HS_E_STATE (barrier). */
+ * mappings, meets at hs_comm.barrier, then frees its released memory.  ALWAYS collective in SPMD
+ * mode: every rank must call it (also when it has nothing pending), because every rank enters the
+ * barrier.  No-op in local mode.  hs_group_destroy does it too.  Errors: HS_E_INVAL (NULL),
+ * HS_E_STATE (the barrier failed: the exported regions are then left allocated, never freed under
+ * a peer's mapping; everything else is released). */
 hs_status hs_release_peer_memory(hs_group* g);
 
-/* Frees everything the group owns.  SPMD: collective (every rank calls it on the same group);
- * the ranks close their CUDA-IPC mappings of peer memory, meet at hs_comm.barrier, then free
- * their own memory, so no exporter frees a region a peer still maps.  After hs_scale_up,
- * destroy the emptied group (which holds the peer mappings) before the endpoints.
- * A dead group (HS_E_CUDA) skips the barrier.  NULL is a no-op. */
+/* Frees everything the group owns.  SPMD: collective (every rank calls it on the same group,
+ * also after an HS_E_CUDA failure); the ranks close their CUDA-IPC mappings of peer memory,
+ * meet at hs_comm.barrier, then free their own memory, so no exporter frees a region a peer
+ * still maps.  If the barrier fails the exported regions stay allocated (leaked for the life of
+ * the process) and HS_E_STATE is returned; the group is freed in every case.  After
+ * hs_scale_up, destroy the emptied group (which holds the peer mappings) before the endpoints.
+ * NULL is a no-op. */
 hs_status hs_group_destroy(hs_group* g);
 const char* hs_last_error(void);
 

@@ -51,12 +51,6 @@ hs_status hs_debug_gemm_trace(int32_t enable, void* host_out, int32_t n_ctas);
  * host_out (optional) receives n_words uint64.  enable == 0 frees the buffer. */
 hs_status hs_debug_dstack_trace(int32_t enable, void* host_out, int64_t n_words);
 
-/* Test-only probe of the tcgen05 A-operand-in-TMEM path: one 128 x 16 tile, K a multiple of
- * 64; A [128][K], B [16][K] bf16 device pointers; out_ss / out_ts [16][128] fp32 device
- * pointers receive D = A.B^T computed with A from shared memory / A copied to TMEM
- * (tcgen05.cp.128x256b) respectively.  Synchronous. */
-hs_status hs_debug_tmem_a_gemm(const void* A, const void* B, int32_t K, float* out_ss, float* out_ts);
-
 #ifdef __cplusplus
 }
 #endif

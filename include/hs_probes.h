@@ -1,0 +1,23 @@
+/* hs_probes.h — test-only hardware probes, built into libhs_probe.so (never into libhs.so).
+ * They measured design alternatives of the decode stack and are kept so the
+ * measurement can be repeated; no product path calls them. */
+#ifndef HS_PROBES_H_
+#define HS_PROBES_H_
+#include <stdint.h>
+
+#include "hs.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Test-only probe of the tcgen05 A-operand-in-TMEM path: one 128 x 16 tile, K a multiple of
+ * 64; A [128][K], B [16][K] bf16 device pointers; out_ss / out_ts [16][128] fp32 device
+ * pointers receive D = A.B^T computed with A from shared memory / A copied to TMEM
+ * (tcgen05.cp.128x256b) respectively.  Synchronous. */
+hs_status hs_debug_tmem_a_gemm(const void* A, const void* B, int32_t K, float* out_ss, float* out_ts);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

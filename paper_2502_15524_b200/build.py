@@ -8,6 +8,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libhs.so")
+PROBES = os.path.join(HERE, "probes")
+PROBE_SO = os.path.join(HERE, "libhs_probe.so")  # test-only hardware probes (never in libhs.so)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
@@ -24,11 +26,15 @@ def headers():
         [os.path.join(inc, f) for f in os.listdir(inc)]
 
 
+def probe_sources():
+    return sorted(os.path.join(PROBES, f) for f in os.listdir(PROBES) if f.endswith(".cu"))
+
+
 def stale() -> bool:
-    if not os.path.exists(SO):
+    if not os.path.exists(SO) or not os.path.exists(PROBE_SO):
         return True
-    t = os.path.getmtime(SO)
-    return any(os.path.getmtime(f) > t for f in sources() + headers())
+    t = min(os.path.getmtime(SO), os.path.getmtime(PROBE_SO))
+    return any(os.path.getmtime(f) > t for f in sources() + probe_sources() + headers())
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -56,6 +62,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         print("\n".join(logs))
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", SO, *objs, "-Xcompiler", "-fPIC"])
+    # test-only probes: a separate library linked against libhs.so
+    pobjs = []
+    for src in probe_sources():
+        obj = os.path.join(HERE, "build", "probe_" + os.path.basename(src) + ".o")
+        subprocess.check_call([NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj], stdout=subprocess.DEVNULL)
+        pobjs.append(obj)
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", PROBE_SO, *pobjs, "-Xcompiler", "-fPIC",
+                           "-L" + HERE, "-lhs", "-Xlinker", "-rpath,$ORIGIN"])
     return SO
 
 

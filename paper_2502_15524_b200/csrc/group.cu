@@ -139,6 +139,7 @@ struct hs_group {
   hs_comm comm{};
   int owned_stage = -1;
   bool dead = false;
+  bool comm_failed = false;  // an hs_comm callback failed: collective teardown cannot be agreed on
   std::vector<hs::Stage> st;
   std::vector<int> active;  // stage indices in pipeline order
   hs::CommLayout cl;
@@ -171,6 +172,17 @@ static hs_status stage_of_layer(hs_group* g, int layer, int* out) {
   for (int k : g->active)
     if (layer >= g->st[k].lb && layer < g->st[k].le) { *out = k; return HS_OK; }
   HS_FAIL(HS_E_INVAL, "layer %d not held by any active stage", layer);
+}
+
+// SPMD barrier through the caller's callback; a failure is remembered (teardown then cannot
+// agree with the peers and keeps exported memory alive rather than free it under a mapping).
+static bool comm_barrier(hs_group* g) {
+  if (!g->spmd) return true;
+  if (g->comm_failed || !g->comm.barrier || g->comm.barrier(g->comm.ctx) != 0) {
+    g->comm_failed = true;
+    return false;
+  }
+  return true;
 }
 
 // ---- per-kernel-kind profile ------------------------------------------------------------
@@ -221,12 +233,14 @@ static double gemm_bytes(double M, double N, double K, double Mout, bool resid) 
   return 2.0 * (M * K + N * K + N * Mout + (resid ? N * Mout : 0.0));
 }
 
-// Free everything a stage owns (device + pinned).
-static void free_stage(Stage& s) {
+// Free everything a stage owns (device + pinned).  keep_exported: leave the memory peers may
+// map over CUDA IPC (arena, KV pools, comm block) allocated (SPMD teardown without agreement).
+static void free_stage(Stage& s, bool keep_exported = false) {
   DeviceGuard dg(s.device);
   auto F = [](void* p) { if (p) cudaFree(p); };
   if (s.owned) {
-    F(s.arena); F(s.kv_mem); F(s.comm); F(s.xa); F(s.xb); F(s.nrm); F(s.qkv); F(s.q); F(s.o);
+    if (!keep_exported) { F(s.arena); F(s.kv_mem); F(s.comm); }
+    F(s.xa); F(s.xb); F(s.nrm); F(s.qkv); F(s.q); F(s.o);
     F(s.act); F(s.fin); F(s.logits); F(s.ws); F(s.attn_ws); F(s.ctr); F(s.rope); F(s.d_meta); F(s.d_tok_out);
     if (s.h_meta) cudaFreeHost(s.h_meta);
     if (s.h_out) cudaFreeHost(s.h_out);
@@ -968,8 +982,10 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
       const uint64_t tb = align_up((uint64_t)m.n * 4, 16);
       // token feedback to the first stage (the next decode embeds it on the device); in SPMD
       // mode to every stage, so that every rank can return the tokens
+      // (local mode: also every full-memory stage, a possible consolidation target that then
+      // embeds the fed-back tokens of the next decode step itself)
       for (int kk : g->active) {
-        if (!g->spmd && kk != first) continue;
+        if (!g->spmd && kk != first && !g->st[kk].full_memory) continue;
         Stage& d = g->st[kk];
         launch_send(s.d_tok_out, d.comm + g->cl.tok_in, tb, s.done(), d.flag_tok(), ep, 1, st);
       }
@@ -1140,6 +1156,18 @@ static hs_status open_peer_memory(hs_group* g, Stage& s) {
   return HS_OK;
 }
 
+// Appends {src, dst, bytes} to a copy list in pieces of at most `piece` bytes.  copy_list_kernel
+// moves 16-byte words: every address and size must be a multiple of 16 (weight slices are
+// HS_IMAGE_ALIGN aligned, KV blocks are 16 * 2 * H * 2 bytes), checked here rather than
+// silently dropping a tail.
+static hs_status add_copy(std::vector<CopyDesc>& list, uint64_t src, uint64_t dst, uint64_t bytes, uint64_t piece) {
+  if ((src | dst | bytes | piece) & 15)
+    HS_FAIL(HS_E_INVAL, "copy list: src 0x%llx dst 0x%llx bytes %llu not 16-byte aligned", (unsigned long long)src,
+            (unsigned long long)dst, (unsigned long long)bytes);
+  for (uint64_t o = 0; o < bytes; o += piece) list.push_back({src + o, dst + o, std::min(piece, bytes - o)});
+  return HS_OK;
+}
+
 static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
   const auto t_enter = std::chrono::steady_clock::now();
   if (g->dead) HS_FAIL(HS_E_CUDA, "group is dead");
@@ -1156,7 +1184,7 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
     HS_CUDA(cudaStreamSynchronize(s.comp));
     HS_CUDA(cudaStreamSynchronize(s.copy));
   }
-  if (g->spmd && g->comm.barrier(g->comm.ctx) != 0) HS_FAIL(HS_E_STATE, "barrier failed");
+  if (!comm_barrier(g)) HS_FAIL(HS_E_STATE, "barrier failed");
   const auto t_drained = std::chrono::steady_clock::now();
   auto t_copied = t_drained, t_listed = t_drained, t_synced = t_drained;
   Stage& T = g->st[tgt];
@@ -1180,16 +1208,16 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
       return (e && atoi(e) > 0 ? (uint64_t)atoi(e) : 1024ull) << 10;
     }();
     std::vector<CopyDesc> list;
-    auto add = [&](uint64_t src, uint64_t dst, uint64_t bytes) {
-      for (uint64_t o = 0; o < bytes; o += piece) list.push_back({src + o, dst + o, std::min(piece, bytes - o)});
+    auto add = [&](uint64_t src, uint64_t dst, uint64_t bytes) -> hs_status {
+      return add_copy(list, src, dst, bytes, piece);
     };
     for (int k : g->active) {
       if (k == tgt) continue;
       Stage& S = g->st[k];
       HS_TRY(open_peer_memory(g, S));
       if (T.bg_issued) continue;  // the weights come over the target's own PCIe link
-      add(reinterpret_cast<uint64_t>(S.arena + (S.slice_begin - S.arena_off0)), reinterpret_cast<uint64_t>(T.wptr(S.slice_begin)),
-          S.slice_end - S.slice_begin);
+      HS_TRY(add(reinterpret_cast<uint64_t>(S.arena + (S.slice_begin - S.arena_off0)),
+                 reinterpret_cast<uint64_t>(T.wptr(S.slice_begin)), S.slice_end - S.slice_begin));
       stats.weight_bytes += g->plan.stage_bytes[k];
     }
     if (T.bg_issued) {
@@ -1202,9 +1230,9 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
       for (int l = S.lb; l < S.le; ++l)
         for (auto& kvp : g->seqs)
           for (int b : kvp.second.blocks) {
-            add(reinterpret_cast<uint64_t>(S.kv_pool(l, g->kv_layer_bytes)) + (uint64_t)b * g->kv_block_bytes,
-                reinterpret_cast<uint64_t>(T.kv_pool(l, g->kv_layer_bytes)) + (uint64_t)b * g->kv_block_bytes,
-                g->kv_block_bytes);
+            HS_TRY(add(reinterpret_cast<uint64_t>(S.kv_pool(l, g->kv_layer_bytes)) + (uint64_t)b * g->kv_block_bytes,
+                       reinterpret_cast<uint64_t>(T.kv_pool(l, g->kv_layer_bytes)) + (uint64_t)b * g->kv_block_bytes,
+                       g->kv_block_bytes));
             stats.kv_bytes += g->kv_block_bytes;
           }
     }
@@ -1246,7 +1274,7 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
     HS_CUDA(cudaEventRecord(T.ev_final, T.copy));
     T.load_issued = true;
   }
-  if (g->spmd && g->comm.barrier(g->comm.ctx) != 0) HS_FAIL(HS_E_STATE, "barrier failed");
+  if (!comm_barrier(g)) HS_FAIL(HS_E_STATE, "barrier failed");
   t_copied = std::chrono::steady_clock::now();
   // 5. release the other stages ("other workers are terminated"); a stage
   //    sharing the target's device hands its streams over first
@@ -1328,7 +1356,7 @@ static hs_status scale_up(hs_group* g, const int32_t* owner_in, int32_t n_live, 
     HS_CUDA(cudaStreamSynchronize(s.comp));
     HS_CUDA(cudaStreamSynchronize(s.copy));
   }
-  if (g->spmd && g->comm.barrier(g->comm.ctx) != 0) HS_FAIL(HS_E_STATE, "barrier failed");
+  if (!comm_barrier(g)) HS_FAIL(HS_E_STATE, "barrier failed");
   hs_consolidate_stats tot{};
   const uint64_t piece = 64ull << 10;
   struct Pending { int k; CopyDesc* d; cudaEvent_t e0, e1; };
@@ -1338,23 +1366,23 @@ static hs_status scale_up(hs_group* g, const int32_t* owner_in, int32_t n_live, 
     if (!T.owned) continue;
     DeviceGuard dg(T.device);
     std::vector<CopyDesc> list;
-    auto add = [&](uint64_t src, uint64_t dst, uint64_t bytes) {
-      for (uint64_t o = 0; o < bytes; o += piece) list.push_back({src + o, dst + o, std::min(piece, bytes - o)});
+    auto add = [&](uint64_t src, uint64_t dst, uint64_t bytes) -> hs_status {
+      return add_copy(list, src, dst, bytes, piece);
     };
     for (int k : g->active) {
       if (k == t) continue;
       Stage& S = g->st[k];
       HS_TRY(open_peer_memory(g, S));
-      add(reinterpret_cast<uint64_t>(S.arena + (S.slice_begin - S.arena_off0)), reinterpret_cast<uint64_t>(T.wptr(S.slice_begin)),
-          S.slice_end - S.slice_begin);
+      HS_TRY(add(reinterpret_cast<uint64_t>(S.arena + (S.slice_begin - S.arena_off0)),
+                 reinterpret_cast<uint64_t>(T.wptr(S.slice_begin)), S.slice_end - S.slice_begin));
       tot.weight_bytes += g->plan.stage_bytes[k];
       for (int l = S.lb; l < S.le; ++l)
         for (auto& kvp : g->seqs) {
           if (owner[kvp.first] != t) continue;
           for (int b : kvp.second.blocks) {
-            add(reinterpret_cast<uint64_t>(S.kv_pool(l, g->kv_layer_bytes)) + (uint64_t)b * g->kv_block_bytes,
-                reinterpret_cast<uint64_t>(T.kv_pool(l, g->kv_layer_bytes)) + (uint64_t)b * g->kv_block_bytes,
-                g->kv_block_bytes);
+            HS_TRY(add(reinterpret_cast<uint64_t>(S.kv_pool(l, g->kv_layer_bytes)) + (uint64_t)b * g->kv_block_bytes,
+                       reinterpret_cast<uint64_t>(T.kv_pool(l, g->kv_layer_bytes)) + (uint64_t)b * g->kv_block_bytes,
+                       g->kv_block_bytes));
             tot.kv_bytes += g->kv_block_bytes;
           }
         }
@@ -1383,7 +1411,7 @@ static hs_status scale_up(hs_group* g, const int32_t* owner_in, int32_t n_live, 
     if (p.d) cudaFree(p.d);
   }
   tot.seconds = secs;
-  if (g->spmd && g->comm.barrier(g->comm.ctx) != 0) HS_FAIL(HS_E_STATE, "barrier failed");
+  if (!comm_barrier(g)) HS_FAIL(HS_E_STATE, "barrier failed");
   // split: each owned stage becomes a single-stage group with its sequences
   int n_out = 0;
   std::vector<int> owned_stages;
@@ -1528,29 +1556,34 @@ extern "C" hs_status hs_scale_up(hs_group* g, const int32_t* seq_owner, int32_t 
 }
 
 // Collective (SPMD): close this rank's mappings of released peers' memory, meet, then free this
-// rank's exported memory of released stages.  Safe to call any number of times.
-static hs_status release_peer_memory(hs_group* g, bool barrier) {
+// rank's exported memory of released stages.  Every rank enters the barrier (a rank-local
+// "dead" flag is not agreed on, so it must not decide who skips it); only a failed comm skips
+// it, and then the exported memory stays allocated (a peer may still map it) while everything
+// else is freed.  Safe to call any number of times.
+static hs_status release_peer_memory(hs_group* g) {
   for (void* p : g->ipc_deferred)
     if (p) cudaIpcCloseMemHandle(p);
   g->ipc_deferred.clear();
   for (Stage& s : g->stage_deferred)  // importer side first: closes the comm mapping
     if (!s.owned) free_stage(s);
-  if (barrier && g->spmd && g->comm.barrier && g->comm.barrier(g->comm.ctx) != 0)
-    HS_FAIL(HS_E_STATE, "barrier failed");
-  for (auto& dp : g->exp_deferred) {
-    DeviceGuard dg(dp.first);
-    cudaFree(dp.second);
+  const bool agreed = comm_barrier(g);
+  if (agreed) {
+    for (auto& dp : g->exp_deferred) {
+      DeviceGuard dg(dp.first);
+      cudaFree(dp.second);
+    }
   }
-  g->exp_deferred.clear();
+  g->exp_deferred.clear();  // (without agreement: intentionally leaked, never freed under a peer)
   for (Stage& s : g->stage_deferred)
     if (s.owned) free_stage(s);
   g->stage_deferred.clear();
+  if (!agreed) HS_FAIL(HS_E_STATE, "barrier failed: exported memory of released stages left allocated");
   return HS_OK;
 }
 
 extern "C" hs_status hs_release_peer_memory(hs_group* g) {
   if (!g) HS_FAIL(HS_E_INVAL, "null group");
-  return release_peer_memory(g, !g->dead);
+  return release_peer_memory(g);
 }
 
 extern "C" hs_status hs_group_destroy(hs_group* g) {
@@ -1570,12 +1603,14 @@ extern "C" hs_status hs_group_destroy(hs_group* g) {
     if (!s.owned) free_stage(s);
   // SPMD: every importer closes its mappings of a peer's arena / KV / comm block before that
   // peer frees them (an exporter's cudaFree ahead of an importer's close is undefined), so the
-  // ranks meet between the closes and the frees.  A dead group skips the barrier.
-  release_peer_memory(g, !g->dead);
+  // ranks meet between the closes and the frees.  Without agreement (failed comm) the exported
+  // regions stay allocated; every other resource is released either way.
+  const hs_status r = release_peer_memory(g);
+  const bool keep_exported = g->spmd && r != HS_OK;
   for (auto& s : g->st)
-    if (s.owned) free_stage(s);
+    if (s.owned) free_stage(s, keep_exported);
   delete g;
-  return HS_OK;
+  return r;
 }
 
 extern "C" hs_status hs_group_info(hs_group* g, int32_t* pp, int32_t* owned) {

@@ -714,7 +714,8 @@ __global__ void __launch_bounds__(256) span_copy_kernel(const uint64_t* __restri
   for (; i < e; i += 256) d[i] = s[i];
 }
 
-// Copy list: descriptors {src, dst, bytes} (bytes % 16 == 0, <= 64 KiB each), persistent
+// Copy list: descriptors {src, dst, bytes} (src, dst, bytes multiples of 16, checked by the
+// host-side list builder; any size: consolidation uses 1 MiB pieces by default), persistent
 // grid-stride over descriptors; 4 x 16-byte loads in flight per thread before the stores.
 __global__ void __launch_bounds__(256) copy_list_kernel(const CopyDesc* __restrict__ d, int n) {
   PDL_LAUNCH();

@@ -115,7 +115,7 @@ SYMBOLS = ["hs_image_layout", "hs_plan_stages", "hs_predict_ttft_eq1", "hs_predi
            "hs_debug_poison_weights", "hs_debug_launch_count", "hs_stage_timing_get", "hs_profile_enable",
            "hs_profile_read", "hs_debug_comm_selftest",
            "hs_k_gemm", "hs_k_rmsnorm", "hs_k_rope_kv", "hs_k_attention", "hs_k_argmax", "hs_k_embed",
-           "hs_k_span_copy", "hs_debug_gemm_trace", "hs_debug_dstack_trace", "hs_debug_tmem_a_gemm", "hs_plan_auto", "hs_links_create", "hs_links_admit",
+           "hs_k_span_copy", "hs_debug_gemm_trace", "hs_debug_dstack_trace", "hs_plan_auto", "hs_links_create", "hs_links_admit",
            "hs_links_settle", "hs_links_complete", "hs_links_pending", "hs_links_destroy",
            "hs_load_background_async", "hs_scale_up", "hs_release_peer_memory"]
 
@@ -170,7 +170,6 @@ def lib():
     L.hs_k_span_copy.argtypes = [VP, VP, I32, U64, VP]
     L.hs_debug_gemm_trace.argtypes = [I32, VP, I32]
     L.hs_debug_dstack_trace.argtypes = [I32, VP, C.c_int64]
-    L.hs_debug_tmem_a_gemm.argtypes = [VP, VP, I32, VP, VP]
     L.hs_plan_auto.argtypes = [P(ModelCfg), P(Gpu), I32, P(Slo), P(Plan), P(I32)]
     L.hs_links_create.argtypes = [I32, P(C.c_double), P(VP)]
     L.hs_links_admit.argtypes = [VP, I32, C.c_double, C.c_double, C.c_double, P(I32), P(C.c_int64)]
@@ -453,11 +452,16 @@ class Group:
         return v.value
 
     def destroy(self):
+        """Frees the group.  SPMD groups: collective, every rank must call it explicitly."""
         if self.h:
-            check(lib().hs_group_destroy(self.h))
-            self.h = C.c_void_p()
+            h, self.h = self.h, C.c_void_p()
+            check(lib().hs_group_destroy(h))
 
     def __del__(self):
+        # local groups are freed on collection; an SPMD group's destroy is collective (it meets
+        # the peers at a barrier) and must never run from a garbage collector on one rank only
+        if getattr(self, "_comm", None) is not None:
+            return
         try:
             self.destroy()
         except Exception:  # noqa
@@ -520,13 +524,29 @@ def dstack_trace(enable: bool, n_ctas: int = 0, n_layers: int = 0):
     return out[:n].reshape(n_ctas, n_layers, 32), out[n:].reshape(n_layers, 256)
 
 
+_probe = None
+
+
+def probe_lib():
+    """Test-only hardware probes (include/hs_probes.h), a separate library: never on a product path."""
+    global _probe
+    if _probe is None:
+        lib()
+        so = os.path.join(HERE, "libhs_probe.so")
+        if not os.path.exists(so):
+            raise ImportError(f"{so} is missing: build with python -m paper_2502_15524_b200.build")
+        _probe = C.CDLL(so)
+        _probe.hs_debug_tmem_a_gemm.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
+    return _probe
+
+
 def tmem_a_gemm(A, B):
     """Test-only: (D with A from smem, D with A staged in TMEM), each [16, 128] fp32."""
     import torch
     K = A.shape[1]
     o1 = torch.empty(16, 128, dtype=torch.float32, device=A.device)
     o2 = torch.empty_like(o1)
-    check(lib().hs_debug_tmem_a_gemm(_p(A), _p(B), K, _p(o1), _p(o2)))
+    check(probe_lib().hs_debug_tmem_a_gemm(_p(A), _p(B), K, _p(o1), _p(o2)))
     return o1, o2
 
 

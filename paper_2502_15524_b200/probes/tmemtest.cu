@@ -2,9 +2,11 @@
 // the weight tile lands in shared memory by TMA (128B swizzle, as everywhere else), is copied
 // to TMEM with tcgen05.cp.128x256b and multiplied with tcgen05.mma [d], [a_tmem], b_desc.  The
 // same tile multiplied from shared memory (the production path) is the reference.  Exposed as
-// hs_debug_tmem_a_gemm (include/hs_kernels.h).
-#include "gemm.h"
-#include "tc.h"
+// hs_debug_tmem_a_gemm (include/hs_probes.h).  Built into libhs_probe.so, never into the product
+// library libhs.so (it links against libhs.so for the TMA-descriptor helper).
+#include "../../include/hs_probes.h"
+#include "../csrc/gemm.h"
+#include "../csrc/tc.h"
 
 namespace hs {
 

@@ -333,3 +333,22 @@ def test_decode_stack_batches_and_long_context(image, oracle_run, n_seqs, long_c
     # every mismatch is an oracle near-tie (checked in compare); bound how many, per sequence
     assert len(ties) <= max(1, n_seqs // 8), ties
     g.destroy()
+
+
+def test_feedback_after_consolidating_into_a_later_stage(image, oracle_run):
+    """Device token feedback survives consolidation into a full-memory stage that is not the
+    first one (every full-memory stage receives the sampled tokens in local mode)."""
+    prompts, hist, _ = oracle_run
+    n = torch.cuda.device_count()
+    gpus = [dict(device=d, h2d_gbps=50.0, free_bytes=8 << 30) for d in range(max(n, 2))]
+    plan = hs.plan_stages(CFG, gpus, 2, 2)
+    plan.device[0] = plan.device[1] = 0
+    g = hs.Group(CFG, plan, image, num_blocks=64, max_seqs=8, max_tokens=256)
+    g.load_stage_async(-1)
+    toks, _ = g.prefill([0, 1], prompts)
+    for step in range(1, 5):
+        toks, _ = g.decode_step([0, 1])
+    g.consolidate(1)
+    toks, logits = g.decode_step([0, 1], want_logits=True)   # no in_tokens: device feedback
+    assert np.array_equal(toks, hist[5][0]) or np.sort(hist[5][1], axis=1)[:, -2:].ptp(axis=1).min() < 2 * TOL
+    g.destroy()

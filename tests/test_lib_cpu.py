@@ -30,6 +30,18 @@ def test_library_exports_every_declared_symbol():
     assert set(decl) == set(hs.SYMBOLS)
 
 
+def test_probes_live_outside_the_product_library():
+    """Test-only hardware probes (include/hs_probes.h) are exported by libhs_probe.so and absent
+    from libhs.so."""
+    src = open(os.path.join(ROOT, "include", "hs_probes.h")).read()
+    probes = re.findall(r"^\s*hs_status\s+(hs_\w+)\s*\(", src, re.M)
+    assert probes
+    P = hs.probe_lib()
+    for n in probes:
+        assert hasattr(P, n)
+        assert not hasattr(hs.lib(), n), n
+
+
 @pytest.mark.parametrize("name", ["tiny", "llama2-7b", "llama2-13b"])
 def test_image_layout_matches_generator(name):
     a = hs.image_layout(hsgen.CONFIGS[name])
