@@ -122,8 +122,8 @@ def run_ours(args):
 
     rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
     local = env_int("LOCAL_RANK", rank)
-    if world != args.gpus:
-        args.gpus = world
+    if world != args.gpus:  # main() launches N ranks when WORLD_SIZE is unset: never measure N=1 as N
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dist = None
     comm = None
@@ -469,6 +469,18 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def relaunch(n):
+    """`python bench.py --gpus N` without a launcher: start N ranks (one process per GPU) with
+    torch.distributed.run on 127.0.0.1 and pass their output and exit status through."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -488,6 +500,8 @@ def main():
                     help="N>1: the target loads the other stages' weights over its own PCIe link in the "
                          "background after the first token (paper's mechanism); consolidation moves KV only")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.config != 5:
+        sys.exit(relaunch(args.gpus))
     if args.config == 5:
         run_burst(args)
     elif args.impl == "reference":

@@ -329,6 +329,31 @@ hs_status hs_group_info(hs_group* g, int32_t* pp, int32_t* owned_stage);
  * the layer: host_out [n_pos][2][n_heads][head_dim] bf16.  Blocking. */
 hs_status hs_debug_read_kv(hs_group* g, int64_t seq_id, int32_t layer, int32_t pos0,
                            int32_t n_pos, void* host_out);
+/* Layer-boundary capture (test-only; the parity tests compare every half of every decoder
+ * layer on its own: a PP group computes exactly the unpartitioned layers).
+ * enable != 0 allocates, per stage this process drives, a device buffer of
+ * (2 n_layers + 1) x max_tokens x hidden bf16 and makes every later hs_prefill /
+ * hs_decode_step store the hidden state of every token at every capture point it computes:
+ * point 2l is the input of layer l (point 0 = the embedding rows, point 2L = the last layer's
+ * output, the final RMSNorm's input); point 2l + 1 is layer l's h = x + Attention(RMSNorm(x)) W_o^T
+ * (the residual stream between the attention and the MLP halves).  Same kernels and launch
+ * configuration as without capture: the decode stack writes the extra copies from its O- and
+ * down-projection epilogues; the per-kernel path copies behind each layer.  enable == 0 frees
+ * the buffers.  Errors: HS_E_INVAL, HS_E_OOM. */
+hs_status hs_debug_capture(hs_group* g, int32_t enable);
+/* Copies capture point `point` (0..2 n_layers) of rows [row0, row0 + n_rows) of the LATEST call
+ * to host_out ([n_rows][hidden] bf16).  Rows are in call order: hs_prefill's packed tokens
+ * (sequence by sequence, as passed), or one row per sequence for hs_decode_step, whatever
+ * micro-batch layout the call used on the device.  Blocking.  Errors: HS_E_STATE (capture
+ * off), HS_E_INVAL (rows outside the latest call, or the point lives on a stage driven by
+ * another process). */
+hs_status hs_debug_read_hidden(hs_group* g, int32_t point, int32_t row0, int32_t n_rows, void* host_out);
+/* Prefill micro-batching knobs (tests and A/B measurements; defaults are the product): a
+ * prefill is cut into nchunks = max(1, min(max_chunks, shortest prompt / 16, T / min_chunk_tokens))
+ * micro-batches (0 = default: max_chunks 4, min_chunk_tokens 1024).  max_chunks = 1 disables
+ * micro-batching.  The choice depends on the call's shapes only, never on the number of stages.
+ * Errors: HS_E_INVAL. */
+hs_status hs_debug_set_prefill_chunking(hs_group* g, int32_t min_chunk_tokens, int32_t max_chunks);
 /* Copies bytes [image_off, image_off+bytes) of the device weight arena of `stage` to host. */
 hs_status hs_debug_read_weights(hs_group* g, int32_t stage, uint64_t image_off,
                                 uint64_t bytes, void* host_out);

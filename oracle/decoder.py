@@ -159,9 +159,17 @@ class Worker:
         self.is_first = 0 in self.layers
         self.is_last = self.cfg["n_layers"] - 1 in self.layers
 
-    def layer_forward(self, l: int, x: np.ndarray, batch) -> np.ndarray:
+    def layer_forward(self, l: int, x: np.ndarray, batch, trace: dict | None = None) -> np.ndarray:
         """One decoder layer over the packed tokens of ``batch`` (list of (seq, positions,
-        slots, table) per sequence, in packing order).  x: float64 bf16 values [T, H]."""
+        slots, table) per sequence, in packing order).  x: float64 bf16 values [T, H].
+        ``trace`` (optional dict) receives the layer's materialised intermediates (n, q', k', v,
+        o, h, n2, a) for the layer-level parity tests' error bounds; it changes nothing."""
+        h = self.attention_half(l, x, batch, trace)                                # steps 4.1-4.6
+        return self.mlp_half(l, h, trace)                                            # steps 4.7-4.9
+
+    def attention_half(self, l: int, x: np.ndarray, batch, trace: dict | None = None) -> np.ndarray:
+        """Steps 4.1-4.6 of layer l: h = x + Attention(RMSNorm(x)) W_o^T (writes the batch's
+        K/V into the layer's pool)."""
         cfg, rnd, W = self.cfg, self.rnd, self.w.layer(l)
         nh, d, eps = cfg["n_heads"], cfg["head_dim"], cfg["rms_eps"]
         T = x.shape[0]
@@ -204,9 +212,19 @@ class Worker:
             o[t0:t0 + m] = rnd(np.einsum("htk,khd->thd", e, Vc) / e.sum(axis=-1).T[:, :, None])
             t0 += m
         h = rnd(x + self.lin(o.reshape(T, nh * d), W["wo"]))                          # step 4.6
-        n2 = rmsnorm(h, W["ffn_norm"], eps, rnd)                                    # step 4.7
+        if trace is not None:
+            trace.update(n=n, q=q, k=k, v=v, o=o, h=h)
+        return h
+
+    def mlp_half(self, l: int, h: np.ndarray, trace: dict | None = None) -> np.ndarray:
+        """Steps 4.7-4.9 of layer l: x' = h + (silu(n2 W_g^T) * (n2 W_u^T)) W_d^T, n2 = RMSNorm(h)."""
+        rnd, W = self.rnd, self.w.layer(l)
+        n2 = rmsnorm(h, W["ffn_norm"], self.cfg["rms_eps"], rnd)                    # step 4.7
         a = rnd(silu(self.lin(n2, W["wg"])) * self.lin(n2, W["wu"]))                    # step 4.8
-        return rnd(h + self.lin(a, W["wd"]))                                          # step 4.9
+        out = rnd(h + self.lin(a, W["wd"]))                                           # step 4.9
+        if trace is not None:
+            trace.update(n2=n2, a=a, out=out)
+        return out
 
     _exact_cache: dict = {}
 
@@ -316,3 +334,51 @@ class Group:
         self.workers = [tgt]
         self.ranges = [(0, cfg["n_layers"])]
         return wbytes, kvb
+
+    def scale_up(self, owner: dict):
+        """Scale up ("converting all cold-start workers into individual serving
+        endpoints"): every worker becomes a standalone endpoint holding the whole model; live
+        sequence s continues on endpoint owner[s], and its KV blocks of the layers that endpoint
+        did not hold are gathered from their owners at the same block ids.
+        Returns (endpoints, weight_bytes, kv_bytes): endpoint k is a one-worker Group whose block
+        manager holds only its sequences (the other blocks are free).  Consumes this group."""
+        cfg = self.cfg
+        L = cfg["n_layers"]
+        srcs = {l: self.owner(l) for l in range(L)}
+        live = sorted(self.bm.tables)
+        eps, wbytes, kvb = [], 0, 0
+        for k, wk in enumerate(self.workers):
+            have = set(wk.layers)
+            moved = [l for l in range(L) if l not in have]
+            wbytes += len(moved) * layer_param_bytes(cfg)
+            if not wk.is_first:
+                wbytes += embed_param_bytes(cfg)
+            if not wk.is_last:
+                wbytes += final_param_bytes(cfg)
+            mine = [sq for sq in live if owner[sq] == k]
+            e = Group.__new__(Group)
+            e.cfg, e.w, e.rnd, e.handoff_bytes = cfg, self.w, self.rnd, 0
+            e.ranges = [(0, L)]
+            ew = Worker(cfg, self.w, 0, L, wk.num_blocks, self.rnd)
+            ew.lin = wk.lin
+            for l in range(L):
+                if l in have:                          # its own layers: the pools as they are
+                    ew.kv[l] = wk.kv[l].copy()
+                else:                                  # pool_k[l][b] <- pool_owner(l)[l][b]
+                    for sq in mine:
+                        for blk in self.bm.tables[sq]:
+                            ew.kv[l][blk] = srcs[l].kv[l][blk]
+                            kvb += kv_block_bytes(cfg)
+            e.workers = [ew]
+            bm = BlockManager(wk.num_blocks)
+            used = set()
+            for sq in mine:
+                bm.tables[sq] = list(self.bm.tables[sq])
+                bm.ctx[sq] = self.bm.ctx[sq]
+                used |= set(bm.tables[sq])
+            bm.free = [b for b in range(wk.num_blocks) if b not in used]
+            heapq.heapify(bm.free)
+            e.bm = bm
+            eps.append(e)
+        self.workers = []
+        return eps, wbytes, kvb

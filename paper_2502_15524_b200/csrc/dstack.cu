@@ -66,6 +66,8 @@ struct DsParams {
   unsigned *c_rows, *c_norm;
   unsigned base_rows, base_norm;
   unsigned long long* trace;  // optional: [G][nl][16] globaltimer stamps (hs_debug_dstack_trace)
+  bf16* cap;                  // optional capture: layer l's h at cap + 2l * cap_stride, its output at (2l + 1)
+  long long cap_stride;
 };
 
 // trace slots per (CTA, layer)
@@ -562,7 +564,10 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
         for (int j = 0; j < NC; ++j) {
           const bf16 y = __float2bfloat16_rn(a[j] + r[j]);
           a[j] = n0 + j < p.N ? __bfloat162float(y) : 0.f;
-          if (n0 + j < p.N) out[(size_t)(n0 + j) * H + m] = y;
+          if (n0 + j < p.N) {
+            out[(size_t)(n0 + j) * H + m] = y;
+            if (p.cap) p.cap[(size_t)(2 * l + (k == 3 ? 1 : 0)) * p.cap_stride + (size_t)(n0 + j) * H + m] = y;
+          }
         }
         ds_ssq_chunk<NC>(a, n0, p.N, et, vals, p.ssq + (size_t)t * DS_MAXSEQ);
       }
@@ -1024,6 +1029,8 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
     p.ch = ch;
   }
   p.ws_attn = s->ws_attn;
+  p.cap = a.cap;
+  p.cap_stride = a.cap_stride;
   {
     static bool bo_set[64] = {};
     if (s->device < 64 && !bo_set[s->device]) {

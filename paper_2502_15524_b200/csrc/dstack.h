@@ -44,6 +44,11 @@ struct DstackArgs {
   const SeqDesc* seqs;
   const float2* rope;         // RoPE table [max_seq][hd/2] (cos, sin)
   const int* ctx;             // host copy: keys of each sequence after this step (pos0 + 1)
+  // test-only capture (hs_debug_capture): non-null => layer l of the range also stores its
+  // h = x + o W_o^T at cap + 2l * cap_stride and its output at cap + (2l + 1) * cap_stride
+  // ([N, H] bf16 rows each)
+  bf16* cap = nullptr;
+  int64_t cap_stride = 0;     // elements
 };
 
 // Per-stage persistent state (workspaces + flags); create once, reuse every step.

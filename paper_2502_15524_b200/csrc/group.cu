@@ -112,6 +112,7 @@ struct Stage {
   TmaMat ds_w[4];
   int ds_lb = -1, ds_le = -1;
   const void* ds_arena = nullptr;
+  bf16* cap = nullptr;  // test-only capture [2 n_layers + 1][max_tokens][hidden] (hs_debug_capture)
 
   uint8_t* wptr(uint64_t image_off) const { return arena + (image_off - arena_off0); }
   bf16* kv_pool(int l, uint64_t layer_bytes) const {
@@ -149,6 +150,12 @@ struct hs_group {
   std::set<int> free_blocks;
   std::map<int64_t, hs::SeqState> seqs;
   std::vector<int64_t> last_ids;  // seq order of the previous call (device token feedback)
+  // test-only layer-boundary capture (hs_debug_capture / hs_debug_read_hidden): buffer row of
+  // each token of the latest call (call order), and the stage that stored each boundary
+  int chunk_tokens = 0, max_chunks = 0;  // prefill micro-batching knobs (0 = defaults)
+  bool capture = false;
+  std::vector<int> cap_rowmap;
+  std::vector<int> cap_owner;
   unsigned epoch = 0;
   // per-kernel-kind event profile (hs_profile_*)
   bool prof_on = false;
@@ -241,7 +248,7 @@ static void free_stage(Stage& s, bool keep_exported = false) {
   if (s.owned) {
     if (!keep_exported) { F(s.arena); F(s.kv_mem); F(s.comm); }
     F(s.xa); F(s.xb); F(s.nrm); F(s.qkv); F(s.q); F(s.o);
-    F(s.act); F(s.fin); F(s.logits); F(s.ws); F(s.attn_ws); F(s.ctr); F(s.rope); F(s.d_meta); F(s.d_tok_out);
+    F(s.act); F(s.fin); F(s.cap); F(s.logits); F(s.ws); F(s.attn_ws); F(s.ctr); F(s.rope); F(s.d_meta); F(s.d_tok_out);
     if (s.h_meta) cudaFreeHost(s.h_meta);
     if (s.h_out) cudaFreeHost(s.h_out);
     if (s.ds) dstack_destroy(s.ds);
@@ -753,6 +760,11 @@ static hs_status run_dstack(hs_group* g, Stage& s, const CallMeta& m, const uint
   a.seqs = reinterpret_cast<const SeqDesc*>(meta + m.o_seqs);
   a.rope = s.rope;
   a.ctx = ctx.data();
+  if (g->capture && s.cap) {  // test-only: every layer's output rows (decode: one chunk, rows 0..N-1)
+    a.cap_stride = (int64_t)g->kv.max_tokens * c.hidden;
+    a.cap = s.cap + (size_t)(2 * s.lb + 1) * a.cap_stride;  // point 2 lb + 1: h of the range's first layer
+    for (int pt = 2 * s.lb + 1; pt <= 2 * s.le; ++pt) g->cap_owner[pt] = s.idx;
+  }
   {
     const double H = c.hidden, F = c.ffn;
     const double wbytes = (double)nl * 2.0 * (4 * H * H + 3 * F * H + 2 * H);
@@ -802,7 +814,9 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
       const char* e = getenv("HS_CHUNK_TOKENS");
       return e && atoi(e) > 0 ? atoi(e) : kChunkTokens;
     }();
-    nchunks = std::max(1, std::min<int>({kMaxChunks, min_len / 16, m0.T / chunk_tokens}));
+    const int ct = g->chunk_tokens > 0 ? g->chunk_tokens : chunk_tokens;
+    const int mc = g->max_chunks > 0 ? std::min(g->max_chunks, kMaxChunks) : kMaxChunks;
+    nchunks = std::max(1, std::min<int>({mc, min_len / 16, m0.T / ct}));
   }
   std::vector<int> dctx;  // decode: keys per sequence after this step (decode-stack item split)
   if (m0.decode)
@@ -836,6 +850,21 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
       off += align_up(m.bytes, 256);
       row += m.T;
     }
+  }
+  if (g->capture) {  // test-only: buffer row of every token of the call, in call order
+    std::vector<int> start(m0.n + 1, 0);
+    for (int i = 0; i < m0.n; ++i) start[i + 1] = start[i] + (m0.decode ? 1 : g->seqs[ids[i]].ctx);
+    g->cap_rowmap.assign(start[m0.n], 0);
+    for (int cidx = 0; cidx < nchunks; ++cidx) {
+      int qs = 0;
+      for (int i = 0; i < m0.n; ++i) {
+        const int n_new = m0.decode ? 1 : g->seqs[ids[i]].ctx;
+        const int b = (int)((int64_t)n_new * cidx / nchunks), e = (int)((int64_t)n_new * (cidx + 1) / nchunks);
+        for (int j = b; j < e; ++j) g->cap_rowmap[start[i] + j] = ch[cidx].row0 + qs + (j - b);
+        qs += e - b;
+      }
+    }
+    g->cap_owner.assign(2 * c.n_layers + 1, -1);
   }
   for (size_t ai = 0; ai < g->active.size(); ++ai) {
     const int k = g->active[ai];
@@ -921,6 +950,21 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
       launch_send(xrows(cidx), reinterpret_cast<uint8_t*>(nx->comm + g->cl.x_in) + (size_t)ch[cidx].row0 * H * 2,
                   (uint64_t)ch[cidx].m.T * H * 2, s.done(), nx->flag_x(), ep0 + cidx, kSendCtas, st);
     };
+    // test-only capture: point pt's rows of chunk cidx (pt = 2l: the input of layer l, 0 = the
+    // embedding rows, 2L = the last layer's output; pt = 2l + 1: layer l's h, which run_layer
+    // leaves in s.xb rows 0..T_c-1), on the compute stream right behind their producer
+    auto capture = [&](int pt, int cidx) -> hs_status {
+      if (!g->capture || !s.cap) return HS_OK;
+      const bf16* src = (pt & 1) ? s.xb : xrows(cidx);
+      HS_CUDA(cudaMemcpyAsync(s.cap + ((size_t)pt * g->kv.max_tokens + ch[cidx].row0) * H, src,
+                              (size_t)ch[cidx].m.T * H * 2, cudaMemcpyDeviceToDevice, st));
+      g->cap_owner[pt] = k;
+      return HS_OK;
+    };
+    auto capture_layer = [&](int l, int cidx) -> hs_status {
+      HS_TRY(capture(2 * l + 1, cidx));
+      return capture(2 * l + 2, cidx);
+    };
     bool normed = false, fin_done = false;
     // layer-major while this stage's weights are still arriving, chunk-major once resident
     const bool loading = nchunks > 1 && is_first && cudaEventQuery(s.ev_l1) == cudaErrorNotReady;
@@ -928,6 +972,7 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
     if (nchunks == 1 || !loading) {
       for (int cidx = 0; cidx < nchunks; ++cidx) {
         HS_TRY(stage_input(cidx));
+        if (is_first && s.lb == 0) HS_TRY(capture(0, cidx));
         normed = false;
         bool used = false;
         if (dec) {
@@ -941,17 +986,22 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
           if (dec && l + 1 == c.n_layers) HS_CUDA(cudaStreamWaitEvent(st, s.ev_final, 0));  // fused final norm
           const bf16* xin = (l == s.lb && !is_first) ? in_rows(cidx) : xrows(cidx);
           HS_TRY(run_layer(g, s, l, xin, xrows(cidx), ch[cidx].m, meta_of(cidx), normed, fin_done));
+          HS_TRY(capture_layer(l, cidx));
         }
         if (!is_last) hand_off(cidx);
       }
     } else {
-      for (int cidx = 0; cidx < nchunks; ++cidx) HS_TRY(stage_input(cidx));
+      for (int cidx = 0; cidx < nchunks; ++cidx) {
+        HS_TRY(stage_input(cidx));
+        if (is_first && s.lb == 0) HS_TRY(capture(0, cidx));
+      }
       for (int l = s.lb; l < s.le; ++l) {
         HS_CUDA(cudaStreamWaitEvent(st, s.ev_layer[l], 0));
         for (int cidx = 0; cidx < nchunks; ++cidx) {
           bool nrm = false, fd = false;
           const bf16* xin = (l == s.lb && !is_first) ? in_rows(cidx) : xrows(cidx);
           HS_TRY(run_layer(g, s, l, xin, xrows(cidx), ch[cidx].m, meta_of(cidx), nrm, fd));
+          HS_TRY(capture_layer(l, cidx));
           if (l + 1 == s.le && !is_last) hand_off(cidx);
         }
       }
@@ -1752,4 +1802,56 @@ extern "C" hs_status hs_load_background_async(hs_group* g, int32_t target_stage,
   if (std::find(g->active.begin(), g->active.end(), target_stage) == g->active.end())
     HS_FAIL(HS_E_INVAL, "stage %d is not active", target_stage);
   return load_background(g, target_stage, chunk_bytes);
+}
+
+extern "C" hs_status hs_debug_capture(hs_group* g, int32_t enable) {
+  if (!g) HS_FAIL(HS_E_INVAL, "null group");
+  const size_t bytes = (size_t)(2 * g->cfg.n_layers + 1) * g->kv.max_tokens * g->cfg.hidden * 2;
+  for (int k : g->active) {
+    Stage& s = g->st[k];
+    if (!s.owned) continue;
+    DeviceGuard dg(s.device);
+    if (enable && !s.cap) HS_ALLOC(s.cap, bytes);
+    if (!enable && s.cap) {
+      HS_CUDA(cudaDeviceSynchronize());
+      HS_CUDA(cudaFree(s.cap));
+      s.cap = nullptr;
+    }
+  }
+  g->capture = enable != 0;
+  g->cap_rowmap.clear();
+  g->cap_owner.clear();
+  return HS_OK;
+}
+
+extern "C" hs_status hs_debug_read_hidden(hs_group* g, int32_t boundary, int32_t row0, int32_t n_rows, void* host_out) {
+  if (!g || !host_out || n_rows < 0) HS_FAIL(HS_E_INVAL, "bad args");
+  if (!g->capture) HS_FAIL(HS_E_STATE, "capture is not enabled");
+  if (boundary < 0 || boundary > 2 * g->cfg.n_layers || boundary >= (int)g->cap_owner.size())
+    HS_FAIL(HS_E_INVAL, "bad boundary %d", boundary);
+  if (row0 < 0 || row0 + n_rows > (int)g->cap_rowmap.size()) HS_FAIL(HS_E_INVAL, "rows outside the latest call");
+  const int k = g->cap_owner[boundary];
+  if (k < 0 || k >= (int)g->st.size() || !g->st[k].owned || !g->st[k].cap)
+    HS_FAIL(HS_E_INVAL, "boundary %d was not captured by this process in the latest call", boundary);
+  Stage& s = g->st[k];
+  DeviceGuard dg(s.device);
+  HS_CUDA(cudaStreamSynchronize(s.comp));
+  const size_t H = g->cfg.hidden;
+  const bf16* base = s.cap + (size_t)boundary * g->kv.max_tokens * H;
+  uint8_t* out = static_cast<uint8_t*>(host_out);
+  for (int r = row0; r < row0 + n_rows;) {  // contiguous runs of buffer rows
+    int e = r + 1;
+    while (e < row0 + n_rows && g->cap_rowmap[e] == g->cap_rowmap[e - 1] + 1) ++e;
+    HS_CUDA(cudaMemcpy(out + (size_t)(r - row0) * H * 2, base + (size_t)g->cap_rowmap[r] * H, (size_t)(e - r) * H * 2,
+                       cudaMemcpyDeviceToHost));
+    r = e;
+  }
+  return HS_OK;
+}
+
+extern "C" hs_status hs_debug_set_prefill_chunking(hs_group* g, int32_t min_chunk_tokens, int32_t max_chunks) {
+  if (!g || min_chunk_tokens < 0 || max_chunks < 0) HS_FAIL(HS_E_INVAL, "bad args");
+  g->chunk_tokens = min_chunk_tokens;
+  g->max_chunks = max_chunks;
+  return HS_OK;
 }

@@ -117,7 +117,8 @@ SYMBOLS = ["hs_image_layout", "hs_plan_stages", "hs_predict_ttft_eq1", "hs_predi
            "hs_k_gemm", "hs_k_rmsnorm", "hs_k_rope_kv", "hs_k_attention", "hs_k_argmax", "hs_k_embed",
            "hs_k_span_copy", "hs_debug_gemm_trace", "hs_debug_dstack_trace", "hs_plan_auto", "hs_links_create", "hs_links_admit",
            "hs_links_settle", "hs_links_complete", "hs_links_pending", "hs_links_destroy",
-           "hs_load_background_async", "hs_scale_up", "hs_release_peer_memory"]
+           "hs_load_background_async", "hs_scale_up", "hs_release_peer_memory", "hs_debug_capture",
+           "hs_debug_read_hidden", "hs_debug_set_prefill_chunking"]
 
 _lib = None
 
@@ -179,6 +180,9 @@ def lib():
     L.hs_links_destroy.argtypes = [VP]
     L.hs_load_background_async.argtypes = [VP, I32, U64]
     L.hs_scale_up.argtypes = [VP, P(I32), I32, P(VP), P(ConsolidateStats)]
+    L.hs_debug_capture.argtypes = [VP, I32]
+    L.hs_debug_read_hidden.argtypes = [VP, I32, I32, I32, VP]
+    L.hs_debug_set_prefill_chunking.argtypes = [VP, I32, I32]
     _lib = L
     return L
 
@@ -421,6 +425,21 @@ class Group:
         out = np.zeros((n, 2, self.cfg["n_heads"], self.cfg["head_dim"]), dtype=np.uint16)
         check(lib().hs_debug_read_kv(self.h, seq_id, layer, pos0, n, out.ctypes.data))
         return out
+
+    def capture(self, on: bool = True):
+        """Test-only: store every layer boundary's hidden rows of later calls (hs_debug_capture)."""
+        check(lib().hs_debug_capture(self.h, 1 if on else 0))
+
+    def read_hidden(self, boundary: int, row0: int = 0, n: int | None = None) -> np.ndarray:
+        """bf16 bits [n, hidden] of layer boundary `boundary` of the latest call, call order."""
+        if n is None:
+            raise ValueError("pass the number of rows")
+        out = np.zeros((n, self.cfg["hidden"]), dtype=np.uint16)
+        check(lib().hs_debug_read_hidden(self.h, boundary, row0, n, out.ctypes.data))
+        return out
+
+    def set_prefill_chunking(self, min_chunk_tokens: int = 0, max_chunks: int = 0):
+        check(lib().hs_debug_set_prefill_chunking(self.h, min_chunk_tokens, max_chunks))
 
     def read_weights(self, stage: int, off: int, nbytes: int) -> np.ndarray:
         out = np.empty(nbytes, dtype=np.uint8)

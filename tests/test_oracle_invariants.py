@@ -141,3 +141,41 @@ def test_config4_kv_bytes_formula():
     cfg = hsgen.CONFIGS["llama2-13b"]
     kv_per_block = BLOCK * 2 * cfg["hidden"] * 2
     assert 16 * (576 // BLOCK) * kv_per_block * 30 == 5_662_310_400
+
+
+@pytest.mark.parametrize("pp", [2, 4])
+def test_scale_up_endpoints_bitwise_and_bytes(tiny_cfg, W, pp):
+    """Scale-up (PAPER.md:608-612): after 8 pipelined steps every worker becomes an endpoint;
+    each sequence then decodes on its endpoint bitwise equal to the unpartitioned run (its KV of
+    every layer is the single-worker KV); bytes: each endpoint receives the
+    model minus its own slice ((s-1) x model in total) and, for every layer it lacked, the used
+    blocks of its own sequences."""
+    cfg = tiny_cfg
+    prompts = hsgen.prompts(3, 32, cfg["vocab"])
+    g1, h1 = run(cfg, W, 1, prompts, 12)
+    g = Group(cfg, W, pp=pp, num_blocks=64)
+    ids = [0, 1, 2]
+    toks, _ = g.prefill(ids, prompts)
+    for _ in range(8):
+        toks, _ = g.decode(ids, toks)
+    layers_of = [list(wk.layers) for wk in g.workers]
+    owner = {0: 0, 1: pp - 1, 2: 1}
+    eps, wb, kvb = g.scale_up(owner)
+    model = cfg["n_layers"] * layer_param_bytes(cfg) + embed_param_bytes(cfg) + final_param_bytes(cfg)
+    assert wb == (pp - 1) * model
+    ctx = 32 + 8
+    blocks = (ctx + BLOCK - 1) // BLOCK
+    assert kvb == sum(blocks * BLOCK * 2 * cfg["hidden"] * 2 * (cfg["n_layers"] - len(layers_of[owner[s]])) for s in ids)
+    assert len(eps) == pp
+    for s in ids:
+        e = eps[owner[s]]
+        assert sorted(e.bm.tables) == sorted(x for x in ids if owner[x] == owner[s])
+        for layer in range(cfg["n_layers"]):
+            assert np.array_equal(e.read_kv(s, layer, 0, ctx), g1.read_kv(s, layer, 0, ctx))
+    for step in range(4):  # each endpoint continues its sequences == the unpartitioned run
+        t1, l1 = h1[9 + step]
+        for s in ids:
+            e = eps[owner[s]]
+            t, lg = e.decode([s], [toks[s]])
+            assert t[0] == t1[s] and np.array_equal(lg[0], l1[s])
+        toks = list(t1)
