@@ -30,10 +30,6 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "cold-start TTFT (s) and decode tok/s at PP=1/2/4/8; consolidation GB/s vs NVLink"
-PCIE_H2D_GBS = 55.6        # measured per GPU in isolation (profiles/r01_links_measured.json)
-# (a first probe that read ONE shared pinned buffer from 4 GPUs saw 115 GB/s in total; with a
-# buffer per GPU, as here, PP=4 loads reach 209 GB/s: links are independent, so the
-# aggregate peak is N x the isolated per-link figure)
 NVLINK_GBS = 900.0         # nominal per direction per GPU (north star); measured P2P 770
 PROFILE_STEPS = int(os.environ.get("HS_PROFILE_STEPS", "8"))  # decode steps per timed step under the event profile
 
@@ -136,7 +132,22 @@ def run_ours(args):
     if cfgn == 4 and world == 1:
         pp = 1
     hdr = hs.image_layout(cfg)
-    gpus = [dict(device=i, h2d_gbps=PCIE_H2D_GBS, free_bytes=torch.cuda.mem_get_info(local)[1]) for i in range(pp)]
+
+    def gather(v):
+        if not dist:
+            return [v]
+        t = torch.tensor([float(v)], dtype=torch.float64, device="cuda")
+        out = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(out, t)
+        return [x.item() for x in out]
+
+    # host->device link of every stage GPU, measured here from a 1 GiB pinned buffer: alone (one
+    # rank at a time: p_i of Eq. 1/5, the load roofline's per-link peak) and all at once (shared
+    # uplinks show up as a lower concurrent sum)
+    iso_gbs, conc_gbs = link_probe(torch, dist, rank, world)
+    p_iso = gather(iso_gbs)
+    gpus = [dict(device=i, h2d_gbps=p_iso[i] if world > 1 else iso_gbs, free_bytes=torch.cuda.mem_get_info(local)[1])
+            for i in range(pp)]
     plan = hs.plan_stages(cfg, gpus, pp, pp if args.scale_up else 1)
     for k in range(pp):
         plan.device[k] = k if world > 1 else local
@@ -253,24 +264,6 @@ def run_ours(args):
                     g.release_seq(i)
         return r
 
-    # this box's concurrent H2D capability with every rank copying at once from its own pinned
-    # buffer (some boxes share PCIe uplinks between GPUs: the measured aggregate, not N x one
-    # link, is the load roofline's denominator)
-    probe = min(1 << 30, img.buf.numel())
-    scratch = torch.empty(probe, dtype=torch.uint8, device="cuda")
-    for _ in range(2):
-        scratch.copy_(img.buf[:probe], non_blocking=True)
-    best = 1e9
-    for _ in range(3):
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        scratch.copy_(img.buf[:probe], non_blocking=True)
-        e1.record()
-        e1.synchronize()
-        best = min(best, e0.elapsed_time(e1) / 1e3)
-    del scratch
-    h2d_rank_gbs = probe / best / 1e9
     for _ in range(args.warmup):
         one_step(False)
     clocks = Clocks(os.path.join(ROOT, "gpurun_out", f"clocks_r{rank}.csv")) if rank == 0 else None
@@ -306,7 +299,8 @@ def run_ours(args):
     dec_dev = agg_max(med("decode_dev"))
     dec_host = agg_max(med("decode_host"))
     launches = int(agg_sum(launches))
-    h2d_concurrent = agg_sum(h2d_rank_gbs)
+    h2d_concurrent = agg_sum(conc_gbs)
+    h2d_isolated_sum = agg_sum(iso_gbs)
     # per-kind profile (this rank) -> dominant decode GEMM
     prof = {}
     for s in steps:
@@ -347,7 +341,7 @@ def run_ours(args):
     pre_gemm = [v for k, v in prof.items() if k.startswith("gemm_") and k.endswith(".prefill")]
     out = None
     if rank == 0:
-        agg_link = PCIE_H2D_GBS * pp
+        agg_link = h2d_isolated_sum
         load_gbs = loaded / (load_ms / 1e3) / 1e9
         out = {
             "metric": METRIC, "value": round(ttft_dev, 5), "unit": "s", "n_gpus": world, "steps": args.steps,
@@ -366,7 +360,8 @@ def run_ours(args):
                      "per_step_device_s": [round(s["ttft_dev"], 5) for s in steps]},
             "load": {"bytes_per_stage_max": max(pd["stage_bytes"]), "bytes_total": int(loaded),
                      "stage_load_ms_max": round(load_ms, 2), "achieved_gbs": round(load_gbs, 2),
-                     "peak_gbs_isolated_sum": round(PCIE_H2D_GBS * pp, 1),
+                     "peak_gbs_isolated_sum": round(agg_link, 1),
+                     "peak_gbs_isolated_per_gpu": [round(x, 1) for x in p_iso],
                      "frac_of_isolated_sum": round(load_gbs / agg_link, 4),
                      "peak_gbs_measured_concurrent": round(h2d_concurrent, 1),
                      "frac_of_measured_concurrent": round(load_gbs / h2d_concurrent, 4)},
@@ -400,6 +395,25 @@ def run_ours(args):
                                     "pause_s": round(statistics.median(s["cons_pause"] for s in steps), 4)}
             out["decode"]["after_consolidation_tok_s_device"] = round(
                 n_seqs * dsteps / statistics.median(s["decode2_dev"] for s in steps), 2)
+        # every part of the path against its own roofline (the "roofline" key above is the
+        # dominant kernel, the decode stack): load / PCIe, prefill GEMMs / tensor, decode / HBM,
+        # consolidation / NVLink
+        pre_ms = sum(v["ms"] for v in pre_gemm)
+        pre_tf = sum(v["flops"] for v in pre_gemm) / max(1e-12, pre_ms / 1e3) / 1e12
+        rl = [{"part": "load (a3)", "bound": "pcie", "achieved": round(load_gbs, 2), "unit": "GB/s",
+               "peak": round(agg_link, 1), "frac": round(load_gbs / agg_link, 4),
+               "peak_source": f"sum over the {pp} stage GPUs of the isolated pinned-H2D probe in this run"},
+              {"part": "prefill GEMMs (a7, a10-a12, a14), warm", "bound": "tensor", "achieved": round(pre_tf, 1),
+               "unit": "TFLOP/s", "peak": pk.get("bf16_tflops"), "frac": round(pre_tf / pk.get("bf16_tflops", 1659.3), 4),
+               "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst: a prefill is a few ms)"},
+              {"part": "decode stack (a16)", "bound": "hbm", "achieved": roof["achieved"], "unit": "GB/s",
+               "peak": roof["peak"], "frac": roof["frac"], "peak_source": roof["peak_source"]}]
+        if consolidate:
+            cgbs = statistics.median(s["cons_bytes"] for s in steps) / statistics.median(s["cons_s"] for s in steps) / 1e9
+            rl.append({"part": "consolidation (a17)", "bound": "nvlink", "achieved": round(cgbs, 1), "unit": "GB/s",
+                       "peak": NVLINK_GBS, "frac": round(cgbs / NVLINK_GBS, 4),
+                       "peak_source": "NVLink 5 nominal per direction (target ingress)"})
+        out["rooflines"] = rl
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(cfg, plen, n_seqs)
         print(json.dumps(out), flush=True)
@@ -409,12 +423,45 @@ def run_ours(args):
     return out
 
 
-def oracle_ttft_sample(cfg, plen, n_seqs, layers=1):
-    """The oracle as it stands: prefill of the real prompt through `layers` decoder layers +
-    embedding + final norm/lm_head, extrapolated linearly to all layers.  Weights are drawn
-    before the timer (input generation is not the oracle's work)."""
-    import numpy as np
+def link_probe(torch, dist, rank, world, nbytes=1 << 30):
+    """Pinned host -> HBM copy bandwidth of this rank's GPU (GB/s): isolated (the ranks take
+    turns) and concurrent (all at once); best of 3 each, CUDA events on the copy."""
+    src = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    src.fill_(1)
+    dst = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
 
+    def timed():
+        best = 1e9
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dst.copy_(src, non_blocking=True)
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1) / 1e3)
+        return nbytes / best / 1e9
+
+    dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    iso = 0.0
+    for r in range(world):
+        if dist:
+            dist.barrier()
+        if r == rank:
+            iso = timed()
+    if dist:
+        dist.barrier()
+    conc = timed()
+    del src, dst
+    return iso, conc
+
+
+def oracle_sample(cfg, plen, n_seqs, decode_steps=4, layers=1):
+    """The oracle as it stands, on a bounded sample of the workload: the real prompt(s) through
+    `layers` decoder layers (+ embedding, final norm, lm_head), then `decode_steps` cached decode
+    steps; per-layer times extrapolated linearly to all layers.  Weights are drawn before the
+    timer (input generation is not the oracle's work).  Returns (prefill_s, decode_s_per_step,
+    sampled seconds)."""
     import hsgen
     from oracle.decoder import Group, Weights
     W = Weights(cfg, cache=True)
@@ -425,11 +472,35 @@ def oracle_ttft_sample(cfg, plen, n_seqs, layers=1):
     W.lm_head()
     W.final_norm()
     prompts = hsgen.prompts(n_seqs, plen, cfg["vocab"])
-    g = Group(sub, W, pp=1, num_blocks=n_seqs * (plen // 16 + 2))
+    ids = list(range(n_seqs))
+    g = Group(sub, W, pp=1, num_blocks=n_seqs * ((plen + decode_steps) // 16 + 2))
     t0 = time.perf_counter()
-    g.prefill(list(range(n_seqs)), prompts)
-    t = time.perf_counter() - t0
-    return t * cfg["n_layers"] / layers, t
+    toks, _ = g.prefill(ids, prompts)
+    t_pre = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    for _ in range(decode_steps):
+        toks, _ = g.decode(ids, toks)
+    t_dec = (time.perf_counter() - t1) / max(1, decode_steps)
+    L = cfg["n_layers"]
+    return t_pre * L / layers, t_dec * L / layers, t_pre + t_dec * decode_steps
+
+
+def oracle_copy_gbs(nbytes=1 << 30, piece=None):
+    """The oracle's load and consolidation are byte copies: host memcpy
+    bandwidth of numpy copies, whole (load: a stage slice) or in KV-block pieces."""
+    import numpy as np
+    src = np.ones(nbytes, dtype=np.uint8)
+    dst = np.empty_like(src)
+    best = 1e9
+    for _ in range(3):
+        t0 = time.perf_counter()
+        if piece:
+            for o in range(0, nbytes, piece):
+                dst[o:o + piece] = src[o:o + piece]
+        else:
+            np.copyto(dst, src)
+        best = min(best, time.perf_counter() - t0)
+    return nbytes / best / 1e9
 
 
 def cpu_cores():
@@ -440,31 +511,47 @@ def cpu_cores():
 
 
 def cpu_baseline(cfg, plen, n_seqs):
-    est, t = oracle_ttft_sample(cfg, plen, n_seqs, 1)
-    return {"value": round(est, 3), "unit": "s", "cores": cpu_cores(), "kind": "oracle",
-            "sample": f"numpy-fp64 oracle prefill of the {n_seqs}x{plen}-token prompt through 1 of "
-                      f"{cfg['n_layers']} layers (+ embedding, lm_head) in {t:.2f} s, extrapolated x{cfg['n_layers']}; "
-                      "weights resident (no load term)"}
+    """CPU oracle on this host (SURVEY §8(d) "CPU oracle beside it"): TTFT-equivalent = load
+    (memcpy of the model image at the oracle's copy bandwidth) + prefill; decode s/token;
+    consolidation copy GB/s (KV-block pieces)."""
+    import hsgen
+    pre, dec, sampled = oracle_sample(cfg, plen, n_seqs)
+    load_gbs = oracle_copy_gbs()
+    kv_block = 16 * 2 * cfg["hidden"] * 2
+    cons_gbs = oracle_copy_gbs(piece=kv_block)
+    img = hsgen.image_header(cfg).param_bytes
+    ttft = img / (load_gbs * 1e9) + pre
+    return {"value": round(ttft, 3), "unit": "s", "cores": cpu_cores(), "kind": "oracle",
+            "prefill_s": round(pre, 3), "load_s": round(img / (load_gbs * 1e9), 3), "load_gbs": round(load_gbs, 2),
+            "decode_s_per_token": round(dec / n_seqs, 4), "decode_tok_s": round(n_seqs / dec, 3),
+            "consolidation_copy_gbs": round(cons_gbs, 2),
+            "sample": f"numpy-fp64 oracle: the {n_seqs}x{plen}-token prefill and 4 cached decode steps through 1 of "
+                      f"{cfg['n_layers']} layers (+ embedding, lm_head) in {sampled:.2f} s, extrapolated x{cfg['n_layers']}; "
+                      f"load = {img / 1e9:.2f} GB image at the measured numpy copy bandwidth (1 GiB sample); "
+                      f"consolidation copy = 1 GiB in {kv_block // 1024} KiB KV-block pieces; value = load + prefill"}
 
 
 def run_reference(args):
+    """--impl reference: the CPU oracle as it stands on this host, the same workload and metric
+    (TTFT-equivalent: image load at the oracle's copy bandwidth + prefill), each step a bounded
+    sample (cpu_baseline).  Under torchrun only rank 0 works."""
     rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
     if rank != 0:
         return
     cfgn, model, cfg, n_seqs, plen, dsteps = workload(args, world)
-    vals = []
+    vals, last = [], None
     for i in range(args.warmup + args.steps):
-        est, t = oracle_ttft_sample(cfg, plen, n_seqs, 1)
+        last = cpu_baseline(cfg, plen, n_seqs)
         if i >= args.warmup:
-            vals.append(est)
+            vals.append(last["value"])
     v = statistics.median(vals)
-    samp = (f"numpy-fp64 oracle prefill of {n_seqs}x{plen} tokens through 1 of {cfg['n_layers']} layers per step, "
-            f"extrapolated x{cfg['n_layers']}")
+    cb = dict(last)
+    cb["value"] = round(v, 3)
     out = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "higher_is_better": False, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"config {cfgn}: {model}, {n_seqs}x{plen}-token prompt (oracle TTFT, no load)"},
-           "cpu_baseline": {"value": round(v, 3), "unit": "s", "cores": cpu_cores(), "kind": "oracle", "sample": samp},
+           "config": {"workload": f"config {cfgn}: {model}, {n_seqs}x{plen}-token prompt (oracle TTFT-equivalent)"},
+           "cpu_baseline": cb,
            "e2e": {"value": round(v, 3), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 

@@ -113,6 +113,13 @@ struct Stage {
   int ds_lb = -1, ds_le = -1;
   const void* ds_arena = nullptr;
   bf16* cap = nullptr;  // test-only capture [2 n_layers + 1][max_tokens][hidden] (hs_debug_capture)
+  // consolidation copy list of a full-memory stage (a possible target), prepared before T0:
+  // [0, cons_nw) the weight slices of every other stage (pieces, prebuilt at create),
+  // [cons_nw, ...) the used KV blocks of the live sequences (written at the call)
+  CopyDesc* cons_d = nullptr;  // device
+  CopyDesc* cons_h = nullptr;  // pinned staging
+  int cons_cap = 0, cons_nw = 0;
+  cudaEvent_t ev_cons0 = nullptr, ev_cons1 = nullptr;
 
   uint8_t* wptr(uint64_t image_off) const { return arena + (image_off - arena_off0); }
   bf16* kv_pool(int l, uint64_t layer_bytes) const {
@@ -249,6 +256,9 @@ static void free_stage(Stage& s, bool keep_exported = false) {
     if (!keep_exported) { F(s.arena); F(s.kv_mem); F(s.comm); }
     F(s.xa); F(s.xb); F(s.nrm); F(s.qkv); F(s.q); F(s.o);
     F(s.act); F(s.fin); F(s.cap); F(s.logits); F(s.ws); F(s.attn_ws); F(s.ctr); F(s.rope); F(s.d_meta); F(s.d_tok_out);
+    F(s.cons_d);
+    if (s.cons_h) cudaFreeHost(s.cons_h);
+    for (auto e : {s.ev_cons0, s.ev_cons1}) if (e) cudaEventDestroy(e);
     if (s.h_meta) cudaFreeHost(s.h_meta);
     if (s.h_out) cudaFreeHost(s.h_out);
     if (s.ds) dstack_destroy(s.ds);
@@ -390,6 +400,42 @@ static hs_status validate_image(hs_group* g, const hs_image* im, uint64_t b, uin
 
 // ------------------------------------------------------------------ create ---------------
 static hs_status open_peer_memory(hs_group* g, Stage& s);
+static hs_status add_copy(std::vector<CopyDesc>& list, uint64_t src, uint64_t dst, uint64_t bytes, uint64_t piece);
+
+static uint64_t cons_piece() {
+  static const uint64_t piece = [] {
+    const char* e = getenv("HS_CONS_PIECE_KB");
+    return (e && atoi(e) > 0 ? (uint64_t)atoi(e) : 1024ull) << 10;
+  }();
+  return piece;
+}
+
+// Prepares the consolidation of the group into full-memory stage T before T0:
+// the copy list's weight part (every other stage's slice, in pieces) is built and uploaded once,
+// and room for the KV part (at most every block of every layer) is reserved on the device and in
+// pinned staging, so the consolidation pause does no allocation, no upload of the weight list
+// and no driver call besides one small H2D of the KV descriptors.  Needs every peer arena mapped.
+static hs_status prepare_consolidation(hs_group* g, Stage& T) {
+  if (!T.owned || !T.full_memory || T.cons_d) return HS_OK;
+  std::vector<CopyDesc> list;
+  for (int k : g->active) {
+    if (k == T.idx) continue;
+    Stage& S = g->st[k];
+    if (!S.arena) return HS_OK;  // peer arena not mapped yet (HS_CONS_LATE_OPEN): at the call
+    HS_TRY(add_copy(list, reinterpret_cast<uint64_t>(S.arena + (S.slice_begin - S.arena_off0)),
+                    reinterpret_cast<uint64_t>(T.wptr(S.slice_begin)), S.slice_end - S.slice_begin, cons_piece()));
+  }
+  DeviceGuard dg(T.device);
+  T.cons_nw = (int)list.size();
+  T.cons_cap = T.cons_nw + g->kv.num_blocks * g->cfg.n_layers;
+  HS_CUDA(cudaMalloc(reinterpret_cast<void**>(&T.cons_d), (size_t)T.cons_cap * sizeof(CopyDesc)));
+  HS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&T.cons_h), (size_t)T.cons_cap * sizeof(CopyDesc), cudaHostAllocPortable));
+  if (!list.empty())
+    HS_CUDA(cudaMemcpy(T.cons_d, list.data(), list.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
+  HS_CUDA(cudaEventCreate(&T.ev_cons0));
+  HS_CUDA(cudaEventCreate(&T.ev_cons1));
+  return HS_OK;
+}
 
 static hs_status create(const hs_model_cfg* cfg, const hs_plan* plan, const hs_image* image,
                         const hs_image* stage_images, const hs_kv_cfg* kv, const hs_comm* comm,
@@ -506,8 +552,9 @@ static hs_status create(const hs_model_cfg* cfg, const hs_plan* plan, const hs_i
     if (me.full_memory && !late_open)
       for (int k = 0; k < pp; ++k)
         if (k != g->owned_stage) HS_TRY(open_peer_memory(g.get(), g->st[k]));
-    if (g->comm.barrier(g->comm.ctx) != 0) HS_FAIL(HS_E_STATE, "barrier failed");
+    if (!comm_barrier(g.get())) HS_FAIL(HS_E_STATE, "barrier failed");
   }
+  for (int k = 0; k < pp; ++k) HS_TRY(prepare_consolidation(g.get(), g->st[k]));
   *out = g.release();
   return HS_OK;
 }
@@ -1219,14 +1266,21 @@ static hs_status add_copy(std::vector<CopyDesc>& list, uint64_t src, uint64_t ds
 }
 
 static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
-  const auto t_enter = std::chrono::steady_clock::now();
+  using clk = std::chrono::steady_clock;
+  const auto t_enter = clk::now();
   if (g->dead) HS_FAIL(HS_E_CUDA, "group is dead");
   if (tgt < 0 || tgt >= (int)g->st.size() || std::find(g->active.begin(), g->active.end(), tgt) == g->active.end())
     HS_FAIL(HS_E_INVAL, "target stage %d is not active", tgt);
   if (!g->st[tgt].full_memory) HS_FAIL(HS_E_INVAL, "target stage %d is not a full-memory worker", tgt);
   const hs_model_cfg& c = g->cfg;
   hs_consolidate_stats stats{};
-  // 1. drain: "stop scheduling ... wait for all on-the-fly batches"
+  // 1. drain: "stop scheduling ... wait for all on-the-fly batches".  Only this
+  //    process's streams: no cross-rank barrier is needed in SPMD mode, because the previous call
+  //    returned on every rank only after the last stage's token broadcast, and each stage hands
+  //    off (release, system scope) only after all its layers (KV writes included) completed, so
+  //    every source's KV and weights are final and visible before the target's copy starts; and
+  //    the released memory is freed only at hs_release_peer_memory / destroy, behind a barrier
+  //    that the target reaches after its copy.
   for (int k : g->active) {
     Stage& s = g->st[k];
     if (!s.owned) continue;
@@ -1234,86 +1288,63 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
     HS_CUDA(cudaStreamSynchronize(s.comp));
     HS_CUDA(cudaStreamSynchronize(s.copy));
   }
-  if (!comm_barrier(g)) HS_FAIL(HS_E_STATE, "barrier failed");
-  const auto t_drained = std::chrono::steady_clock::now();
-  auto t_copied = t_drained, t_listed = t_drained, t_synced = t_drained;
+  const auto t_drained = clk::now();
+  auto t_listed = t_drained, t_copied = t_drained;
   Stage& T = g->st[tgt];
   if (T.owned) {
     DeviceGuard dg(T.device);
     cudaSetDevice(T.device);
-    // the target must have its own slice resident before it takes over
-    HS_CUDA(cudaStreamSynchronize(T.copy));
     cudaStream_t s2 = T.comp;
-    cudaEvent_t e0, e1, e2;
-    HS_CUDA(cudaEventCreate(&e0));
-    HS_CUDA(cudaEventCreate(&e1));
-    HS_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
     // 2. one copy list, pulled over NVLink by the target's SMs (16-byte loads, many in flight):
-    //    (a) the weight regions the target lacks (each owner's stage slice), (b) the used KV
-    //    blocks of every live sequence for those layers, placed at the same block ids ("collect
-    //    these blocks from all workers with a gather operation ... placed at different layers,
-    //    according to which worker it comes from")
-    static const uint64_t piece = [] {
-      const char* e = getenv("HS_CONS_PIECE_KB");
-      return (e && atoi(e) > 0 ? (uint64_t)atoi(e) : 1024ull) << 10;
-    }();
-    std::vector<CopyDesc> list;
-    auto add = [&](uint64_t src, uint64_t dst, uint64_t bytes) -> hs_status {
-      return add_copy(list, src, dst, bytes, piece);
-    };
+    //    (a) the weight regions the target lacks (each owner's stage slice; prebuilt at create),
+    //    (b) the used KV blocks of every live sequence for those layers, placed at the same block
+    //    ids ("collect these blocks from all workers with a gather operation ... placed at
+    //    different layers, according to which worker it comes from")
+    for (int k : g->active)
+      if (k != tgt) HS_TRY(open_peer_memory(g, g->st[k]));
+    HS_TRY(prepare_consolidation(g, T));
+    std::vector<CopyDesc> kv;
+    kv.reserve((size_t)g->kv.num_blocks * c.n_layers);
     for (int k : g->active) {
       if (k == tgt) continue;
       Stage& S = g->st[k];
-      HS_TRY(open_peer_memory(g, S));
-      if (T.bg_issued) continue;  // the weights come over the target's own PCIe link
-      HS_TRY(add(reinterpret_cast<uint64_t>(S.arena + (S.slice_begin - S.arena_off0)),
-                 reinterpret_cast<uint64_t>(T.wptr(S.slice_begin)), S.slice_end - S.slice_begin));
-      stats.weight_bytes += g->plan.stage_bytes[k];
+      if (!T.bg_issued) stats.weight_bytes += g->plan.stage_bytes[k];
+      for (int l = S.lb; l < S.le; ++l)
+        for (auto& kvp : g->seqs)
+          for (int b : kvp.second.blocks) {
+            HS_TRY(add_copy(kv, reinterpret_cast<uint64_t>(S.kv_pool(l, g->kv_layer_bytes)) + (uint64_t)b * g->kv_block_bytes,
+                            reinterpret_cast<uint64_t>(T.kv_pool(l, g->kv_layer_bytes)) + (uint64_t)b * g->kv_block_bytes,
+                            g->kv_block_bytes, g->kv_block_bytes));
+            stats.kv_bytes += g->kv_block_bytes;
+          }
     }
+    if ((int)kv.size() > T.cons_cap - T.cons_nw) HS_FAIL(HS_E_INVAL, "consolidation list overflow");
+    if (!kv.empty()) {
+      memcpy(T.cons_h + T.cons_nw, kv.data(), kv.size() * sizeof(CopyDesc));
+      HS_CUDA(cudaMemcpyAsync(T.cons_d + T.cons_nw, T.cons_h + T.cons_nw, kv.size() * sizeof(CopyDesc),
+                              cudaMemcpyHostToDevice, s2));
+    }
+    // with the background host path the weights came over the target's own PCIe link: only KV
+    const int first = T.bg_issued ? T.cons_nw : 0;
+    const int n = T.cons_nw + (int)kv.size() - first;
     if (T.bg_issued) {
       HS_CUDA(cudaStreamWaitEvent(s2, T.ev_bg, 0));  // background host-path load must be complete
       stats.weight_bytes_host = T.bg_bytes;
     }
-    for (int k : g->active) {
-      if (k == tgt) continue;
-      Stage& S = g->st[k];
-      for (int l = S.lb; l < S.le; ++l)
-        for (auto& kvp : g->seqs)
-          for (int b : kvp.second.blocks) {
-            HS_TRY(add(reinterpret_cast<uint64_t>(S.kv_pool(l, g->kv_layer_bytes)) + (uint64_t)b * g->kv_block_bytes,
-                       reinterpret_cast<uint64_t>(T.kv_pool(l, g->kv_layer_bytes)) + (uint64_t)b * g->kv_block_bytes,
-                       g->kv_block_bytes));
-            stats.kv_bytes += g->kv_block_bytes;
-          }
-    }
-    CopyDesc* d_list = nullptr;
-    if (!list.empty()) {
-      HS_CUDA(cudaMalloc(&d_list, list.size() * sizeof(CopyDesc)));
-      HS_CUDA(cudaMemcpy(d_list, list.data(), list.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice));
-    }
-    t_listed = std::chrono::steady_clock::now();
+    t_listed = clk::now();
     if (getenv("HS_DEBUG_CONS_SYNC")) {
       cudaError_t pe = cudaDeviceSynchronize();
       if (pe != cudaSuccess) HS_FAIL(HS_E_CUDA, "consolidate: fault before the copy list: %s", cudaGetErrorString(pe));
-      for (auto& d : list) {
-        cudaPointerAttributes at{};
-        if (cudaPointerGetAttributes(&at, reinterpret_cast<void*>(d.src)) != cudaSuccess || at.devicePointer == nullptr)
-          HS_FAIL(HS_E_CUDA, "consolidate: unmapped source 0x%llx", (unsigned long long)d.src);
-      }
     }
-    HS_CUDA(cudaEventRecord(e0, s2));
-    launch_copy_list(d_list, (int)list.size(), 8 * num_sms(T.device), s2);
-    HS_CUDA(cudaEventRecord(e1, s2));
-    HS_CUDA(cudaEventSynchronize(e1));
+    HS_CUDA(cudaEventRecord(T.ev_cons0, s2));
+    launch_copy_list(T.cons_d + first, n, 8 * num_sms(T.device), s2);
+    HS_CUDA(cudaEventRecord(T.ev_cons1, s2));
+    HS_CUDA(cudaEventSynchronize(T.ev_cons1));
     float ms = 0;
-    HS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    HS_CUDA(cudaEventElapsedTime(&ms, T.ev_cons0, T.ev_cons1));
     stats.seconds = ms / 1e3;
-    t_synced = std::chrono::steady_clock::now();
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaEventDestroy(e2);
-    if (d_list) cudaFree(d_list);
-    // 4. rebind the target to every layer (maps already exist for a full-memory arena)
+    t_copied = clk::now();
+    // 3. rebind the target to every layer (maps already exist for a full-memory arena)
     T.lb = 0;
     T.le = c.n_layers;
     for (int l = 0; l < c.n_layers; ++l)
@@ -1324,9 +1355,8 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
     HS_CUDA(cudaEventRecord(T.ev_final, T.copy));
     T.load_issued = true;
   }
-  if (!comm_barrier(g)) HS_FAIL(HS_E_STATE, "barrier failed");
-  t_copied = std::chrono::steady_clock::now();
-  // 5. release the other stages ("other workers are terminated"); a stage
+  const auto t_rebound = clk::now();
+  // 4. release the other stages ("other workers are terminated"); a stage
   //    sharing the target's device hands its streams over first
   for (int k : g->active)
     if (k != tgt && g->st[k].owned && g->st[k].owns_streams && g->st[k].device == T.device && T.owned &&
@@ -1362,17 +1392,15 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
   g->st[tgt].lb = 0;
   g->st[tgt].le = c.n_layers;
   g->plan.pp = 1;
-  stats.pause_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_enter).count();
-  if (getenv("HS_DEBUG_CONS"))
-    fprintf(stderr, "[hs] consolidate: drain %.1f ms, copy-list build+copy %.1f ms (list %.1f, copy %.1f, "
-            "barrier %.1f), free %.1f ms, total %.1f ms\n",
-            1e3 * std::chrono::duration<double>(t_drained - t_enter).count(),
-            1e3 * std::chrono::duration<double>(t_copied - t_drained).count(),
-            1e3 * std::chrono::duration<double>(t_listed - t_drained).count(),
-            1e3 * std::chrono::duration<double>(t_synced - t_listed).count(),
-            1e3 * std::chrono::duration<double>(t_copied - t_synced).count(),
-            1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t_copied).count(),
-            1e3 * stats.pause_seconds);
+  const auto t_end = clk::now();
+  stats.pause_seconds = std::chrono::duration<double>(t_end - t_enter).count();
+  if (getenv("HS_DEBUG_CONS")) {
+    auto ms = [](clk::time_point a, clk::time_point b) { return 1e3 * std::chrono::duration<double>(b - a).count(); };
+    fprintf(stderr, "[hs] consolidate (stage %d): drain %.2f ms, KV list build + upload %.2f ms, copy %.2f ms "
+            "(device %.2f ms), rebind %.2f ms, release %.2f ms, pause %.2f ms\n", g->owned_stage,
+            ms(t_enter, t_drained), ms(t_drained, t_listed), ms(t_listed, t_copied), 1e3 * stats.seconds,
+            ms(t_copied, t_rebound), ms(t_rebound, t_end), 1e3 * stats.pause_seconds);
+  }
   if (out) *out = stats;
   return HS_OK;
 }
