@@ -137,6 +137,10 @@ struct DsCfg {
 };
 
 __device__ __constant__ unsigned p_backoff_ns = 256;
+// Weight k-blocks the producer keeps in flight as L2 prefetches beyond the shared-memory ring
+// (HS_DSTACK_L2AHEAD; 0 = off): while the ring is full (the MMA waits on an activation flag) the
+// prefetches keep HBM busy with the weights that come next.
+__device__ __constant__ int p_l2_ahead = 0;
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
@@ -626,6 +630,13 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
       const CUtensorMap* wm[4] = {&tw0, &tw1, &tw2, &tw3};
       DsIt ld;
       bool ld_ok = ds_it_begin(p, ld);
+      DsIt pf = ld;  // L2 prefetch cursor, p_l2_ahead k-blocks past the ring's last slot
+      bool pf_ok = ld_ok;
+      const int ahead = p_l2_ahead;
+      for (int j = 0; j < C::STAGES + ahead && pf_ok; ++j) {
+        if (j >= C::STAGES) tma_prefetch_3d(wm[pf.k], (pf.x % p.nkb[pf.k]) * 64, (pf.x / p.nkb[pf.k]) * 128, pf.l);
+        pf_ok = ds_it_next(p, pf);
+      }
       for (int i = 0; ld_ok; ++i) {
         const int s = i % C::STAGES;
         mbar_wait(&empty[s], ((i / C::STAGES) & 1) ^ 1);
@@ -634,6 +645,10 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
         mbar_expect_tx(&full[s], C::A_BYTES);
         tma_load_3d(wm[k], &full[s], smem + s * C::STAGE_BYTES, (x % p.nkb[k]) * 64, (x / p.nkb[k]) * 128, l);
         ld_ok = ds_it_next(p, ld);
+        if (ahead > 0 && pf_ok) {
+          tma_prefetch_3d(wm[pf.k], (pf.x % p.nkb[pf.k]) * 64, (pf.x / p.nkb[pf.k]) * 128, pf.l);
+          pf_ok = ds_it_next(p, pf);
+        }
       }
     }
   } else if (warp == 1) {
@@ -1037,6 +1052,9 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
       const char* e = getenv("HS_DSTACK_BACKOFF");
       const unsigned ns = e ? (unsigned)atoi(e) : 256u;
       HS_CUDA(cudaMemcpyToSymbol(p_backoff_ns, &ns, sizeof(ns)));
+      const char* e2 = getenv("HS_DSTACK_L2AHEAD");
+      const int ahead = e2 ? atoi(e2) : 0;
+      HS_CUDA(cudaMemcpyToSymbol(p_l2_ahead, &ahead, sizeof(ahead)));
       bo_set[s->device] = true;
     }
   }
