@@ -109,7 +109,33 @@ typedef struct {
   const void* data;
   uint64_t data_offset;
   uint64_t data_bytes;
+  /* Optional 8-byte "fetched end" watermark of a region still being filled by the model
+   * prefetcher (hs_prefetch_start): image offset up to which data is valid,
+   * in mapped pinned memory.  NULL = the whole range is resident.  Every H2D chunk waits on the
+   * device (cuStreamWaitValue64 on the copy stream) until the watermark covers it, and a prefill
+   * reading embedding rows from the host image waits until the embedding region is covered. */
+  const uint64_t* fetched_end;
 } hs_image;
+
+/* ---------------------------------------------------------------------------------------
+ * Model prefetcher (§5.1): "the prefetcher starts to load the model
+ * weights from remote storage to a shared memory region ... we use the first eight bytes to
+ * store the address that represents the end of currently fetched model weights".  A library
+ * thread reads bytes [file_offset, file_offset + bytes) of the model file at `path` (the host
+ * image's byte layout: header first, then the regions in image order) into dst (caller-owned
+ * pinned memory holding those image bytes), chunk_bytes at a time (0 = 8 MiB), and after each
+ * chunk stores the image offset of the fetched end into *watermark with release semantics
+ * (watermark: 8 bytes of mapped pinned memory; pass it as hs_image.fetched_end so the loader
+ * streams each chunk to HBM as soon as it is fetched).  max_gbps > 0 throttles the reads to that
+ * rate (emulating remote storage: Eq. 1's b).  Errors: HS_E_INVAL (cannot open the file).
+ * hs_prefetch_wait joins the thread (HS_E_INVAL if the file was short / unreadable; the
+ * watermark then stays at the last complete chunk); hs_prefetch_destroy stops and frees it. */
+typedef struct hs_prefetch hs_prefetch;
+hs_status hs_prefetch_start(const char* path, uint64_t file_offset, void* dst, uint64_t bytes,
+                            uint64_t chunk_bytes, double max_gbps, uint64_t* watermark,
+                            hs_prefetch** out);
+hs_status hs_prefetch_wait(hs_prefetch* p, uint64_t* fetched, double* seconds);
+hs_status hs_prefetch_destroy(hs_prefetch* p);
 
 /* Computes the image layout for cfg (host only).  total_bytes etc. filled in. */
 hs_status hs_image_layout(const hs_model_cfg* cfg, hs_image_header* out);

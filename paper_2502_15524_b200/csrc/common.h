@@ -68,6 +68,10 @@ void warm_kernels();
 #define PDL_LAUNCH() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
 bool pdl_enabled();
 
+// Enqueues on st a device-side wait until the 8-byte watermark (mapped pinned memory) is >= value
+// (cuStreamWaitValue64; prefetch.cc).  watermark == nullptr: no-op.
+hs_status stream_wait_watermark(cudaStream_t st, const uint64_t* watermark, uint64_t value);
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launchk(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
   cudaLaunchConfig_t cfg = {};

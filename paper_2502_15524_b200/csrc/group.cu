@@ -571,6 +571,8 @@ static hs_status load_stage(hs_group* g, int k, uint64_t chunk) {
   auto copy_region = [&](uint64_t off, uint64_t bytes, cudaEvent_t ev) -> hs_status {
     for (uint64_t o = 0; o < bytes; o += chunk) {
       const uint64_t n = std::min(chunk, bytes - o);
+      // pipelined with the prefetcher: the copy engine starts the chunk once it is fetched
+      HS_TRY(stream_wait_watermark(s.copy, s.img->fetched_end, off + o + n));
       HS_CUDA(cudaMemcpyAsync(s.wptr(off + o), src + (off + o - s.img->data_offset), n, cudaMemcpyHostToDevice, s.copy));
     }
     if (ev) HS_CUDA(cudaEventRecord(ev, s.copy));
@@ -620,6 +622,7 @@ static hs_status load_background(hs_group* g, int tgt, uint64_t chunk) {
     const Stage& S = g->st[k];
     for (uint64_t o = S.slice_begin; o < S.slice_end; o += chunk) {
       const uint64_t n = std::min(chunk, S.slice_end - o);
+      HS_TRY(stream_wait_watermark(T.copy, T.img->fetched_end, o + n));
       HS_CUDA(cudaMemcpyAsync(T.wptr(o), src + (o - T.img->data_offset), n, cudaMemcpyHostToDevice, T.copy));
     }
     T.bg_bytes += g->plan.stage_bytes[k];
@@ -976,7 +979,10 @@ static hs_status run_call(hs_group* g, const CallMeta& m0, const std::vector<int
         // prefill while the table is still streaming: read the prompt's rows from the image
         const bool from_host = !dec && s.host_embed && cudaEventQuery(s.ev_embed) == cudaErrorNotReady;
         cudaGetLastError();
-        if (from_host) E = s.host_embed;
+        if (from_host) {  // the prompt's rows are read from the host image: once fetched
+          E = s.host_embed;
+          HS_TRY(stream_wait_watermark(st, s.img->fetched_end, g->hdr.embed_off + g->hdr.embed_bytes));
+        }
         else if (cidx == 0 && s.lb == 0) HS_CUDA(cudaStreamWaitEvent(st, s.ev_embed, 0));
         const int* d_tok = reinterpret_cast<const int*>(meta_of(cidx) + ch[cidx].m.o_tok);
         if (feedback) {

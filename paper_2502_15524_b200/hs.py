@@ -45,7 +45,7 @@ class ImageHeader(C.Structure):
 
 class Image(C.Structure):
     _fields_ = [("header", C.POINTER(ImageHeader)), ("data", C.c_void_p),
-                ("data_offset", C.c_uint64), ("data_bytes", C.c_uint64)]
+                ("data_offset", C.c_uint64), ("data_bytes", C.c_uint64), ("fetched_end", C.c_void_p)]
 
 
 class Gpu(C.Structure):
@@ -118,7 +118,8 @@ SYMBOLS = ["hs_image_layout", "hs_plan_stages", "hs_predict_ttft_eq1", "hs_predi
            "hs_k_span_copy", "hs_debug_gemm_trace", "hs_debug_dstack_trace", "hs_plan_auto", "hs_links_create", "hs_links_admit",
            "hs_links_settle", "hs_links_complete", "hs_links_pending", "hs_links_destroy",
            "hs_load_background_async", "hs_scale_up", "hs_release_peer_memory", "hs_debug_capture",
-           "hs_debug_read_hidden", "hs_debug_set_prefill_chunking"]
+           "hs_debug_read_hidden", "hs_debug_set_prefill_chunking", "hs_prefetch_start", "hs_prefetch_wait",
+           "hs_prefetch_destroy"]
 
 _lib = None
 
@@ -183,6 +184,9 @@ def lib():
     L.hs_debug_capture.argtypes = [VP, I32]
     L.hs_debug_read_hidden.argtypes = [VP, I32, I32, I32, VP]
     L.hs_debug_set_prefill_chunking.argtypes = [VP, I32, I32]
+    L.hs_prefetch_start.argtypes = [C.c_char_p, U64, VP, U64, U64, C.c_double, VP, P(VP)]
+    L.hs_prefetch_wait.argtypes = [VP, P(U64), P(C.c_double)]
+    L.hs_prefetch_destroy.argtypes = [VP]
     _lib = L
     return L
 
@@ -291,7 +295,39 @@ class HostImage:
         return self.buf.data_ptr()
 
     def c_image(self) -> Image:
-        return Image(C.pointer(self.header), C.c_void_p(self.ptr), self.begin, self.end - self.begin)
+        wm = C.c_void_p(self.watermark.data_ptr()) if getattr(self, "watermark", None) is not None else None
+        return Image(C.pointer(self.header), C.c_void_p(self.ptr), self.begin, self.end - self.begin, wm)
+
+    def prefetch_from(self, path: str, chunk_bytes: int = 0, max_gbps: float = 0.0) -> "Prefetch":
+        """Starts the model prefetcher filling this image from `path` (the image's byte layout)
+        and attaches its 8-byte fetched-end watermark: create the group afterwards."""
+        import torch
+        self.watermark = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+        return Prefetch(path, self.begin, self.ptr, self.end - self.begin, self.watermark.data_ptr(), chunk_bytes,
+                        max_gbps)
+
+
+class Prefetch:
+    """hs_prefetch_*: the model prefetcher thread."""
+
+    def __init__(self, path, file_offset, dst, nbytes, watermark_ptr, chunk_bytes=0, max_gbps=0.0):
+        self.h = C.c_void_p()
+        check(lib().hs_prefetch_start(path.encode(), file_offset, C.c_void_p(dst), nbytes, chunk_bytes, max_gbps,
+                                      C.c_void_p(watermark_ptr), C.byref(self.h)))
+
+    def wait(self):
+        """Joins the prefetcher: (bytes fetched, seconds)."""
+        n, t = C.c_uint64(), C.c_double()
+        check(lib().hs_prefetch_wait(self.h, C.byref(n), C.byref(t)))
+        return n.value, t.value
+
+    def destroy(self):
+        if self.h:
+            lib().hs_prefetch_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        self.destroy()
 
 
 class DistComm:

@@ -10,6 +10,8 @@ every half-layer of every layer, fed the GPU's own input, within one bf16 ulp at
 of the oracle; the GPU's K/V likewise; logits from the GPU's final hidden state within 2e-2 of the
 oracle's head on the same state; greedy tokens equal to the oracle's for >= 64 steps (a fork only
 at an oracle near-tie).  The measured errors are written to gpurun_out/parity_*.json."""
+import time
+
 import numpy as np
 import pytest
 
@@ -462,3 +464,42 @@ def test_feedback_after_consolidating_into_a_later_stage(image, oracle_run):
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     g.destroy()
     g1.destroy()
+
+
+def test_prefetch_watermark_gates_load_and_prefill(image, oracle_run, tmp_path):
+    """the model file is streamed into pinned memory by
+    the prefetcher at a throttled rate (256 KiB pieces, 50 MB/s) while the loader, issued at once,
+    gates every H2D chunk on the 8-byte fetched-end watermark (cuStreamWaitValue64 on the copy
+    stream) and the prefill gates its host-image embedding reads the same way.  Unfetched bytes
+    are bf16 NaN (0xFF) and the device weights are poisoned: any chunk copied or row read before
+    its fetch would show up.  The result equals the resident-image run bit for bit, and the first
+    token cannot arrive before the prefetcher has fetched what the prefill needs."""
+    prompts, hist, _ = oracle_run
+    h = hs.image_layout(CFG)
+    path = tmp_path / "tiny.hsimg"
+    image.buf.numpy().tofile(path)  # the model file: the host image's bytes, header first
+    ref = make_group(image, 2)
+    ref.load_stage_async(-1)
+    ref.load_stats(0)
+    ref.load_stats(1)
+    rt, rl = ref.prefill([0, 1], prompts, want_logits=True)
+    img = hs.HostImage(h, 0, h.total_bytes)
+    img.buf.fill_(0xFF)
+    pf = img.prefetch_from(str(path), chunk_bytes=256 << 10, max_gbps=0.05)
+    t0 = time.perf_counter()
+    g = make_group(img, 2)
+    g.poison(0)
+    g.poison(1)
+    g.load_stage_async(-1, chunk_bytes=64 << 10)
+    toks, logits = g.prefill([0, 1], prompts, want_logits=True)
+    t1 = time.perf_counter()
+    n, secs = pf.wait()
+    assert n == h.total_bytes
+    assert np.array_equal(toks, rt) and np.array_equal(logits, rl)
+    # the last stage's slice ends the file: its last chunk cannot be copied before the fetch ends
+    assert t1 - t0 >= 0.8 * secs, (t1 - t0, secs)
+    s1 = g.load_stats(1)
+    assert s1.done == 1 and s1.load_ms >= 0.5 * 1e3 * secs * (h.total_bytes - g.plan.as_dict()["slices"][1][0]) / h.total_bytes
+    g.destroy()
+    ref.destroy()
+    pf.destroy()

@@ -97,3 +97,38 @@ def test_predictors_spec_values():
     assert hs.predict_ttft_eq5(4, 2, 6, 100, 4, 0, [16] * 4, [128] * 4, 0.5, 0.01) == pytest.approx(14.04)
     for args in [(3, 1, 2, 50, 2, 1, [10, 20], [30, 5], 0.2, 0.01), (0, 0, 0, 400, 4, 0, [16] * 4, [1000] * 4, 0, 0)]:
         assert hs.predict_ttft_eq5(*args) == pytest.approx(oplan.eq5_ttft(*args), rel=1e-12)
+
+
+def test_prefetcher_fills_region_and_publishes_watermark(tmp_path):
+    """Model prefetcher on the host only: the region equals the file bytes,
+    the 8-byte watermark ends at the fetched end (image offsets), the throttle holds, and a short
+    file is reported with the watermark left at the last complete chunk."""
+    import time
+
+    import numpy as np
+    data = np.random.default_rng(0).integers(0, 256, 3 << 20, dtype=np.uint8)
+    path = tmp_path / "model.img"
+    data.tofile(path)
+    off = 1 << 20
+    dst = np.zeros(2 << 20, dtype=np.uint8)
+    wm = np.zeros(1, dtype=np.uint64)
+    t0 = time.perf_counter()
+    p = hs.Prefetch(str(path), off, dst.ctypes.data, dst.nbytes, wm.ctypes.data, chunk_bytes=256 << 10, max_gbps=0.02)
+    seen = []
+    while True:
+        v = int(wm[0])
+        seen.append(v)
+        if v >= off + dst.nbytes:
+            break
+        time.sleep(0.002)
+    n, secs = p.wait()
+    assert n == dst.nbytes and np.array_equal(dst, data[off:off + dst.nbytes])
+    assert seen == sorted(seen) and seen[-1] == off + dst.nbytes and any(off < v < off + dst.nbytes for v in seen)
+    assert secs >= 0.9 * dst.nbytes / 0.02e9 and time.perf_counter() - t0 >= 0.09
+    p.destroy()
+    short = np.zeros(4 << 20, dtype=np.uint8)
+    p = hs.Prefetch(str(path), off, short.ctypes.data, short.nbytes, wm.ctypes.data, chunk_bytes=1 << 20)
+    with pytest.raises(hs.HsError):
+        p.wait()
+    assert int(wm[0]) == off + (2 << 20)
+    p.destroy()
