@@ -285,6 +285,22 @@ hs_status hs_prefill(hs_group* g, int32_t n_seqs, const int64_t* seq_ids,
 hs_status hs_decode_step(hs_group* g, int32_t n_seqs, const int64_t* seq_ids,
                          const int32_t* in_tokens, int32_t* out_tokens, float* out_logits);
 
+/* n_steps greedy decode steps of n_seqs live sequences with the batch split into n_micro
+ * micro-batches ("virtual engines"; the per-stage t_d and t_n terms of Eq. 2,
+ * PAPER.md:416-418, overlap across micro-batches): micro-batch j of step t runs on stage k while
+ * stage k + 1 runs micro-batch j - 1, and the first stage starts micro-batch j of step t + 1 as
+ * soon as the last stage has sampled its tokens (device feedback), so with n_micro >= pp every
+ * stage streams its weights without waiting for the others.  Micro-batches are contiguous runs of
+ * whole 4-sequence groups (n_micro is clamped to ceil(n_seqs / 4) and 8).  in_tokens: the first
+ * step's input tokens, or NULL for device feedback from the previous call (same seq_ids order).
+ * out_tokens [n_steps][n_seqs] receives every step's greedy tokens; in SPMD mode it is written
+ * on the ranks owning the first and the last stage only.  Afterwards the group is in the same
+ * state as after n_steps hs_decode_step calls (device feedback continues).  Each micro-batch's
+ * decode stack launch sees only its own sequences, so its per-sequence results equal an
+ * hs_decode_step call on the same micro-batch.  Errors as hs_decode_step. */
+hs_status hs_decode_steps(hs_group* g, int32_t n_seqs, const int64_t* seq_ids, const int32_t* in_tokens,
+                          int32_t n_steps, int32_t n_micro, int32_t* out_tokens);
+
 hs_status hs_release_seq(hs_group* g, int64_t seq_id);
 
 typedef struct {

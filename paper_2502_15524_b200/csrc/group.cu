@@ -42,13 +42,14 @@ static constexpr int kSendCtas = 64;
 static constexpr uint64_t kCounters = 1 << 16;
 static constexpr int kMaxChunks = 4;       // prefill micro-batches
 static constexpr int kChunkTokens = 1024;  // minimum tokens per micro-batch
+static constexpr int kMaxMicro = 8;        // decode micro-batches ("virtual engines") per call
 
 // Comm block of a stage (one allocation, shared with peers): flags + token / hidden inputs.
 struct CommLayout {
   static constexpr size_t FLAG_X = 0, FLAG_TOK = 4, DONE = 8, ERR = 12;
   size_t tok_in = 256, x_in = 0, bytes = 0;
   void init(int max_seqs, int max_tokens, int H) {
-    x_in = align_up(tok_in + (size_t)align_up(max_seqs * 4, 16), 256);
+    x_in = align_up(tok_in + (size_t)align_up(max_seqs * 4, 16) + 16, 256);
     bytes = x_in + (size_t)max_tokens * H * 2;
   }
 };
@@ -136,6 +137,16 @@ struct SeqState {
   int ctx = 0;
 };
 
+struct VeBuffers {
+  uint8_t* h = nullptr;  // pinned staging, R slots
+  uint8_t* d = nullptr;  // device, R slots
+  size_t slot_bytes = 0;
+  int slots = 0;
+  std::vector<cudaEvent_t> ev;
+  int* h_tok = nullptr;  // pinned token log [n_steps][align(n, 4)]
+  size_t tok_cap = 0;
+};
+
 }  // namespace hs
 
 struct hs_group {
@@ -160,6 +171,7 @@ struct hs_group {
   // test-only layer-boundary capture (hs_debug_capture / hs_debug_read_hidden): buffer row of
   // each token of the latest call (call order), and the stage that stored each boundary
   int chunk_tokens = 0, max_chunks = 0;  // prefill micro-batching knobs (0 = defaults)
+  std::map<int, hs::VeBuffers> ve;       // hs_decode_steps staging per owned stage
   bool capture = false;
   std::vector<int> cap_rowmap;
   std::vector<int> cap_owner;
@@ -1242,6 +1254,234 @@ static hs_status decode(hs_group* g, int n, const int64_t* ids, const int32_t* i
   return run_call(g, m, v, ht, feedback, out_tokens, out_logits);
 }
 
+// ------------------------------------------------------------------ pipelined decode -----
+// hs_decode_steps: n_steps greedy steps with the batch split into micro-batches ("virtual
+// engines") that flow through the stages concurrently (the t_d and t_n
+// terms of Eq. 2, are per-stage and overlap across micro-batches).  Every stage
+// works through items (step t, micro-batch j) in order; a stage hands micro-batch j of step t to
+// the next stage as soon as its layers are done (hand-off flag epoch e(t, j), rows s0_j..), and
+// the first stage starts micro-batch j of step t + 1 as soon as the last stage has sampled its
+// tokens (token flag e(t, j)), so with m >= s micro-batches every stage streams its weights
+// continuously.  Epochs: e(t, j) = base + t * m + j + 1, monotone in every stage's order.
+static hs_status ve_reserve(hs_group* g, Stage& s, VeBuffers& b, size_t slot_bytes, int slots, size_t tok_ints) {
+  DeviceGuard dg(s.device);
+  if (b.slot_bytes < slot_bytes || b.slots < slots) {
+    if (b.h) cudaFreeHost(b.h);
+    if (b.d) cudaFree(b.d);
+    for (auto e : b.ev) cudaEventDestroy(e);
+    b.ev.clear();
+    b.slot_bytes = std::max(b.slot_bytes, slot_bytes);
+    b.slots = std::max(b.slots, slots);
+    HS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&b.h), b.slot_bytes * b.slots, cudaHostAllocMapped | cudaHostAllocPortable));
+    HS_CUDA(cudaMalloc(reinterpret_cast<void**>(&b.d), b.slot_bytes * b.slots));
+    b.ev.assign(b.slots, nullptr);
+    for (auto& e : b.ev) HS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  if (b.tok_cap < tok_ints) {
+    if (b.h_tok) cudaFreeHost(b.h_tok);
+    b.tok_cap = tok_ints;
+    HS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&b.h_tok), b.tok_cap * 4 + 64, cudaHostAllocMapped | cudaHostAllocPortable));
+  }
+  (void)g;
+  return HS_OK;
+}
+
+static void ve_free(VeBuffers& b) {
+  if (b.h) cudaFreeHost(b.h);
+  if (b.d) cudaFree(b.d);
+  for (auto e : b.ev) cudaEventDestroy(e);
+  if (b.h_tok) cudaFreeHost(b.h_tok);
+  b = VeBuffers{};
+}
+
+static hs_status decode_steps(hs_group* g, int n, const int64_t* ids, const int32_t* in_tokens, int n_steps, int m_req,
+                              int32_t* out_tokens) {
+  if (g->dead) HS_FAIL(HS_E_CUDA, "group is dead after a CUDA error");
+  if (n <= 0 || n > g->kv.max_seqs || !ids || !out_tokens || n_steps <= 0 || m_req <= 0)
+    HS_FAIL(HS_E_INVAL, "bad decode_steps args");
+  if (g->spmd && std::find(g->active.begin(), g->active.end(), g->owned_stage) == g->active.end())
+    HS_FAIL(HS_E_STATE, "this rank's stage was released by consolidation");
+  const hs_model_cfg& c = g->cfg;
+  std::vector<int64_t> v(ids, ids + n);
+  if ((int)std::set<int64_t>(v.begin(), v.end()).size() != n) HS_FAIL(HS_E_INVAL, "duplicate sequence ids");
+  int need = 0;
+  for (int i = 0; i < n; ++i) {
+    auto it = g->seqs.find(ids[i]);
+    if (it == g->seqs.end()) HS_FAIL(HS_E_INVAL, "sequence %lld was never prefilled", (long long)ids[i]);
+    if (it->second.ctx + n_steps > c.max_seq) HS_FAIL(HS_E_INVAL, "sequence exceeds max_seq");
+    need += (it->second.ctx + n_steps + kBlock - 1) / kBlock - (int)it->second.blocks.size();
+  }
+  if (need > (int)g->free_blocks.size()) HS_FAIL(HS_E_OOM, "KV blocks exhausted");
+  const bool feedback = in_tokens == nullptr;
+  if (feedback && v != g->last_ids) HS_FAIL(HS_E_INVAL, "device token feedback needs the previous call's seq order");
+  if (!feedback)
+    for (int i = 0; i < n; ++i)
+      if (in_tokens[i] < 0 || in_tokens[i] >= c.vocab) HS_FAIL(HS_E_INVAL, "token id out of range");
+  // micro-batches on 4-sequence boundaries (token hand-offs move 16-byte words)
+  const int quads = (n + 3) / 4;
+  const int m = std::max(1, std::min({m_req, quads, kMaxMicro}));
+  std::vector<int> s0(m + 1);
+  for (int j = 0; j <= m; ++j) s0[j] = std::min(n, 4 * (int)((int64_t)quads * j / m));
+  std::vector<int> ctx0(n);
+  for (int i = 0; i < n; ++i) {
+    ctx0[i] = g->seqs[ids[i]].ctx;
+    HS_TRY(alloc_tokens(g, ids[i], n_steps));  // every step's slot, up front (blocks checked above)
+  }
+  const int first = g->active.front(), last = g->active.back();
+  const unsigned ep_prev = g->epoch;
+  const unsigned base = g->epoch;
+  auto ep = [&](int t, int j) { return base + (unsigned)(t * m + j) + 1; };
+  g->epoch += (unsigned)(n_steps * m);
+  const int H = c.hidden;
+  const size_t row_ints = align_up((size_t)n, 4);
+  CallMeta mx;
+  mx.T = s0[1] - s0[0];
+  for (int j = 0; j < m; ++j) mx.T = std::max(mx.T, s0[j + 1] - s0[j]);
+  mx.n = mx.T;
+  layout_meta(mx, g->max_blocks);
+  const size_t slot_bytes = align_up(mx.bytes, 256);
+  const int R = 2 * m;
+  for (size_t ai = 0; ai < g->active.size(); ++ai) {
+    Stage& s = g->st[g->active[ai]];
+    if (!s.owned) continue;
+    if (!s.load_issued) HS_FAIL(HS_E_STATE, "stage %d: no load issued", s.idx);
+    HS_TRY(ve_reserve(g, s, g->ve[s.idx], slot_bytes, R, (size_t)n_steps * row_ints));
+  }
+  int item = 0;
+  for (int t = 0; t < n_steps; ++t)
+    for (int j = 0; j < m; ++j, ++item) {
+      const int a = s0[j], nb = s0[j + 1] - s0[j];
+      CallMeta mm;
+      mm.T = nb; mm.n = nb; mm.max_nq = 1; mm.decode = true;
+      for (int i = a; i < a + nb; ++i) {
+        mm.max_ctx = std::max(mm.max_ctx, ctx0[i] + t + 1);
+        mm.kv_tokens += ctx0[i] + t + 1;
+        mm.attn_pairs += ctx0[i] + t + 1;
+      }
+      layout_meta(mm, g->max_blocks);
+      std::vector<int> dctx(nb);
+      for (int i = 0; i < nb; ++i) dctx[i] = ctx0[a + i] + t + 1;
+      for (size_t ai = 0; ai < g->active.size(); ++ai) {
+        const int k = g->active[ai];
+        Stage& s = g->st[k];
+        if (!s.owned) continue;
+        VeBuffers& vb = g->ve[k];
+        DeviceGuard dg(s.device);
+        cudaStream_t st = s.comp;
+        const int slot = item % R;
+        if (item >= R) HS_CUDA(cudaEventSynchronize(vb.ev[slot]));  // staging slot free again
+        uint8_t* hm = vb.h + (size_t)slot * vb.slot_bytes;
+        int* tok = reinterpret_cast<int*>(hm + mm.o_tok);
+        int* pos = reinterpret_cast<int*>(hm + mm.o_pos);
+        int* sl = reinterpret_cast<int*>(hm + mm.o_slot);
+        int* lastr = reinterpret_cast<int*>(hm + mm.o_last);
+        SeqDesc* sd = reinterpret_cast<SeqDesc*>(hm + mm.o_seqs);
+        int* tab = reinterpret_cast<int*>(hm + mm.o_tab);
+        for (int i = 0; i < nb; ++i) {
+          const SeqState& ss = g->seqs[ids[a + i]];
+          const int p = ctx0[a + i] + t;
+          pos[i] = p;
+          sl[i] = ss.blocks[p / kBlock] * kBlock + p % kBlock;
+          tok[i] = (!feedback && t == 0) ? in_tokens[a + i] : 0;
+          lastr[i] = i;
+          sd[i].q_start = i; sd[i].n_q = 1; sd[i].pos0 = p; sd[i].table = i;
+          for (int bb = 0; bb < g->max_blocks; ++bb)
+            tab[(size_t)i * g->max_blocks + bb] = bb < (int)ss.blocks.size() ? ss.blocks[bb] : 0;
+        }
+        uint8_t* meta = vb.d + (size_t)slot * vb.slot_bytes;
+        if (t == 0 && j == 0) HS_CUDA(cudaEventRecord(s.ev_c0, st));
+        launch_small_copy(hm, meta, mm.bytes, st);
+        HS_CUDA(cudaEventRecord(vb.ev[slot], st));
+        const bool is_first = k == first, is_last = k == last;
+        Stage* nx = is_last ? nullptr : &g->st[g->active[ai + 1]];
+        bf16* x_in_rows = reinterpret_cast<bf16*>(s.comm + g->cl.x_in) + (size_t)a * H;
+        int* tok_in = reinterpret_cast<int*>(s.comm + g->cl.tok_in) + a;
+        // stage input
+        if (is_first) {
+          const int* d_tok = reinterpret_cast<const int*>(meta + mm.o_tok);
+          if (t > 0 || feedback) {
+            launch_wait(s.flag_tok(), t > 0 ? ep(t - 1, j) : ep_prev, s.err(), st);
+            d_tok = tok_in;
+            // the tokens of step t - 1 (this micro-batch) into the host token log
+            if (t > 0) launch_small_copy(tok_in, vb.h_tok + (size_t)(t - 1) * row_ints + a, align_up((uint64_t)nb * 4, 16), st);
+          }
+          if (t == 0 && j == 0) HS_CUDA(cudaStreamWaitEvent(st, s.ev_embed, 0));
+          launch_embed(d_tok, reinterpret_cast<const bf16*>(s.wptr(g->hdr.embed_off)), s.xa, nb, H, c.vocab, st);
+        } else {
+          launch_wait(s.flag_x(), ep(t, j), s.err(), st);
+        }
+        // this stage's layers: the decode stack (or the per-kernel path)
+        if (t == 0 && j == 0) {
+          for (int l = s.lb; l < s.le; ++l) HS_CUDA(cudaStreamWaitEvent(st, s.ev_layer[l], 0));
+          if (s.le == c.n_layers) HS_CUDA(cudaStreamWaitEvent(st, s.ev_final, 0));
+        }
+        bool used = false, fin_done = false, normed = false;
+        HS_TRY(run_dstack(g, s, mm, meta, is_first ? s.xa : x_in_rows, s.xa, dctx, &used, &fin_done));
+        for (int l = s.lb; l < s.le && !used; ++l) {
+          const bf16* xin = (l == s.lb && !is_first) ? x_in_rows : s.xa;
+          HS_TRY(run_layer(g, s, l, xin, s.xa, mm, meta, normed, fin_done));
+        }
+        if (!is_last) {
+          launch_send(s.xa, nx->comm + g->cl.x_in + (size_t)a * H * 2, (uint64_t)nb * H * 2, s.done(), nx->flag_x(), ep(t, j),
+                      kSendCtas, st);
+        } else {
+          if (!fin_done)
+            launch_rmsnorm(s.xa, reinterpret_cast<const int*>(meta + mm.o_last),
+                           reinterpret_cast<const bf16*>(s.wptr(g->hdr.final_off + g->hdr.t_final_norm)), s.fin, nb, H,
+                           c.rms_eps, st);
+          GemmArgs ga{};
+          ga.A = &s.lm; ga.B = s.b_fin; ga.M = c.vocab; ga.N = nb; ga.K = H; ga.epi = EPI_F32; ga.out = s.logits;
+          ga.ldo = c.vocab; ga.workspace = s.ws; ga.workspace_bytes = kWorkspace; ga.counters = s.ctr;
+          HS_TRY(gemm(ga, st));
+          launch_argmax(s.logits, c.vocab, nb, s.d_tok_out + a, st);
+          const uint64_t tb = align_up((uint64_t)nb * 4, 16);
+          for (int kk : g->active) {  // token feedback (SPMD: every stage; local: first + full-memory)
+            if (!g->spmd && kk != first && !g->st[kk].full_memory) continue;
+            launch_send(s.d_tok_out + a, g->st[kk].comm + g->cl.tok_in + (size_t)a * 4, tb, s.done(), g->st[kk].flag_tok(),
+                        ep(t, j), 1, st);
+          }
+          launch_small_copy(s.d_tok_out + a, vb.h_tok + (size_t)t * row_ints + a, tb, st);
+        }
+        if (t == n_steps - 1 && j == m - 1) {
+          if (is_first && !is_last) {  // the last step's tokens, once sampled
+            for (int jj = 0; jj < m; ++jj) {
+              launch_wait(s.flag_tok(), ep(n_steps - 1, jj), s.err(), st);
+              launch_small_copy(reinterpret_cast<int*>(s.comm + g->cl.tok_in) + s0[jj],
+                                vb.h_tok + (size_t)(n_steps - 1) * row_ints + s0[jj],
+                                align_up((uint64_t)(s0[jj + 1] - s0[jj]) * 4, 16), st);
+            }
+          }
+          launch_small_copy(s.comm, s.h_out + align_up((uint64_t)n, 4), 16, st);  // flags + err word
+          HS_CUDA(cudaEventRecord(s.ev_c1, st));
+          s.called = true;
+        }
+      }
+    }
+  int err = 0;
+  bool got = false;
+  for (int k : g->active) {
+    Stage& s = g->st[k];
+    if (!s.owned) continue;
+    DeviceGuard dg(s.device);
+    cudaError_t e = cudaStreamSynchronize(s.comp);
+    if (e != cudaSuccess) {
+      g->dead = true;
+      HS_FAIL(HS_E_CUDA, "stage %d: %s", k, cudaGetErrorString(e));
+    }
+    err |= s.h_out[align_up((uint64_t)n, 4) + CommLayout::ERR / 4];
+    if (!got && (k == first || k == last)) {
+      for (int t = 0; t < n_steps; ++t) memcpy(out_tokens + (size_t)t * n, g->ve[k].h_tok + (size_t)t * row_ints, (size_t)n * 4);
+      got = true;
+    }
+  }
+  if (err) {
+    g->dead = true;
+    HS_FAIL(HS_E_TIMEOUT, "a cross-stage wait timed out (peer never signalled)");
+  }
+  g->last_ids = v;
+  return HS_OK;
+}
+
 // ------------------------------------------------------------------ consolidation (a17) --
 static hs_status open_peer_memory(hs_group* g, Stage& s) {
   if (s.owned || s.ipc_arena_open || !g->spmd) return HS_OK;
@@ -1683,6 +1923,11 @@ extern "C" hs_status hs_group_destroy(hs_group* g) {
     DeviceGuard dg(kv.first);
     for (auto e : kv.second) cudaEventDestroy(e);
   }
+  for (auto& kv : g->ve) {
+    DeviceGuard dg(g->st[kv.first].device >= 0 ? g->st[kv.first].device : 0);
+    ve_free(kv.second);
+  }
+  g->ve.clear();
   for (auto& s : g->st)
     if (!s.owned) free_stage(s);
   // SPMD: every importer closes its mappings of a peer's arena / KV / comm block before that
@@ -1888,4 +2133,10 @@ extern "C" hs_status hs_debug_set_prefill_chunking(hs_group* g, int32_t min_chun
   g->chunk_tokens = min_chunk_tokens;
   g->max_chunks = max_chunks;
   return HS_OK;
+}
+
+extern "C" hs_status hs_decode_steps(hs_group* g, int32_t n_seqs, const int64_t* seq_ids, const int32_t* in_tokens,
+                                     int32_t n_steps, int32_t n_micro, int32_t* out_tokens) {
+  if (!g) HS_FAIL(HS_E_INVAL, "null group");
+  return decode_steps(g, n_seqs, seq_ids, in_tokens, n_steps, n_micro, out_tokens);
 }

@@ -119,7 +119,7 @@ SYMBOLS = ["hs_image_layout", "hs_plan_stages", "hs_predict_ttft_eq1", "hs_predi
            "hs_links_settle", "hs_links_complete", "hs_links_pending", "hs_links_destroy",
            "hs_load_background_async", "hs_scale_up", "hs_release_peer_memory", "hs_debug_capture",
            "hs_debug_read_hidden", "hs_debug_set_prefill_chunking", "hs_prefetch_start", "hs_prefetch_wait",
-           "hs_prefetch_destroy"]
+           "hs_prefetch_destroy", "hs_decode_steps"]
 
 _lib = None
 
@@ -187,6 +187,7 @@ def lib():
     L.hs_prefetch_start.argtypes = [C.c_char_p, U64, VP, U64, U64, C.c_double, VP, P(VP)]
     L.hs_prefetch_wait.argtypes = [VP, P(U64), P(C.c_double)]
     L.hs_prefetch_destroy.argtypes = [VP]
+    L.hs_decode_steps.argtypes = [VP, I32, VP, VP, I32, I32, VP]
     _lib = L
     return L
 
@@ -418,6 +419,16 @@ class Group:
         check(lib().hs_decode_step(self.h, n, ids.ctypes.data, tin.ctypes.data if tin is not None else None,
                                    out.ctypes.data, logits.ctypes.data if logits is not None else None))
         return out, logits
+
+    def decode_steps(self, seq_ids, n_steps: int, n_micro: int = 1, in_tokens=None):
+        """n_steps pipelined greedy steps with n_micro micro-batches; returns tokens [n_steps, n]."""
+        n = len(seq_ids)
+        ids = np.asarray(seq_ids, dtype=np.int64)
+        tin = None if in_tokens is None else np.ascontiguousarray(np.asarray(in_tokens, dtype=np.int32))
+        out = np.zeros((n_steps, n), dtype=np.int32)
+        check(lib().hs_decode_steps(self.h, n, ids.ctypes.data, tin.ctypes.data if tin is not None else None, n_steps,
+                                    n_micro, out.ctypes.data))
+        return out
 
     def release_seq(self, seq_id: int):
         check(lib().hs_release_seq(self.h, seq_id))

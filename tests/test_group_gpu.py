@@ -503,3 +503,32 @@ def test_prefetch_watermark_gates_load_and_prefill(image, oracle_run, tmp_path):
     g.destroy()
     ref.destroy()
     pf.destroy()
+
+
+@pytest.mark.parametrize("pp,n,m", [(1, 8, 2), (2, 8, 2), (4, 16, 4), (2, 6, 2)])
+def test_decode_steps_micro_batched_equals_stepwise(image, pp, n, m):
+    """SURVEY §8(f) row 4 (decode half): hs_decode_steps runs the batch as m micro-batches
+    ("virtual engines") through the stages with device feedback.  Per sequence it is bitwise
+    equal to n stepwise hs_decode_step calls (tokens of every step, the KV of every layer and
+    position), and device feedback continues across the two APIs."""
+    lens = [5 + 3 * i for i in range(n)]
+    prompts = [hsgen.tokens(700 + i, k, CFG["vocab"]) for i, k in enumerate(lens)]
+    ids = list(range(n))
+    ga = make_group(image, pp, num_blocks=96, max_seqs=n)
+    gb = make_group(image, pp, num_blocks=96, max_seqs=n)
+    for g in (ga, gb):
+        g.load_stage_async(-1)
+        g.prefill(ids, prompts)
+    toks = ga.decode_steps(ids, 8, n_micro=m)
+    ref = np.stack([gb.decode_step(ids)[0] for _ in range(8)])
+    assert np.array_equal(toks, ref)
+    for s, k in zip(ids, lens):
+        for l in range(L):
+            assert np.array_equal(ga.read_kv(s, l, 0, k + 8), gb.read_kv(s, l, 0, k + 8))
+    a, b = ga.decode_step(ids, want_logits=True), gb.decode_step(ids, want_logits=True)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    toks2 = ga.decode_steps(ids, 3, n_micro=m, in_tokens=a[0])
+    ref2 = np.stack([gb.decode_step(ids, a[0] if i == 0 else None)[0] for i in range(3)])
+    assert np.array_equal(toks2, ref2)
+    ga.destroy()
+    gb.destroy()
