@@ -198,9 +198,13 @@ def run_ours(args):
             g.load_background_async(0, args.chunk_mb << 20)
         dev = 0.0
         t2 = time.perf_counter()
-        for _ in range(dsteps):
-            last_toks, _ = g.decode_step(ids)
+        if args.micro > 1 and pp > 1:  # pipelined decode: micro-batches through the stages at once
+            last_toks = g.decode_steps(ids, dsteps, n_micro=args.micro)[-1]
             dev += g.timing(stage).call_ms
+        else:
+            for _ in range(dsteps):
+                last_toks, _ = g.decode_step(ids)
+                dev += g.timing(stage).call_ms
         r["decode_host"] = time.perf_counter() - t2
         r["decode_dev"] = dev / 1e3
         if profile:  # per-kernel event profile on extra decode steps (events break PDL overlap)
@@ -353,6 +357,7 @@ def run_ours(args):
                                    f"{dsteps} greedy decode steps" + (", consolidate to stage 0, "
                                                                       f"{dsteps} more steps" if consolidate else ""),
                        "pp": pp, "prompt_tokens": plen, "n_seqs": n_seqs, "decode_steps": dsteps,
+                       "decode_micro_batches": args.micro if (args.micro > 1 and pp > 1) else 1,
                        "chunk_mb": args.chunk_mb, "l2": "inputs > L2 (weights 13.5 GB), no flush needed",
                        "parallelism": f"pp{pp} (one process per GPU)" if world > 1 else "pp1"},
             "ttft": {"device_s": round(ttft_dev, 5), "host_s": round(ttft_host, 5),
@@ -579,6 +584,9 @@ def main():
     ap.add_argument("--prompt-len", type=int, default=512)
     ap.add_argument("--decode-steps", type=int, default=64)
     ap.add_argument("--chunk-mb", type=int, default=32)
+    ap.add_argument("--micro", type=int, default=0,
+                    help="N>1: decode the batch as this many micro-batches flowing through the stages "
+                         "concurrently (hs_decode_steps, 'virtual engines'); 0 = one step per call")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scale-up", action="store_true",
                     help="N>1: every stage becomes a standalone endpoint (scale-up consolidation) instead of "
