@@ -206,6 +206,21 @@ hs_status hs_links_pending(hs_links* l, int32_t group, int32_t max_n, int32_t* n
                            double* pending, int64_t* ids);
 hs_status hs_links_destroy(hs_links* l);
 
+/* Contention-aware placement of one cold start arriving at now_s (DESIGN.md
+ * R20): Algorithm 1's selection over s = 1..max_pp on the contention-adjusted links (GPU i's
+ * p'_i = min(p_i, B_g / (N_g + 1)), N_g = loads recorded on its link group g), low-memory stages
+ * (w = 0), TTFT_pred(s) = max_k stage_bytes_k / min(p_k, B_g / (N_g + s_g)); admissible iff
+ * TTFT_pred <= slo_ttft_s and every load already on a touched group still meets its deadline
+ * under the new share (Eq. 3); the admissible candidate with the smallest prediction wins (else
+ * the smallest prediction).  The chosen stages are recorded in `links` as workers (pending =
+ * stage bytes, deadline = now_s + TTFT_pred); worker_ids (optional, [pp]) receive their ids
+ * (hs_links_complete them when the load ends, or let Eq. 4 retire them).  gpus[i].link_group
+ * indexes `links`; gpus[i].h2d_gbps = p_i (GB/s); link group bandwidths are bytes/s.
+ * Errors: HS_E_INVAL, HS_E_INFEASIBLE (no GPU set holds the model). */
+hs_status hs_place_cold_start(const hs_model_cfg* cfg, const hs_gpu* gpus, int32_t n_gpus, hs_links* links,
+                              double now_s, double slo_ttft_s, int32_t max_pp, hs_plan* out,
+                              double* pred_ttft_s, int32_t* admitted, int64_t* worker_ids);
+
 /* Paper's predictors, exposed for the planner's tests (PAPER.md:398 Eq. 1, :417 Eq. 2,
  * :579-584 Eq. 5).  Bandwidth arrays have s entries; M in the same unit as b,p numerators. */
 double hs_predict_ttft_eq1(double t_c, double M, int32_t s, int32_t w, const double* b,

@@ -136,3 +136,56 @@ class ContentionRegistry:
     def complete(self, wid, now):
         self.settle(now)
         self.ws.pop(wid, None)
+
+    def record(self, S, D):
+        """A placed cold-start worker enters the list (pending S, deadline D)."""
+        wid = self.next
+        self.next += 1
+        self.ws[wid] = (S, D)
+        return wid
+
+
+def place_cold_start(cfg: dict, gpus, regs: dict, now: float, slo_ttft: float, max_pp: int = 4):
+    """Contention-aware placement of one cold start (reading R20), written out from
+    Algorithm 1, Eq. 3 and Eq. 4:
+      1. settle every link group to `now` (Eq. 4);
+      2. for s = 1..max_pp: Alg. 1's GPU selection with w = 0 on the contended links
+         p'_i = min(p_i, B_g / (N_g + 1)) (ties: fewer loads N_g, then device id);
+      3. stage k on group g gets p_eff = min(p_k, B_g / (N_g + s_g)); TTFT_pred = max_k bytes_k / p_eff;
+      4. admissible iff TTFT_pred <= SLO and Eq. 3 holds for every worker on a touched group with
+         N + s_g workers;
+      5. the admissible choice with the smallest TTFT_pred (ties: smaller s), else the smallest;
+      6. its stages are recorded (pending = stage bytes, deadline = now + TTFT_pred).
+    gpus: dicts {device, h2d_gbps, link_group, free_bytes}; regs: group -> ContentionRegistry
+    (B in bytes/s).  Returns (plan dict, pred, admitted, worker ids)."""
+    for g in sorted({x["link_group"] for x in gpus}):
+        regs[g].settle(now)
+    N = {g: len(r.ws) for g, r in regs.items()}
+    view = [dict(x, h2d_gbps=min(x["h2d_gbps"], regs[x["link_group"]].B / 1e9 / (N[x["link_group"]] + 1)),
+                 n_workers=N[x["link_group"]]) for x in gpus]
+    by_dev = {x["device"]: x for x in gpus}
+    best = None
+    for s in range(1, min(max_pp, cfg["n_layers"], len(gpus)) + 1):
+        try:
+            p = plan(cfg, view, s, 0)
+        except ValueError:
+            continue
+        sg = {}
+        for d in p["device"]:
+            g = by_dev[d]["link_group"]
+            sg[g] = sg.get(g, 0) + 1
+        pred = max(p["stage_bytes"][k] / min(by_dev[d]["h2d_gbps"] * 1e9,
+                                             regs[by_dev[d]["link_group"]].B / (N[by_dev[d]["link_group"]] + sg[by_dev[d]["link_group"]]))
+                   for k, d in enumerate(p["device"]))
+        ok = pred <= slo_ttft
+        for g, n in sg.items():
+            share = regs[g].B / (N[g] + n)
+            ok = ok and all(S <= share * (D - now) for S, D in regs[g].ws.values())
+        key = (0 if ok else 1, pred, s)
+        if best is None or key < best[0]:
+            best = (key, p, pred, ok)
+    if best is None:
+        raise ValueError("infeasible")
+    _, p, pred, ok = best
+    ids = [regs[by_dev[d]["link_group"]].record(p["stage_bytes"][k], now + pred) for k, d in enumerate(p["device"])]
+    return p, pred, ok, ids

@@ -159,3 +159,94 @@ extern "C" hs_status hs_links_destroy(hs_links* l) {
   delete l;
   return HS_OK;
 }
+
+// Contention-aware placement of one cold start (reading R20):
+// Algorithm 1's selection on the contention-adjusted link view,
+// Eq. 3 admission against the loads already streaming over each link group, Eq. 4
+// bookkeeping.  For s = 1..max_pp the GPUs are ranked by 1/p'_i with
+// p'_i = min(p_i, B_g / (N_g + 1)) (the bandwidth a new load on GPU i would get; ties -> fewer
+// loads N_g on its group), all stages low-memory (w = 0: a burst of cold starts, no
+// consolidation).  Each stage k on group g gets the equal credit p_eff = min(p_k, B_g / (N_g + s_g))
+// (s_g: the candidate's stages on g), so TTFT_pred(s) = max_k bytes_k / p_eff_k (Eq. 5 as in R9,
+// with the fetching term replaced by the contended link).  A candidate is admissible iff every
+// worker already on a touched group still meets its deadline under the new share (Eq. 3 with
+// N + s_g) and TTFT_pred <= SLO.  The admissible candidate with the smallest prediction wins
+// (ties: smaller s); if none, the smallest prediction.  Its stages are then recorded as workers
+// (pending = stage bytes, deadline D = T + TTFT_pred, "the fetching deadline comes from the
+// prediction of TTFT").
+extern "C" hs_status hs_place_cold_start(const hs_model_cfg* cfg, const hs_gpu* gpus, int32_t n_gpus, hs_links* l,
+                                         double now, double slo_ttft_s, int32_t max_pp, hs_plan* out,
+                                         double* pred_ttft_s, int32_t* admitted, int64_t* worker_ids) {
+  if (!cfg || !gpus || n_gpus <= 0 || !l || !out) {
+    set_error("hs_place_cold_start: bad arguments");
+    return HS_E_INVAL;
+  }
+  std::vector<int> seen;
+  for (int i = 0; i < n_gpus; ++i) {
+    const int g = gpus[i].link_group;
+    if (!grp_ok(l, g) || gpus[i].h2d_gbps <= 0) {
+      set_error("hs_place_cold_start: a GPU's link group is not in the registry");
+      return HS_E_INVAL;
+    }
+    if (std::find(seen.begin(), seen.end(), g) == seen.end()) {
+      seen.push_back(g);
+      hs_status r = hs_links_settle(l, g, now);  // Eq. 4 up to T
+      if (r != HS_OK) return r;
+    }
+  }
+  auto N = [&](int g) { return (double)l->ws[g].size(); };
+  std::vector<hs_gpu> view(gpus, gpus + n_gpus);
+  for (auto& v : view) {
+    v.h2d_gbps = std::min(v.h2d_gbps, l->bw[v.link_group] / 1e9 / (N(v.link_group) + 1.0));
+    v.n_workers = (int32_t)N(v.link_group);
+  }
+  auto gpu_of = [&](int dev) {
+    for (int i = 0; i < n_gpus; ++i)
+      if (gpus[i].device == dev) return i;
+    return -1;
+  };
+  bool have = false, best_ok = false;
+  double best_pred = 0;
+  hs_plan best{};
+  const int smax = std::max(1, std::min<int>({max_pp > 0 ? max_pp : 4, HS_MAX_STAGES, cfg->n_layers, n_gpus}));
+  for (int s = 1; s <= smax; ++s) {
+    hs_plan p;
+    if (hs_plan_stages(cfg, view.data(), n_gpus, s, 0, 0.0, 0.0, &p) != HS_OK) continue;
+    std::map<int, int> sg;  // stages per group
+    for (int k = 0; k < s; ++k) sg[gpus[gpu_of(p.device[k])].link_group]++;
+    double pred = 0;
+    for (int k = 0; k < s; ++k) {
+      const hs_gpu& gk = gpus[gpu_of(p.device[k])];
+      const int g = gk.link_group;
+      const double peff = std::min(gk.h2d_gbps * 1e9, l->bw[g] / (N(g) + sg[g]));
+      pred = std::max(pred, (double)p.stage_bytes[k] / peff);
+    }
+    bool ok = pred <= slo_ttft_s;
+    for (auto& kv : sg) {  // Eq. 3 for every worker already on the group, under the new share
+      const double share = l->bw[kv.first] / (N(kv.first) + kv.second);
+      for (const auto& w : l->ws[kv.first]) ok = ok && w.pending <= share * (w.deadline - now);
+    }
+    const bool better = !have || (ok && !best_ok) || (ok == best_ok && pred < best_pred);
+    if (better) {
+      have = true;
+      best_ok = ok;
+      best_pred = pred;
+      best = p;
+    }
+  }
+  if (!have) {
+    set_error("hs_place_cold_start: no GPU set can hold the model");
+    return HS_E_INFEASIBLE;
+  }
+  best.pred_ttft_s = best_pred;
+  for (int k = 0; k < best.pp; ++k) {  // record the stages as cold-start workers of their groups
+    const int g = gpus[gpu_of(best.device[k])].link_group;
+    l->ws[g].push_back({l->next_id, (double)best.stage_bytes[k], now + best_pred});
+    if (worker_ids) worker_ids[k] = l->next_id;
+    ++l->next_id;
+  }
+  *out = best;
+  if (pred_ttft_s) *pred_ttft_s = best_pred;
+  if (admitted) *admitted = best_ok ? 1 : 0;
+  return HS_OK;
+}

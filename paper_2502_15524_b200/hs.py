@@ -119,7 +119,7 @@ SYMBOLS = ["hs_image_layout", "hs_plan_stages", "hs_predict_ttft_eq1", "hs_predi
            "hs_links_settle", "hs_links_complete", "hs_links_pending", "hs_links_destroy",
            "hs_load_background_async", "hs_scale_up", "hs_release_peer_memory", "hs_debug_capture",
            "hs_debug_read_hidden", "hs_debug_set_prefill_chunking", "hs_prefetch_start", "hs_prefetch_wait",
-           "hs_prefetch_destroy", "hs_decode_steps"]
+           "hs_prefetch_destroy", "hs_decode_steps", "hs_place_cold_start"]
 
 _lib = None
 
@@ -188,6 +188,8 @@ def lib():
     L.hs_prefetch_wait.argtypes = [VP, P(U64), P(C.c_double)]
     L.hs_prefetch_destroy.argtypes = [VP]
     L.hs_decode_steps.argtypes = [VP, I32, VP, VP, I32, I32, VP]
+    L.hs_place_cold_start.argtypes = [P(ModelCfg), P(Gpu), I32, VP, C.c_double, C.c_double, I32, P(Plan),
+                                      P(C.c_double), P(I32), P(C.c_int64)]
     _lib = L
     return L
 
@@ -250,6 +252,15 @@ class Links:
         ids = (C.c_int64 * max(n.value, 1))()
         check(lib().hs_links_pending(self.h, group, n.value, C.byref(n), pend, ids))
         return {ids[i]: pend[i] for i in range(n.value)}
+
+    def place(self, cfg: dict, gpus, now: float, slo_ttft_s: float, max_pp: int = 4):
+        """hs_place_cold_start: (plan, predicted TTFT s, admitted, worker ids)."""
+        out, pred, ok = Plan(), C.c_double(), C.c_int32()
+        ids = (C.c_int64 * HS_MAX_STAGES)()
+        c = model_cfg(cfg)
+        check(lib().hs_place_cold_start(C.byref(c), _gpus(gpus), len(gpus), self.h, now, slo_ttft_s, max_pp,
+                                        C.byref(out), C.byref(pred), C.byref(ok), ids))
+        return out, pred.value, bool(ok.value), list(ids[:out.pp])
 
     def __del__(self):
         try:

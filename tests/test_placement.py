@@ -89,3 +89,51 @@ def test_alg1_prefers_free_gpus_and_falls_back():
     # a tight TTFT SLO forces s > 1 (7B: 242 ms over one link, 63 ms at s = 4)
     p, share, ok = hs.plan_auto(CFG, gpus_box(8), 0.005, 0.005, 1e-5, 0.1, 1.0, max_pp=8)
     assert ok and p.pp >= 3
+
+
+@pytest.mark.parametrize("case", range(40))
+def test_place_cold_start_matches_oracle(case):
+    """hs_place_cold_start (library) == oracle.plan.place_cold_start (Alg. 1 + Eq. 3/4, reading
+    R20) over a random burst of mixed 7B / 13B cold starts on 4 or 8 GPUs with per-GPU or shared
+    link groups: same GPUs, stage ranges, prediction, admission, and the same registries after."""
+    rng = np.random.default_rng(100 + case)
+    n = int(rng.choice([4, 8]))
+    shared = bool(rng.integers(0, 2))
+    groups = [i // 2 if shared else i for i in range(n)]
+    ng = max(groups) + 1
+    B = [float(rng.uniform(40, 120)) * 1e9 for _ in range(ng)]
+    gpus = [dict(device=i, h2d_gbps=float(rng.uniform(40, 60)), link_group=groups[i], free_bytes=180 * 10**9)
+            for i in range(n)]
+    links = hs.Links(B)
+    regs = {g: oplan.ContentionRegistry(B[g]) for g in range(ng)}
+    now = 0.0
+    for j in range(10):
+        now += float(rng.gamma(1 / 64, 64 / 8.0))
+        cfg = hsgen.CONFIGS["llama2-7b" if rng.random() < 0.5 else "llama2-13b"]
+        slo = float(rng.uniform(0.05, 0.6))
+        p, pred, ok, ids = links.place(cfg, gpus, now, slo, max_pp=4)
+        rp, rpred, rok, rids = oplan.place_cold_start(cfg, gpus, regs, now, slo, max_pp=4)
+        d = p.as_dict()
+        assert d["device"] == rp["device"] and d["ranges"] == rp["ranges"], (case, j)
+        assert ok == rok and pred == pytest.approx(rpred, rel=1e-12) and len(set(ids)) == len(ids) == p.pp
+        for g in range(ng):  # same workers (pending bytes, deadlines) on every link group
+            pend = sorted(links.pending(g).values())
+            ref = sorted(S for S, _ in regs[g].ws.values())
+            assert len(pend) == len(ref)
+            for a, b in zip(pend, ref):
+                assert a == pytest.approx(b, rel=1e-9, abs=1e-3)
+
+
+def test_place_cold_start_spreads_a_burst():
+    """Four simultaneous 7B cold starts on 4 GPUs with independent links: the first takes all 4
+    GPUs (s = 4 is the fastest), later ones see the links busy and the predictions grow; each
+    prediction accounts for the equal-credit share of every load in flight."""
+    gpus = [dict(device=i, h2d_gbps=55.0, link_group=i, free_bytes=180 * 10**9) for i in range(4)]
+    links = hs.Links([55e9] * 4)
+    preds = []
+    for j in range(4):
+        p, pred, ok, ids = links.place(CFG, gpus, 0.0, 10.0, max_pp=4)
+        preds.append(pred)
+        assert len(ids) == p.pp
+    assert preds[0] == pytest.approx(max(oplan.stage_param_bytes(CFG, 4)) / 55e9, rel=1e-9)
+    assert preds == sorted(preds)

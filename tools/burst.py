@@ -8,13 +8,10 @@ from its arrival to its first token on the host (weights in pinned host memory a
 
 Policies (placement is decided at each arrival from the state the scheduler sees then):
   naive   : model j -> PP = 1 on GPU j mod n (its own PCIe link, no coordination);
-  hydra   : for every s in 1..n, stages on the s GPUs with the fewest loads in flight
-            (hs_plan_stages, n_workers tie-break), each stage's bandwidth predicted as
-            min(link, B_host / (loads in flight + s)) (B_host = measured concurrent H2D of the
-            box), Eq. 3 admission (hs_links_admit, deadline = arrival + SLO) against the loads
-            already in flight (Eq. 4 settles them); the admissible s with the smallest predicted
-            TTFT wins (none admissible: the smallest predicted TTFT).
-Host-side scheduling uses the library's own calls (hs_plan_stages, hs_links_*)."""
+  hydra   : the library's hs_place_cold_start (Alg. 1 on the contended links + Eq. 3 admission
+            + Eq. 4 bookkeeping, R20), one link group per GPU at its measured isolated
+            pinned-H2D bandwidth.
+This file is harness only: the placement policy lives in the library."""
 from __future__ import annotations
 
 import json
@@ -30,9 +27,6 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import hsgen  # noqa: E402
 from paper_2502_15524_b200 import hs  # noqa: E402
 
-LINK_GBS = 55.6
-
-
 def arrivals(n, cv=8.0, rate=8.0, seed=7):
     rng = np.random.default_rng(seed)
     gaps = rng.gamma(1.0 / cv ** 2, cv ** 2 / rate, size=n)
@@ -40,12 +34,23 @@ def arrivals(n, cv=8.0, rate=8.0, seed=7):
     return (t - t[0]).tolist()
 
 
-def measure_host_gbs(n_gpus, img):
-    """Concurrent pinned-H2D bandwidth with every GPU copying at once (the host cap)."""
+def measure_links(n_gpus, img):
+    """Isolated pinned-H2D bandwidth of every GPU's link (GB/s, best of 3) and the concurrent sum."""
     probe = min(1 << 30, img.buf.numel())
     bufs = [torch.empty(probe, dtype=torch.uint8, device=f"cuda:{d}") for d in range(n_gpus)]
     streams = [torch.cuda.Stream(device=d) for d in range(n_gpus)]
-    best = 0.0
+    iso = []
+    for d in range(n_gpus):
+        best = 1e9
+        for _ in range(3):
+            torch.cuda.synchronize(d)
+            t0 = time.perf_counter()
+            with torch.cuda.stream(streams[d]):
+                bufs[d].copy_(img.buf[:probe], non_blocking=True)
+            torch.cuda.synchronize(d)
+            best = min(best, time.perf_counter() - t0)
+        iso.append(probe / best / 1e9)
+    conc = 0.0
     for _ in range(3):
         for d in range(n_gpus):
             torch.cuda.synchronize(d)
@@ -55,54 +60,31 @@ def measure_host_gbs(n_gpus, img):
                 bufs[d].copy_(img.buf[:probe], non_blocking=True)
         for d in range(n_gpus):
             torch.cuda.synchronize(d)
-        best = max(best, n_gpus * probe / (time.perf_counter() - t0) / 1e9)
+        conc = max(conc, n_gpus * probe / (time.perf_counter() - t0) / 1e9)
     del bufs
-    return best
+    return iso, conc
 
 
-def place(policy, models, offs, cfgs, n_gpus, b_host, slo_s):
-    """Placement of every request at its arrival (host-side simulation of loads in flight)."""
+def place(policy, models, offs, cfgs, n_gpus, link_gbs, slo_s):
+    """Placement of every request at its arrival.  naive: PP = 1 on GPU j mod n.  hydra: the
+    library's contention-aware placement (hs_place_cold_start: Alg. 1 + Eq. 3/4 over the GPUs'
+    host links, one link group per GPU with its measured isolated bandwidth)."""
     plans = []
     if policy == "naive":
         for j, m in enumerate(models):
-            gpus = [dict(device=j % n_gpus, h2d_gbps=LINK_GBS, free_bytes=170 << 30)]
+            gpus = [dict(device=j % n_gpus, h2d_gbps=link_gbs[j % n_gpus], free_bytes=170 << 30)]
             plans.append(hs.plan_stages(cfgs[m], gpus, 1, 0))
         return plans
-    links = hs.Links([b_host * 1e9])
-    inflight = []  # (gpu, end_time, worker id)
+    links = hs.Links([g * 1e9 for g in link_gbs])
+    gpus = [dict(device=d, h2d_gbps=link_gbs[d], link_group=d, free_bytes=170 << 30) for d in range(n_gpus)]
     for j, m in enumerate(models):
-        now = offs[j]
-        links.settle(0, now)
-        inflight = [x for x in inflight if x[1] > now]
-        busy = [sum(1 for x in inflight if x[0] == d) for d in range(n_gpus)]
-        n_active = len(inflight)
-        best = None
-        for s in range(1, n_gpus + 1):
-            p_eff = min(LINK_GBS, b_host / (n_active + s))
-            gpus = [dict(device=d, h2d_gbps=LINK_GBS / (1 + busy[d]), free_bytes=170 << 30, n_workers=busy[d])
-                    for d in range(n_gpus)]
-            try:
-                pl = hs.plan_stages(cfgs[m], gpus, s, 0)
-            except hs.HsError:
-                continue
-            pred = max(pl.stage_bytes[k] for k in range(s)) / (p_eff * 1e9)
-            # Eq. 3 against the loads in flight (admit tentatively, then roll back)
-            ok, wid = links.admit(0, float(sum(pl.stage_bytes[k] for k in range(s))), now + slo_s, now)
-            if ok:
-                links.complete(0, wid, now)
-            key = (0 if ok else 1, pred)
-            if best is None or key < best[0]:
-                best = (key, pl, s, pred)
-        _, pl, s, pred = best
-        ok, wid = links.admit(0, float(sum(pl.stage_bytes[k] for k in range(s))), now + max(slo_s, pred), now)
-        for k in range(s):
-            inflight.append((pl.device[k], now + pred, wid))
+        pl, pred, ok, _ = links.place(cfgs[m], gpus, offs[j], slo_s, max_pp=n_gpus)
         plans.append(pl)
     return plans
 
 
-def run(policy, models, offs, cfgs, imgs, n_gpus, b_host, slo_s):
-    plans = place(policy, models, offs, cfgs, n_gpus, b_host, slo_s)
+def run(policy, models, offs, cfgs, imgs, n_gpus, link_gbs, slo_s):
+    plans = place(policy, models, offs, cfgs, n_gpus, link_gbs, slo_s)
     groups = []
     for j, m in enumerate(models):
         groups.append(hs.Group(cfgs[m], plans[j], imgs[m], num_blocks=40, max_seqs=1, max_tokens=512))
@@ -148,11 +130,11 @@ def main(n_gpus=None):
         imgs[m] = hs.HostImage(h, h.embed_off, h.total_bytes)
         hsgen.image_fill(hsgen.image_header(cfgs[m]), hsgen.WEIGHT_SEED, imgs[m].ptr, h.embed_off, h.total_bytes)
     offs = arrivals(len(models))
-    b_host = measure_host_gbs(n_gpus, imgs["llama2-7b"])
+    link_gbs, conc = measure_links(n_gpus, imgs["llama2-7b"])
     slo = 0.25  # TTFT SLO (s): about one 7B PP=1 load over one link
     out = dict(n_gpus=n_gpus, models=models, arrivals_s=[round(x, 4) for x in offs],
-               host_concurrent_h2d_gbs=round(b_host, 1), link_gbs=LINK_GBS, slo_ttft_s=slo,
-               runs=[run(p, models, offs, cfgs, imgs, n_gpus, b_host, slo) for p in ("naive", "hydra")])
+               host_concurrent_h2d_gbs=round(conc, 1), link_gbs=[round(x, 1) for x in link_gbs], slo_ttft_s=slo,
+               runs=[run(p, models, offs, cfgs, imgs, n_gpus, link_gbs, slo) for p in ("naive", "hydra")])
     return out
 
 
