@@ -362,7 +362,8 @@ hs_status hs_scale_up(hs_group* g, const int32_t* seq_owner, int32_t n_live, hs_
  * ~100 ms, so hs_consolidate defers it off the decode pause).  Each rank closes its deferred
  * mappings, meets at hs_comm.barrier, then frees its released memory.  ALWAYS collective in SPMD
  * mode: every rank must call it (also when it has nothing pending), because every rank enters the
- * barrier.  No-op in local mode.  hs_group_destroy does it too.  Errors: HS_E_INVAL (NULL),
+ * barrier.  Local mode: frees the released stages' memory (consolidation defers those driver frees
+ * off the pause too), no barrier.  hs_group_destroy does it too.  Errors: HS_E_INVAL (NULL),
  * HS_E_STATE (the barrier failed: the exported regions are then left allocated, never freed under
  * a peer's mapping; everything else is released). */
 hs_status hs_release_peer_memory(hs_group* g);

@@ -1627,12 +1627,9 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
         S.kv_mem = nullptr;
         S.comm = nullptr;
       }
-      if (g->spmd) {
-        g->stage_deferred.push_back(S);
-        S = Stage{};
-      } else {
-        free_stage(S);
-      }
+      // the rest of the teardown (driver frees of GBs: tens of ms) waits for the release point
+      g->stage_deferred.push_back(S);
+      S = Stage{};
     }
   g->active = {tgt};
   g->st[tgt].lb = 0;

@@ -614,7 +614,16 @@ def probe_lib():
             raise ImportError(f"{so} is missing: build with python -m paper_2502_15524_b200.build")
         _probe = C.CDLL(so)
         _probe.hs_debug_tmem_a_gemm.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
+        _probe.hs_debug_stream_probe.argtypes = [C.c_int32, C.c_int64, C.c_int64, C.c_int32, C.c_int32,
+                                                 C.POINTER(C.c_double)]
     return _probe
+
+
+def stream_probe(layout: int, M: int, K: int, slots: int = 12, iters: int = 4) -> float:
+    """Test-only: achieved GB/s streaming an [M, K] bf16 matrix in the decode stack's TMA pattern."""
+    v = C.c_double()
+    check(probe_lib().hs_debug_stream_probe(layout, M, K, slots, iters, C.byref(v)))
+    return v.value
 
 
 def tmem_a_gemm(A, B):

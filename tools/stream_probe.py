@@ -1,0 +1,18 @@
+"""Weight-streaming probe (include/hs_probes.h hs_debug_stream_probe): GB/s of the decode stack's
+TMA pattern over the image's row-major layout vs a tiled (contiguous 16 KiB block) layout."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402,F401
+
+from paper_2502_15524_b200 import hs  # noqa: E402
+
+out = []
+for M, K in ((12288, 4096), (22016, 4096), (4096, 11008), (65536, 4096)):
+    for slots in (8, 12):
+        for layout in (0, 1):
+            out.append(dict(M=M, K=K, slots=slots, layout=["row-major", "tiled"][layout],
+                            gbs=round(hs.stream_probe(layout, M, K, slots, 4), 1)))
+            print(json.dumps(out[-1]), flush=True)
