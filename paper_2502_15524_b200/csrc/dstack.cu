@@ -141,6 +141,9 @@ __device__ __constant__ unsigned p_backoff_ns = 256;
 // (HS_DSTACK_L2AHEAD; 0 = off): while the ring is full (the MMA waits on an activation flag) the
 // prefetches keep HBM busy with the weights that come next.
 __device__ __constant__ int p_l2_ahead = 0;
+// Timing experiments only (HS_DSTACK_NOMMA=1, results garbage): skip the tensor-core MMAs, keep
+// every barrier, load and flag, to separate MMA issue/completion cost from the memory stream.
+__device__ __constant__ int p_nomma = 0;
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
@@ -607,10 +610,12 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
   int* s_base = s_nc + DS_MAXSEQ;                                                      // [65]
   int* s_pos = s_base + DS_MAXSEQ + 4;                                                 // [64]
   int* s_slot = s_pos + DS_MAXSEQ;                                                     // [64]
+  volatile int* s_prog = s_slot + DS_MAXSEQ;                                           // [1] k-blocks issued
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int G = p.G;
 
   if (threadIdx.x == 0) {
+    *s_prog = 0;
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 2); mbar_init(&empty[s], 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -630,13 +635,6 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
       const CUtensorMap* wm[4] = {&tw0, &tw1, &tw2, &tw3};
       DsIt ld;
       bool ld_ok = ds_it_begin(p, ld);
-      DsIt pf = ld;  // L2 prefetch cursor, p_l2_ahead k-blocks past the ring's last slot
-      bool pf_ok = ld_ok;
-      const int ahead = p_l2_ahead;
-      for (int j = 0; j < C::STAGES + ahead && pf_ok; ++j) {
-        if (j >= C::STAGES) tma_prefetch_3d(wm[pf.k], (pf.x % p.nkb[pf.k]) * 64, (pf.x / p.nkb[pf.k]) * 128, pf.l);
-        pf_ok = ds_it_next(p, pf);
-      }
       for (int i = 0; ld_ok; ++i) {
         const int s = i % C::STAGES;
         mbar_wait(&empty[s], ((i / C::STAGES) & 1) ^ 1);
@@ -644,16 +642,14 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
         if (x == ld.beg && p.trace) DS_TR(k == 0 ? TR_A0 : TR_A1 + k - 1);
         mbar_expect_tx(&full[s], C::A_BYTES);
         tma_load_3d(wm[k], &full[s], smem + s * C::STAGE_BYTES, (x % p.nkb[k]) * 64, (x / p.nkb[k]) * 128, l);
+        *s_prog = i + 1;  // progress for the L2 prefetcher (warp 3)
         ld_ok = ds_it_next(p, ld);
-        if (ahead > 0 && pf_ok) {
-          tma_prefetch_3d(wm[pf.k], (pf.x % p.nkb[pf.k]) * 64, (pf.x / p.nkb[pf.k]) * 128, pf.l);
-          pf_ok = ds_it_next(p, pf);
-        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer
       constexpr uint32_t idesc = instr_desc<BN>();
+      const bool nomma = p_nomma != 0;
       int i = 0, seg = 0;
       for (int l = 0; l < p.nl; ++l)
         for (int k = 0; k < 4; ++k) {
@@ -673,15 +669,33 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
               asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
               const uint8_t* sa = smem + s * C::STAGE_BYTES;
               const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + C::A_BYTES);
+              if (!nomma) {
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk)
-                umma_bf16(acc, da + 2 * kk, db + 2 * kk, idesc, (kb > kb_lo || kk > 0) ? 1u : 0u);
+                for (int kk = 0; kk < 4; ++kk)
+                  umma_bf16(acc, da + 2 * kk, db + 2 * kk, idesc, (kb > kb_lo || kk > 0) ? 1u : 0u);
+              }
               umma_commit(&empty[s]);
             }
             umma_commit(&tfull[buf]);
             cur += kb_hi - kb_lo;
           }
         }
+    }
+  } else if (warp == 3) {
+    // ---- optional L2 prefetcher (HS_DSTACK_L2AHEAD = d > 0): keeps the k-blocks
+    // [loaded + STAGES, loaded + STAGES + d) of this CTA's weight stream requested into L2, so
+    // HBM keeps streaming while the ring is full and the MMA waits on an activation flag
+    const int ahead = p_l2_ahead;
+    if (ahead > 0 && lane == 0) {
+      const CUtensorMap* wm[4] = {&tw0, &tw1, &tw2, &tw3};
+      DsIt pf;
+      bool pf_ok = ds_it_begin(p, pf);
+      for (int j = 0; j < C::STAGES && pf_ok; ++j) pf_ok = ds_it_next(p, pf);
+      for (int i = C::STAGES; pf_ok; ++i) {
+        while (i >= *s_prog + C::STAGES + ahead) __nanosleep(128);
+        tma_prefetch_3d(wm[pf.k], (pf.x % p.nkb[pf.k]) * 64, (pf.x / p.nkb[pf.k]) * 128, pf.l);
+        pf_ok = ds_it_next(p, pf);
+      }
     }
   } else if (warp == 2) {
     // ---- activation producer: flag-gated.  The whole warp polls up to 32 k-blocks' flags at
@@ -1055,6 +1069,9 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
       const char* e2 = getenv("HS_DSTACK_L2AHEAD");
       const int ahead = e2 ? atoi(e2) : 0;
       HS_CUDA(cudaMemcpyToSymbol(p_l2_ahead, &ahead, sizeof(ahead)));
+      const char* e3 = getenv("HS_DSTACK_NOMMA");
+      const int nomma = e3 ? atoi(e3) : 0;
+      HS_CUDA(cudaMemcpyToSymbol(p_nomma, &nomma, sizeof(nomma)));
       bo_set[s->device] = true;
     }
   }

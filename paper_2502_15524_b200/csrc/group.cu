@@ -1442,21 +1442,27 @@ static hs_status decode_steps(hs_group* g, int n, const int64_t* ids, const int3
           }
           launch_small_copy(s.d_tok_out + a, vb.h_tok + (size_t)t * row_ints + a, tb, st);
         }
-        if (t == n_steps - 1 && j == m - 1) {
-          if (is_first && !is_last) {  // the last step's tokens, once sampled
-            for (int jj = 0; jj < m; ++jj) {
-              launch_wait(s.flag_tok(), ep(n_steps - 1, jj), s.err(), st);
-              launch_small_copy(reinterpret_cast<int*>(s.comm + g->cl.tok_in) + s0[jj],
-                                vb.h_tok + (size_t)(n_steps - 1) * row_ints + s0[jj],
-                                align_up((uint64_t)(s0[jj + 1] - s0[jj]) * 4, 16), st);
-            }
-          }
-          launch_small_copy(s.comm, s.h_out + align_up((uint64_t)n, 4), 16, st);  // flags + err word
-          HS_CUDA(cudaEventRecord(s.ev_c1, st));
-          s.called = true;
-        }
       }
     }
+  // every stage's tail, after all items are enqueued (stages on one device share a stream): the
+  // first stage collects the last step's tokens once sampled; the flags + error word to the host
+  for (size_t ai = 0; ai < g->active.size(); ++ai) {
+    const int k = g->active[ai];
+    Stage& s = g->st[k];
+    if (!s.owned) continue;
+    DeviceGuard dg(s.device);
+    cudaStream_t st = s.comp;
+    if (k == first && k != last)
+      for (int jj = 0; jj < m; ++jj) {
+        launch_wait(s.flag_tok(), ep(n_steps - 1, jj), s.err(), st);
+        launch_small_copy(reinterpret_cast<int*>(s.comm + g->cl.tok_in) + s0[jj],
+                          g->ve[k].h_tok + (size_t)(n_steps - 1) * row_ints + s0[jj],
+                          align_up((uint64_t)(s0[jj + 1] - s0[jj]) * 4, 16), st);
+      }
+    launch_small_copy(s.comm, s.h_out + align_up((uint64_t)n, 4), 16, st);  // flags + err word
+    HS_CUDA(cudaEventRecord(s.ev_c1, st));
+    s.called = true;
+  }
   int err = 0;
   bool got = false;
   for (int k : g->active) {

@@ -2,9 +2,10 @@
 tests/test_spmd_gpu.py under torch.distributed.run.  Each rank owns one stage of the tiny
 model (its own slice of the host image, its own GPU); activations and tokens cross over CUDA
 IPC peer mappings, consolidation pulls the peer's weights and KV over NVLink.  The group is
-created, run and destroyed ROUNDS times (as bench.py does per step).  Teacher-forced: the
-decode inputs are the oracle's tokens (read from argv[1]); each rank writes the logits it
-owns to argv[2] + f".{rank}.npz".  No oracle code runs here."""
+created, run and destroyed ROUNDS times (as bench.py does per step).  Rounds 0 and 2 are
+teacher-forced (decode inputs read from argv[1]) and write the logits each rank owns to
+argv[2] + f".{rank}.npz"; round 1 decodes with hs_decode_steps (2 micro-batches in flight
+through the stages, device feedback) and writes its tokens.  No oracle code runs here."""
 import os
 import sys
 
@@ -43,20 +44,26 @@ def main():
                      num_blocks=64, max_seqs=8, max_tokens=256, comm=comm)
         last = rank == world - 1
         g.load_stage_async(-1)
-        toks, logits = g.prefill([0, 1], prompts, want_logits=last)
-        out[f"r{r}_tok0"] = np.array(toks)
-        if last:
-            out[f"r{r}_log0"] = logits.copy()
-        for step in range(1, PRE + 1):
-            toks, logits = g.decode_step([0, 1], teacher[step - 1], want_logits=last)
-            out[f"r{r}_tok{step}"] = np.array(toks)
+        if r == 1:  # pipelined decode: 8 sequences as 2 micro-batches in flight (hs_decode_steps)
+            ids8 = list(range(8))
+            toks, _ = g.prefill(ids8, hsgen.prompts(8, 32, CFG["vocab"]))
+            out[f"r{r}_tok0"] = np.array(toks)
+            out[f"r{r}_ve"] = g.decode_steps(ids8, PRE, n_micro=2)
+        else:
+            toks, logits = g.prefill([0, 1], prompts, want_logits=last)
+            out[f"r{r}_tok0"] = np.array(toks)
             if last:
-                out[f"r{r}_log{step}"] = logits.copy()
+                out[f"r{r}_log0"] = logits.copy()
+            for step in range(1, PRE + 1):
+                toks, logits = g.decode_step([0, 1], teacher[step - 1], want_logits=last)
+                out[f"r{r}_tok{step}"] = np.array(toks)
+                if last:
+                    out[f"r{r}_log{step}"] = logits.copy()
         st = g.consolidate(0)
         out[f"r{r}_cons_bytes"] = np.array([st.weight_bytes, st.kv_bytes])
         if r % 2 == 0:  # the sources free their HBM before the target decodes on (else: at destroy)
             g.release_peer_memory()
-        if rank == 0:
+        if rank == 0 and r != 1:
             for step in range(PRE + 1, POST + 1):
                 toks, logits = g.decode_step([0, 1], teacher[step - 1], want_logits=True)
                 out[f"r{r}_tok{step}"] = np.array(toks)

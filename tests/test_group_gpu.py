@@ -514,8 +514,8 @@ def test_decode_steps_micro_batched_equals_stepwise(image, pp, n, m):
     lens = [5 + 3 * i for i in range(n)]
     prompts = [hsgen.tokens(700 + i, k, CFG["vocab"]) for i, k in enumerate(lens)]
     ids = list(range(n))
-    ga = make_group(image, pp, num_blocks=96, max_seqs=n)
-    gb = make_group(image, pp, num_blocks=96, max_seqs=n)
+    ga = make_group(image, pp, num_blocks=96, max_seqs=n, max_tokens=512)
+    gb = make_group(image, pp, num_blocks=96, max_seqs=n, max_tokens=512)
     for g in (ga, gb):
         g.load_stage_async(-1)
         g.prefill(ids, prompts)
