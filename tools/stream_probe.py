@@ -10,9 +10,9 @@ import torch  # noqa: E402,F401
 from paper_2502_15524_b200 import hs  # noqa: E402
 
 out = []
-for M, K in ((12288, 4096), (22016, 4096), (4096, 11008), (65536, 4096)):
+for M, K in ((65536, 4096), (131072, 4096)):  # 512 MB / 1 GB: larger than L2
     for slots in (8, 12):
-        for layout in (0, 1):
-            out.append(dict(M=M, K=K, slots=slots, layout=["row-major", "tiled"][layout],
-                            gbs=round(hs.stream_probe(layout, M, K, slots, 4), 1)))
+        for layout in (0, 1, 2, 3):
+            out.append(dict(M=M, K=K, slots=slots, layout=["row-major", "tiled", "row-major+mma", "tiled+mma"][layout],
+                            gbs=round(hs.stream_probe(layout, M, K, slots, 2), 1)))
             print(json.dumps(out[-1]), flush=True)
