@@ -120,15 +120,18 @@ __device__ __forceinline__ bool ds_it_next(const DsParams& p, DsIt& it) {
   return ds_it_fix(p, it);
 }
 
-template <int BN>
+template <int BN, int NC>
 struct DsCfg {
   static constexpr int A_BYTES = 128 * 64 * 2;
   static constexpr int B_BYTES = BN * 64 * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int VALS_BYTES = 128 * BN * 4;  // tile values for the RoPE pairing
-  static constexpr int ROPE_BYTES = BN * 64 * 8;   // cos/sin of the call's positions (head_dim <= 128)
+  // smem kept for the tile epilogues is sized by the tokens a launch can hold (NC == 1: one
+  // sequence), so single-sequence decode gets one more weight slot
+  static constexpr int VS = NC == 1 ? 1 : BN;      // token stride of the staged tile values
+  static constexpr int VALS_BYTES = 128 * VS * 4 < 64 ? 64 : 128 * VS * 4;  // RoPE pairing + Σx² scratch
+  static constexpr int ROPE_BYTES = VS * 64 * 8;   // cos/sin of the call's positions (head_dim <= 128)
   static constexpr int ATT_BYTES = (2 * 8 + 8 * 128) * 4 + 128;  // attention warp merge
-  static constexpr int XN_BYTES = BN <= 16 ? 10240 : 0;  // single-sequence decode: the normalised row (H <= 5120)
+  static constexpr int XN_BYTES = NC == 1 ? 10240 : 0;  // single-sequence decode: the normalised row (H <= 5120)
   static constexpr int MISC = 2048;
   static constexpr int FIT = (232448 - 1024 - MISC - VALS_BYTES - ROPE_BYTES - ATT_BYTES - XN_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = FIT > 12 ? 12 : FIT;
@@ -510,7 +513,7 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
         ds_part_sums<NC>(tws, np, n0, p.N, ml, a, BN);
 #pragma unroll
         for (int j = 0; j < NC; ++j)
-          if (n0 + j < p.N) vals[ml * BN + n0 + j] = __bfloat162float(__float2bfloat16_rn(a[j]));
+          if (n0 + j < p.N) vals[ml * DsCfg<BN, NC>::VS + n0 + j] = __bfloat162float(__float2bfloat16_rn(a[j]));
       }
       named_bar(1, 128);
       if (et == 0) DS_TR(TR_Q_VALS);
@@ -522,7 +525,7 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
         const int head = (r0 + ra) / p.hd;
         bf16* pool = p.pool + (size_t)l * p.pool_stride;
         for (int n = 0; n < p.N; ++n) {
-          const float a = vals[ra * BN + n], b = vals[rb * BN + n];
+          const float a = vals[ra * DsCfg<BN, NC>::VS + n], b = vals[rb * DsCfg<BN, NC>::VS + n];
           const int sl = s_slot[n];
           if (sl < 0 || sl >= p.nslots) continue;
           const size_t blk = (size_t)(sl >> 4), off = (size_t)(sl & 15);
@@ -590,7 +593,7 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
                   const __grid_constant__ CUtensorMap tw2, const __grid_constant__ CUtensorMap tw3,
                   const __grid_constant__ CUtensorMap tbn, const __grid_constant__ CUtensorMap tbo,
                   const __grid_constant__ CUtensorMap tba, const __grid_constant__ DsParams p) {
-  using C = DsCfg<BN>;
+  using C = DsCfg<BN, NC>;
   PDL_LAUNCH();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -991,7 +994,7 @@ void dstack_destroy(DstackState* s) {
 
 template <int BN, int NC>
 static hs_status launch_bn(DstackState* s, const DstackArgs& a, const DsParams& p, int bi, cudaStream_t st) {
-  using C = DsCfg<BN>;
+  using C = DsCfg<BN, NC>;
   static bool attr_set[64] = {};
   if (s->device < 64 && !attr_set[s->device]) {
     HS_CUDA(cudaFuncSetAttribute(dstack_kernel<BN, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -1102,10 +1105,10 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
 
 void warm_dstack() {
   cudaFuncAttributes at;
-  cudaFuncSetAttribute(dstack_kernel<16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, DsCfg<16>::SMEM);
-  cudaFuncSetAttribute(dstack_kernel<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, DsCfg<16>::SMEM);
-  cudaFuncSetAttribute(dstack_kernel<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, DsCfg<32>::SMEM);
-  cudaFuncSetAttribute(dstack_kernel<64, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, DsCfg<64>::SMEM);
+  cudaFuncSetAttribute(dstack_kernel<16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, DsCfg<16, 1>::SMEM);
+  cudaFuncSetAttribute(dstack_kernel<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, DsCfg<16, 8>::SMEM);
+  cudaFuncSetAttribute(dstack_kernel<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, DsCfg<32, 8>::SMEM);
+  cudaFuncSetAttribute(dstack_kernel<64, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, DsCfg<64, 8>::SMEM);
   cudaFuncGetAttributes(&at, dstack_kernel<16, 1>);
   cudaFuncGetAttributes(&at, dstack_kernel<16, 8>);
   cudaFuncGetAttributes(&at, dstack_kernel<32, 8>);
