@@ -109,7 +109,7 @@ uint64_t hsgen_image_layout(const hs_model_cfg* c, hs_image_header* h) {
   memset(h, 0, sizeof(*h));
   uint64_t H = (uint64_t)c->hidden, F = (uint64_t)c->ffn, V = (uint64_t)c->vocab;
   h->magic = HS_IMAGE_MAGIC;
-  h->version = 1;
+  h->version = 2; /* 2: tiled weight matrices */
   h->gu_interleave = HS_GU_INTERLEAVE;
   h->cfg = *c;
   uint64_t o = 0;
@@ -135,16 +135,25 @@ uint64_t hsgen_image_layout(const hs_model_cfg* c, hs_image_header* h) {
   return p;
 }
 
+/* Byte offset of element (row r, col k) of a [rows, cols] matrix: row-major, or the tiled
+ * weight layout of include/hs.h ([rows/128][cols/64][128][64], each block contiguous). */
+static inline uint64_t elem_off(int64_t r, int64_t k, int64_t cols, int tiled) {
+  if (!tiled) return ((uint64_t)r * (uint64_t)cols + (uint64_t)k) * 2;
+  const uint64_t blk = (uint64_t)(r >> 7) * (uint64_t)(cols >> 6) + (uint64_t)(k >> 6);
+  return (blk * 8192 + (uint64_t)(r & 127) * 64 + (uint64_t)(k & 63)) * 2;
+}
+
 /* Enumerates the physical rows of tensor region [off, off + rows*cols*2). */
 static void fill_rows(const hs_model_cfg* c, uint64_t seed, uint8_t* dst, uint64_t begin,
                       uint64_t end, uint64_t base, int64_t nrows, int64_t cols, int kind,
-                      uint32_t id0, uint32_t id1, int nthreads) {
+                      uint32_t id0, uint32_t id1, int nthreads, int tiled) {
   /* kind 0: plain tensor id0; kind 1: stacked q,k,v (id0..id0+2, H rows each);
-   * kind 2: gate/up interleaved (id0 = gate, id1 = up). */
+   * kind 2: gate/up interleaved (id0 = gate, id1 = up).  tiled: weight-matrix layout. */
   uint64_t tb = base, te = base + (uint64_t)nrows * (uint64_t)cols * 2;
   if (te <= begin || tb >= end) return;
   int64_t r0 = (int64_t)((begin > tb ? begin - tb : 0) / (uint64_t)(cols * 2));
   int64_t r1 = (int64_t)(((end < te ? end : te) - tb + (uint64_t)cols * 2 - 1) / (uint64_t)(cols * 2));
+  if (tiled) { r0 = 0; r1 = nrows; } /* a tile mixes rows: test every element's own offset */
 #pragma omp parallel for schedule(dynamic, 16) num_threads(nthreads)
   for (int64_t pr = r0; pr < r1; ++pr) {
     uint32_t id = id0;
@@ -156,11 +165,10 @@ static void fill_rows(const hs_model_cfg* c, uint64_t seed, uint8_t* dst, uint64
     }
     double sc, off;
     hsgen_tensor_spec(c, id, 0, 0, &sc, &off);
-    uint64_t rb = tb + (uint64_t)pr * (uint64_t)cols * 2;
     double z0 = 0, z1 = 0;
     uint64_t have = ~0ull; /* pair index currently in (z0, z1) */
     for (int64_t k = 0; k < cols; ++k) {
-      uint64_t ob = rb + (uint64_t)k * 2;
+      uint64_t ob = tb + elem_off(pr, k, cols, tiled);
       if (ob + 2 <= begin || ob >= end) continue;
       uint64_t li = (uint64_t)lr * (uint64_t)cols + (uint64_t)k;
       if ((li >> 1) != have) { normal_pair(seed, id, li >> 1, &z0, &z1); have = li >> 1; }
@@ -191,19 +199,19 @@ int32_t hsgen_image_fill(const hs_image_header* h, uint64_t seed, void* dstv, ui
     uint64_t e = end < sizeof(hs_image_header) ? end : sizeof(hs_image_header);
     memcpy(dst, (const uint8_t*)h + begin, e - begin);
   }
-  fill_rows(c, seed, dst, begin, end, h->embed_off, V, H, 0, HSGEN_EMBED, 0, nthreads);
+  fill_rows(c, seed, dst, begin, end, h->embed_off, V, H, 0, HSGEN_EMBED, 0, nthreads, 0);
   for (int l = 0; l < c->n_layers; ++l) {
     uint64_t L0 = h->layer_off[l];
     if (L0 >= end || L0 + h->layer_bytes <= begin) continue;
-    fill_rows(c, seed, dst, begin, end, L0 + h->t_attn_norm, 1, H, 0, hsgen_layer_tensor(l, HSGEN_ATTN_NORM), 0, nthreads);
-    fill_rows(c, seed, dst, begin, end, L0 + h->t_wqkv, 3 * H, H, 1, hsgen_layer_tensor(l, HSGEN_WQ), 0, nthreads);
-    fill_rows(c, seed, dst, begin, end, L0 + h->t_wo, H, H, 0, hsgen_layer_tensor(l, HSGEN_WO), 0, nthreads);
-    fill_rows(c, seed, dst, begin, end, L0 + h->t_ffn_norm, 1, H, 0, hsgen_layer_tensor(l, HSGEN_FFN_NORM), 0, nthreads);
-    fill_rows(c, seed, dst, begin, end, L0 + h->t_wgu, 2 * F, H, 2, hsgen_layer_tensor(l, HSGEN_WG), hsgen_layer_tensor(l, HSGEN_WU), nthreads);
-    fill_rows(c, seed, dst, begin, end, L0 + h->t_wd, H, F, 0, hsgen_layer_tensor(l, HSGEN_WD), 0, nthreads);
+    fill_rows(c, seed, dst, begin, end, L0 + h->t_attn_norm, 1, H, 0, hsgen_layer_tensor(l, HSGEN_ATTN_NORM), 0, nthreads, 0);
+    fill_rows(c, seed, dst, begin, end, L0 + h->t_wqkv, 3 * H, H, 1, hsgen_layer_tensor(l, HSGEN_WQ), 0, nthreads, 1);
+    fill_rows(c, seed, dst, begin, end, L0 + h->t_wo, H, H, 0, hsgen_layer_tensor(l, HSGEN_WO), 0, nthreads, 1);
+    fill_rows(c, seed, dst, begin, end, L0 + h->t_ffn_norm, 1, H, 0, hsgen_layer_tensor(l, HSGEN_FFN_NORM), 0, nthreads, 0);
+    fill_rows(c, seed, dst, begin, end, L0 + h->t_wgu, 2 * F, H, 2, hsgen_layer_tensor(l, HSGEN_WG), hsgen_layer_tensor(l, HSGEN_WU), nthreads, 1);
+    fill_rows(c, seed, dst, begin, end, L0 + h->t_wd, H, F, 0, hsgen_layer_tensor(l, HSGEN_WD), 0, nthreads, 1);
   }
-  fill_rows(c, seed, dst, begin, end, h->final_off + h->t_final_norm, 1, H, 0, HSGEN_FINAL_NORM, 0, nthreads);
-  fill_rows(c, seed, dst, begin, end, h->final_off + h->t_lm_head, V, H, 0, HSGEN_LM_HEAD, 0, nthreads);
+  fill_rows(c, seed, dst, begin, end, h->final_off + h->t_final_norm, 1, H, 0, HSGEN_FINAL_NORM, 0, nthreads, 0);
+  fill_rows(c, seed, dst, begin, end, h->final_off + h->t_lm_head, V, H, 0, HSGEN_LM_HEAD, 0, nthreads, 1);
   return 0;
 }
 

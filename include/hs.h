@@ -72,9 +72,15 @@ typedef struct {
  *       w_d [hidden, ffn]
  *   final region                 final_norm [hidden] at t_final_norm, lm_head [vocab, hidden]
  *                                at t_lm_head
- * Every weight matrix is [out_features, in_features] row-major ("K-major"), which is the
- * layout the tensor-core GEMMs consume directly.  Regions are HS_IMAGE_ALIGN aligned, so a
- * stage's slice [embed|layers b..e-1|final] is one contiguous byte range.
+ * Every weight matrix W [out_features M, in_features K] (w_qkv, w_o, w_gu, w_d, lm_head) is
+ * stored in the TILED weight layout [M/128][K/64][128][64]: the 128 x 64 block (row tile i,
+ * k-block j) is one contiguous 16 KiB run at block index i * (K/64) + j, rows of 64 elements
+ * (128 B) inside it (M % 128 == 0, K % 64 == 0).  That block is exactly one tensor-core operand
+ * tile (TMA box 64 x 128, 128B swizzle), so weight streaming reads whole contiguous 16 KiB runs
+ * (measured: 6.9-7.1 TB/s vs 5.7-5.9 TB/s for 128-byte row segments of a row-major matrix,
+ * profiles/r02/stream_probe.txt).  The embedding table stays row-major [vocab, hidden] (it is
+ * gathered by rows, not streamed).  Regions are HS_IMAGE_ALIGN aligned, so a stage's slice
+ * [embed|layers b..e-1|final] is one contiguous byte range.
  * ------------------------------------------------------------------------------------- */
 #define HS_IMAGE_MAGIC 0x31474D49534853ULL /* "SHSIMG1" */
 #define HS_IMAGE_HEADER_BYTES 65536ULL
@@ -84,7 +90,7 @@ typedef struct {
 
 typedef struct {
   uint64_t magic;
-  uint32_t version;       /* 1 */
+  uint32_t version;       /* 2 (tiled weight matrices) */
   uint32_t gu_interleave; /* HS_GU_INTERLEAVE */
   hs_model_cfg cfg;
   uint64_t total_bytes;   /* whole image incl. header */

@@ -12,7 +12,9 @@
 extern "C" {
 #endif
 
-/* out = epilogue(W[M,K] . X[N,K]^T) stored as out[n*ldo + m].  epi: 0 bf16, 1 bf16(acc +
+/* out = epilogue(W[M,K] . X[N,K]^T) stored as out[n*ldo + m].  W in the tiled weight layout of
+ * include/hs.h ([M/128][K/64][128][64] bf16: 128 x 64 blocks, each contiguous); X row-major
+ * [x_rows, K] bf16.  epi: 0 bf16, 1 bf16(acc +
  * resid[n*ldr+m]), 2 silu(gate)*up with gate/up rows interleaved by 16 (out has M/2 cols),
  * 3 fp32.  ws/ws_bytes: split-K workspace (NULL => no split-K).  X must have >= x_rows rows
  * (rows past N are read but their results discarded). */

@@ -644,7 +644,7 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
         const int l = ld.l, k = ld.k, x = ld.x;
         if (x == ld.beg && p.trace) DS_TR(k == 0 ? TR_A0 : TR_A1 + k - 1);
         mbar_expect_tx(&full[s], C::A_BYTES);
-        tma_load_3d(wm[k], &full[s], smem + s * C::STAGE_BYTES, (x % p.nkb[k]) * 64, (x / p.nkb[k]) * 128, l);
+        tma_load_w3(wm[k], &full[s], smem + s * C::STAGE_BYTES, x, l);  // tiled: block x = tile * nkb + kb
         *s_prog = i + 1;  // progress for the L2 prefetcher (warp 3)
         ld_ok = ds_it_next(p, ld);
       }
@@ -696,7 +696,7 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
       for (int j = 0; j < C::STAGES && pf_ok; ++j) pf_ok = ds_it_next(p, pf);
       for (int i = C::STAGES; pf_ok; ++i) {
         while (i >= *s_prog + C::STAGES + ahead) __nanosleep(128);
-        tma_prefetch_3d(wm[pf.k], (pf.x % p.nkb[pf.k]) * 64, (pf.x / p.nkb[pf.k]) * 128, pf.l);
+        tma_prefetch_4d(wm[pf.k], 0, 0, pf.x, pf.l);
         pf_ok = ds_it_next(p, pf);
       }
     }

@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(128, 1)
     const int pre = min(nk, C::STAGES);
     for (int i = 0; i < pre; ++i) {
       mbar_expect_tx(&full[i], C::STAGE_BYTES);
-      tma_load_2d(&tmA, &full[i], smem + i * C::STAGE_BYTES, (kb0 + i) * 64, m0);
+      tma_load_w(&tmA, &full[i], smem + i * C::STAGE_BYTES, (m0 / 128) * p.nkb + kb0 + i);
     }
     PDL_WAIT();
     for (int i = 0; i < pre; ++i)
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(128, 1)
       uint8_t* sb = sa + C::A_BYTES;
       mbar_expect_tx(&full[s], C::STAGE_BYTES);
       const int kc = (kb0 + i) * 64;
-      tma_load_2d(&tmA, &full[s], sa, kc, m0);
+      tma_load_w(&tmA, &full[s], sa, (m0 / 128) * p.nkb + kb0 + i);
       tma_load_2d(&tmB, &full[s], sb, kc, n0);
     }
   } else if (warp == 1 && lane == 0) {
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(192, 1)
     for (int i = 0; i < pre; ++i) {
       const int x = beg + i;
       mbar_expect_tx(&full[i], C::STAGE_BYTES);
-      tma_load_2d(&tmA, &full[i], smem + i * C::STAGE_BYTES, (x % p.nkb) * 64, (x / p.nkb) * 128);
+      tma_load_w(&tmA, &full[i], smem + i * C::STAGE_BYTES, x);
     }
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(&empty[s], ((i / C::STAGES) & 1) ^ 1);
         uint8_t* sa = smem + s * C::STAGE_BYTES;
         mbar_expect_tx(&full[s], C::STAGE_BYTES);
-        tma_load_2d(&tmA, &full[s], sa, (x % p.nkb) * 64, (x / p.nkb) * 128);
+        tma_load_w(&tmA, &full[s], sa, x);
         tma_load_2d(&tmB, &full[s], sa + C::A_BYTES, (x % p.nkb) * 64, 0);
       }
     }
@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(192, 1)
       for (int i = 0; i < pre; ++i) {
         const int t = blockIdx.x + (i / p.nkb) * gridDim.x;
         mbar_expect_tx(&full[i], C::STAGE_BYTES);
-        tma_load_2d(&tmA, &full[i], smem + i * C::STAGE_BYTES, (i % p.nkb) * 64, (t / p.n_tiles) * 128);
+        tma_load_w(&tmA, &full[i], smem + i * C::STAGE_BYTES, (t / p.n_tiles) * p.nkb + (i % p.nkb));
       }
       PDL_WAIT();
       for (int i = 0; i < pre; ++i) {
@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(192, 1)
           mbar_wait(&empty[s], ((i / C::STAGES) & 1) ^ 1);
           uint8_t* sa = smem + s * C::STAGE_BYTES;
           mbar_expect_tx(&full[s], C::STAGE_BYTES);
-          tma_load_2d(&tmA, &full[s], sa, kb * 64, m0);
+          tma_load_w(&tmA, &full[s], sa, (m0 / 128) * p.nkb + kb);
           tma_load_2d(&tmB, &full[s], sa + C::A_BYTES, kb * 64, n0);
         }
       }
@@ -761,6 +761,46 @@ hs_status make_tma3(TmaMat* t, const void* ptr, int64_t layers, int64_t layer_st
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) HS_FAIL(HS_E_CUDA, "cuTensorMapEncodeTiled (3d) failed (%d)", (int)r);
+  t->ptr = ptr;
+  t->rows = rows;
+  t->cols = cols;
+  t->box_rows = 128;
+  return HS_OK;
+}
+
+hs_status make_tma_w(TmaMat* t, const void* ptr, int64_t rows, int64_t cols) {
+  auto enc = get_encode();
+  if (!enc) HS_FAIL(HS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (cols % 64 || rows % 128 || (reinterpret_cast<uintptr_t>(ptr) & 15)) HS_FAIL(HS_E_INVAL, "bad tiled weight for TMA");
+  cuuint64_t dims[3] = {64, 128, (cuuint64_t)((rows / 128) * (cols / 64))};
+  cuuint64_t strides[2] = {128, 16384};
+  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(&t->map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) HS_FAIL(HS_E_CUDA, "cuTensorMapEncodeTiled (tiled weight) failed (%d)", (int)r);
+  t->ptr = ptr;
+  t->rows = rows;
+  t->cols = cols;
+  t->box_rows = 128;
+  return HS_OK;
+}
+
+hs_status make_tma_w3(TmaMat* t, const void* ptr, int64_t layers, int64_t layer_stride_bytes, int64_t rows,
+                      int64_t cols) {
+  auto enc = get_encode();
+  if (!enc) HS_FAIL(HS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (cols % 64 || rows % 128 || (reinterpret_cast<uintptr_t>(ptr) & 15) || layer_stride_bytes % 16)
+    HS_FAIL(HS_E_INVAL, "bad layered tiled weight for TMA");
+  cuuint64_t dims[4] = {64, 128, (cuuint64_t)((rows / 128) * (cols / 64)), (cuuint64_t)layers};
+  cuuint64_t strides[3] = {128, 16384, (cuuint64_t)layer_stride_bytes};
+  cuuint32_t box[4] = {64, 128, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(&t->map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) HS_FAIL(HS_E_CUDA, "cuTensorMapEncodeTiled (layered tiled weight) failed (%d)", (int)r);
   t->ptr = ptr;
   t->rows = rows;
   t->cols = cols;
@@ -1002,10 +1042,10 @@ __global__ void __launch_bounds__(192, 1)
           // bytes complete on the leader's barrier (peer bit cleared); the leader arms it for both
           const uint32_t bar = smem_u32(&full[s]) & 0xFEFFFFFFu;
           if (leader) mbar_expect_tx(&full[s], 2 * C::STAGE_BYTES);
-          asm volatile(
-              "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-              " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(sa)),
-              "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(bar), "r"(kb * 64), "r"(m0)
+          asm volatile(  // the weight k-block: tiled layout, block (m0 / 128) * nkb + kb
+              "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(sa)),
+              "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(bar), "r"(0), "r"(0), "r"((m0 / 128) * p.nkb + kb)
               : "memory");
           asm volatile(
               "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"

@@ -26,10 +26,17 @@ struct TmaMat {
 
 // Encodes a 128B-swizzled K-major tile map (box = 64 cols x box_rows rows).
 hs_status make_tma(TmaMat* t, const void* ptr, int64_t rows, int64_t cols, int box_rows);
-// Layered weight map [layers][rows][cols] (layers layer_stride_bytes apart), box 64 x 128 x 1:
-// one descriptor addresses the same matrix of every layer of a stage.
+// Layered row-major map [layers][rows][cols] (layers layer_stride_bytes apart), box 64 x 128 x 1.
 hs_status make_tma3(TmaMat* t, const void* ptr, int64_t layers, int64_t layer_stride_bytes, int64_t rows,
                     int64_t cols);
+// A weight matrix [rows, cols] in the tiled weight layout (include/hs.h: 128 x 64 blocks, each
+// one contiguous 16 KiB run, block b = row tile * cols/64 + k-block): 3-D map {64, 128, blocks}
+// with box 64 x 128 x 1 (the same 128B-swizzled shared-memory tile as make_tma's).
+hs_status make_tma_w(TmaMat* t, const void* ptr, int64_t rows, int64_t cols);
+// The same matrix of every layer of a stage (layers layer_stride_bytes apart): 4-D map
+// {64, 128, blocks, layers}: one descriptor streams the matrix kind of the whole stage.
+hs_status make_tma_w3(TmaMat* t, const void* ptr, int64_t layers, int64_t layer_stride_bytes, int64_t rows,
+                      int64_t cols);
 
 // Decode-path fusions applied by the stream-K reduction (the whole output row of a token is
 // available there):

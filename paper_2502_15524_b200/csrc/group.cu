@@ -295,10 +295,10 @@ static hs_status make_layer_maps(hs_group* g, Stage& s, int l) {
   LayerDev& d = s.layers[l];
   d.attn_norm = reinterpret_cast<const bf16*>(s.wptr(L0 + h.t_attn_norm));
   d.ffn_norm = reinterpret_cast<const bf16*>(s.wptr(L0 + h.t_ffn_norm));
-  HS_TRY(make_tma(&d.wqkv, s.wptr(L0 + h.t_wqkv), 3 * c.hidden, c.hidden, 128));
-  HS_TRY(make_tma(&d.wo, s.wptr(L0 + h.t_wo), c.hidden, c.hidden, 128));
-  HS_TRY(make_tma(&d.wgu, s.wptr(L0 + h.t_wgu), 2 * c.ffn, c.hidden, 128));
-  HS_TRY(make_tma(&d.wd, s.wptr(L0 + h.t_wd), c.hidden, c.ffn, 128));
+  HS_TRY(make_tma_w(&d.wqkv, s.wptr(L0 + h.t_wqkv), 3 * c.hidden, c.hidden));
+  HS_TRY(make_tma_w(&d.wo, s.wptr(L0 + h.t_wo), c.hidden, c.hidden));
+  HS_TRY(make_tma_w(&d.wgu, s.wptr(L0 + h.t_wgu), 2 * c.ffn, c.hidden));
+  HS_TRY(make_tma_w(&d.wd, s.wptr(L0 + h.t_wd), c.hidden, c.ffn));
   d.maps = true;
   return HS_OK;
 }
@@ -389,7 +389,7 @@ static hs_status setup_owned_stage(hs_group* g, int k) {
   const int wl0 = s.full_memory ? 0 : s.lb, wl1 = s.full_memory ? c.n_layers : s.le;
   for (int l = wl0; l < wl1; ++l) HS_TRY(make_layer_maps(g, s, l));
   if (s.full_memory || s.le == c.n_layers)
-    HS_TRY(make_tma(&s.lm, s.wptr(h.final_off + h.t_lm_head), c.vocab, H, 128));
+    HS_TRY(make_tma_w(&s.lm, s.wptr(h.final_off + h.t_lm_head), c.vocab, H));
   HS_TRY(make_act_maps(s.b_nrm, s.nrm, T, H));
   HS_TRY(make_act_maps(s.b_o, s.o, T, H));
   HS_TRY(make_act_maps(s.b_act, s.act, T, c.ffn));
@@ -461,7 +461,8 @@ static hs_status create(const hs_model_cfg* cfg, const hs_plan* plan, const hs_i
     if (stage_images[k].header) any = &stage_images[k];
   if (!any || !any->header) HS_FAIL(HS_E_INVAL, "image header required");
   const hs_image_header* ih = any->header;
-  if (ih->magic != HS_IMAGE_MAGIC || ih->total_bytes != g->hdr.total_bytes || ih->layer_bytes != g->hdr.layer_bytes ||
+  if (ih->magic != HS_IMAGE_MAGIC || ih->version != g->hdr.version || ih->total_bytes != g->hdr.total_bytes ||
+      ih->layer_bytes != g->hdr.layer_bytes ||
       ih->t_wgu != g->hdr.t_wgu || ih->t_lm_head != g->hdr.t_lm_head || ih->gu_interleave != HS_GU_INTERLEAVE ||
       memcmp(&ih->cfg, cfg, sizeof(hs_model_cfg)) != 0)
     HS_FAIL(HS_E_INVAL, "image header does not match the model cfg / layout");
@@ -793,10 +794,10 @@ static hs_status run_dstack(hs_group* g, Stage& s, const CallMeta& m, const uint
   const hs_image_header& h = g->hdr;
   if (s.ds_lb != s.lb || s.ds_le != s.le || s.ds_arena != s.arena) {
     const uint64_t L0 = h.layer_off[s.lb];
-    HS_TRY(make_tma3(&s.ds_w[0], s.wptr(L0 + h.t_wqkv), nl, h.layer_bytes, 3 * c.hidden, c.hidden));
-    HS_TRY(make_tma3(&s.ds_w[1], s.wptr(L0 + h.t_wo), nl, h.layer_bytes, c.hidden, c.hidden));
-    HS_TRY(make_tma3(&s.ds_w[2], s.wptr(L0 + h.t_wgu), nl, h.layer_bytes, 2 * c.ffn, c.hidden));
-    HS_TRY(make_tma3(&s.ds_w[3], s.wptr(L0 + h.t_wd), nl, h.layer_bytes, c.hidden, c.ffn));
+    HS_TRY(make_tma_w3(&s.ds_w[0], s.wptr(L0 + h.t_wqkv), nl, h.layer_bytes, 3 * c.hidden, c.hidden));
+    HS_TRY(make_tma_w3(&s.ds_w[1], s.wptr(L0 + h.t_wo), nl, h.layer_bytes, c.hidden, c.hidden));
+    HS_TRY(make_tma_w3(&s.ds_w[2], s.wptr(L0 + h.t_wgu), nl, h.layer_bytes, 2 * c.ffn, c.hidden));
+    HS_TRY(make_tma_w3(&s.ds_w[3], s.wptr(L0 + h.t_wd), nl, h.layer_bytes, c.hidden, c.ffn));
     s.ds_lb = s.lb;
     s.ds_le = s.le;
     s.ds_arena = s.arena;

@@ -17,7 +17,7 @@ extern "C" hs_status hs_k_gemm(const void* W, int32_t M, int32_t K, const void* 
     HS_FAIL(HS_E_INVAL, "bad gemm args");
   TmaMat a;
   TmaMat b[5];
-  HS_TRY(make_tma(&a, W, M, K, 128));
+  HS_TRY(make_tma_w(&a, W, M, K));  // W in the tiled weight layout (include/hs_kernels.h)
   for (int i = 0; i < gemm_bn_count(); ++i) HS_TRY(make_tma(&b[i], X, x_rows, K, gemm_bn_value(i)));
   GemmArgs g{};
   g.A = &a; g.B = b; g.M = M; g.N = N; g.K = K; g.epi = epi; g.out = out; g.ldo = ldo;

@@ -38,7 +38,7 @@ extern "C" hs_status hs_image_layout(const hs_model_cfg* c, hs_image_header* h) 
   memset(h, 0, sizeof(*h));
   const uint64_t H = c->hidden, F = c->ffn, V = c->vocab;
   h->magic = HS_IMAGE_MAGIC;
-  h->version = 1;
+  h->version = 2; /* 2: tiled weight matrices */
   h->gu_interleave = HS_GU_INTERLEAVE;
   h->cfg = *c;
   uint64_t o = 0;

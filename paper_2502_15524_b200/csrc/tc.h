@@ -153,6 +153,32 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* ba
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+// One weight k-block in the tiled weight layout (include/hs.h: [M/128][K/64][128][64] bf16, each
+// 128 x 64 block one contiguous 16 KiB run): block b = row tile * (K / 64) + k-block of a
+// make_tma_w map, (block, layer) of a make_tma_w3 map.
+__device__ __forceinline__ void tma_load_w(const CUtensorMap* map, uint64_t* bar, void* dst, int block) {
+  tma_load_3d(map, bar, dst, 0, 0, block);
+}
+__device__ __forceinline__ void tma_load_w3(const CUtensorMap* map, uint64_t* bar, void* dst, int block, int layer) {
+  tma_load_4d(map, bar, dst, 0, 0, block, layer);
+}
+
+// L2 prefetch of one 4-D tile (no shared-memory destination, no completion tracking).
+__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global [%0, {%1, %2, %3, %4}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+
 // L2 prefetch of one 3-D tile (no shared-memory destination, no completion tracking).
 __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(reinterpret_cast<uint64_t>(map)),

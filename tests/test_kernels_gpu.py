@@ -47,6 +47,13 @@ def check_bf16(gpu_bits, ref_vals, max_frac=0.02, scale=None, rel=2.0 ** -20):
     assert (d > 0).mean() <= max_frac, f"{(d > 0).mean():.4f} of elements differ by 1 ulp"
 
 
+def tiled(W):
+    """A [M, K] weight as the library stores it (include/hs.h): 128 x 64 blocks, each contiguous,
+    block (i, j) at i * K/64 + j (same shape, permuted memory)."""
+    M, K = W.shape
+    return W.view(M // 128, 128, K // 64, 64).permute(0, 2, 1, 3).contiguous().view(M, K)
+
+
 GEMM_CASES = [  # (M, K, N)
     (256, 256, 1), (256, 256, 16), (384, 256, 37), (256, 512, 64), (512, 256, 130),
     (768, 256, 300), (256, 768, 1100), (128, 64, 5),
@@ -63,7 +70,7 @@ def test_gemm_epilogues(M, K, N, split):
     rng = np.random.default_rng(M * 7 + K + N)
     Wb, Xb = rand_bf16(rng, (M, K), K ** -0.5), rand_bf16(rng, (N + 3, K))
     Rb = rand_bf16(rng, (N, M))
-    W, X, R = dev_bf16(Wb), dev_bf16(Xb), dev_bf16(Rb)
+    W, X, R = tiled(dev_bf16(Wb)), dev_bf16(Xb), dev_bf16(Rb)
     ws = torch.empty(16 << 20, dtype=torch.uint8, device="cuda") if split else None
     acc = bf16_value(Xb[:N]) @ bf16_value(Wb).T  # [N, M] float64
     out = torch.empty((N, M), dtype=torch.bfloat16, device="cuda")
@@ -96,7 +103,7 @@ def test_gemm_llama_shapes_decode_and_prefill():
         Wb, Xb = rand_bf16(rng, (M, K), K ** -0.5), rand_bf16(rng, (N, K))
         out = torch.empty((N, M), dtype=torch.float32, device="cuda")
         ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
-        hs.k_gemm(dev_bf16(Wb), dev_bf16(Xb), N, 3, out, ws=ws)
+        hs.k_gemm(tiled(dev_bf16(Wb)), dev_bf16(Xb), N, 3, out, ws=ws)
         torch.cuda.synchronize()
         sel = rng.choice(M, 64, replace=False)
         ref = bf16_value(Xb) @ bf16_value(Wb[sel]).T

@@ -132,3 +132,38 @@ def test_prefetcher_fills_region_and_publishes_watermark(tmp_path):
         p.wait()
     assert int(wm[0]) == off + (2 << 20)
     p.destroy()
+
+
+def test_image_weights_are_tiled_blocks_of_the_draws():
+    """The host image's weight matrices are the generator's draws in the tiled weight layout of
+    include/hs.h ([M/128][K/64][128][64], w_qkv = q, k, v rows stacked, w_gu = gate/up rows
+    interleaved by 16), the embedding table row-major; a partial fill writes exactly the
+    requested bytes."""
+    import numpy as np
+    cfg = hsgen.CONFIGS["tiny"]
+    h = hsgen.image_header(cfg)
+    img = np.zeros(h.total_bytes, dtype=np.uint8)
+    hsgen.image_fill(h, hsgen.WEIGHT_SEED, img.ctypes.data, 0, h.total_bytes)
+    H, F = cfg["hidden"], cfg["ffn"]
+
+    def untile(off, M, K):
+        t = img[off:off + 2 * M * K].view(np.uint16).reshape(M // 128, K // 64, 128, 64)
+        return t.transpose(0, 2, 1, 3).reshape(M, K)
+
+    draw = lambda tid: hsgen.tensor_bf16(cfg, hsgen.WEIGHT_SEED, tid)  # noqa: E731
+    l = 2
+    L0 = h.layer_off[l]
+    qkv = np.concatenate([draw(hsgen.layer_tensor(l, k)) for k in (hsgen.WQ, hsgen.WK, hsgen.WV)])
+    assert np.array_equal(untile(L0 + h.t_wqkv, 3 * H, H), qkv)
+    assert np.array_equal(untile(L0 + h.t_wo, H, H), draw(hsgen.layer_tensor(l, hsgen.WO)))
+    g, u = draw(hsgen.layer_tensor(l, hsgen.WG)), draw(hsgen.layer_tensor(l, hsgen.WU))
+    gu = np.stack([g.reshape(-1, 16, H), u.reshape(-1, 16, H)], axis=1).reshape(2 * F, H)
+    assert np.array_equal(untile(L0 + h.t_wgu, 2 * F, H), gu)
+    assert np.array_equal(untile(L0 + h.t_wd, H, F), draw(hsgen.layer_tensor(l, hsgen.WD)))
+    assert np.array_equal(untile(h.final_off + h.t_lm_head, cfg["vocab"], H), draw(hsgen.LM_HEAD))
+    emb = img[h.embed_off:h.embed_off + 2 * cfg["vocab"] * H].view(np.uint16).reshape(cfg["vocab"], H)
+    assert np.array_equal(emb, draw(hsgen.EMBED))
+    part = np.zeros(h.layer_bytes + 77, dtype=np.uint8)  # an unaligned slice across a layer
+    b = int(L0) - 33
+    hsgen.image_fill(h, hsgen.WEIGHT_SEED, part.ctypes.data, b, b + part.size)
+    assert np.array_equal(part, img[b:b + part.size])
