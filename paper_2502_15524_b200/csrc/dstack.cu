@@ -147,6 +147,9 @@ __device__ __constant__ int p_l2_ahead = 0;
 // Timing experiments only (HS_DSTACK_NOMMA=1, results garbage): skip the tensor-core MMAs, keep
 // every barrier, load and flag, to separate MMA issue/completion cost from the memory stream.
 __device__ __constant__ int p_nomma = 0;
+// L2 prefetch of each attention unit's cached K / V before the unit waits for its q, k, v tiles
+// (HS_DSTACK_KVPF=0 disables it: A/B)
+__device__ __constant__ int p_kv_prefetch = 1;
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
@@ -267,6 +270,19 @@ __device__ __forceinline__ void ds_attn_unit(const DsParams& p, int l, unsigned 
   const int* tab = p.tables + (size_t)i * p.max_blocks;
   // block ids of this warp's blocks (call metadata: independent of the flags, fetched first)
   const int my_blk = (b0 + warp + lane * DS_AWARPS < b1) ? tab[b0 + warp + lane * DS_AWARPS] : 0;
+  if (p_kv_prefetch && t >= 128) {
+    // warps 8-11 reach a layer's first unit while warps 4-7 still drain its QKV (they skip that
+    // epilogue): they request the unit's cached K / V slabs (4 KiB contiguous each) into L2, so
+    // the attention that follows QKV reads them from L2 instead of HBM (only the new token's
+    // k, v are produced by this layer; L2 stays coherent with the QKV epilogue's KV write)
+    const bf16* pl = p.pool + (size_t)l * p.pool_stride;
+    for (int j = t - 128; j < 2 * (b1 - b0); j += 128) {
+      int blk = tab[b0 + (j >> 1)];
+      if (blk < 0 || blk >= p.nblocks) blk = 0;
+      const bf16* slab = pl + (((size_t)blk * 2 + (j & 1)) * p.nh + h) * 16 * D;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(slab), "r"(16 * D * 2) : "memory");
+    }
+  }
   if (t < 3) wait_tag(p.f_qkv + (h * D) / 128 + t * (H / 128), tag);  // q, k, v tiles of head h
   named_bar(2, 256);
   if (p.trace && t == 0) DS_TR(TR_AT_FLAGS);
@@ -1072,6 +1088,9 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
       const char* e2 = getenv("HS_DSTACK_L2AHEAD");
       const int ahead = e2 ? atoi(e2) : 0;
       HS_CUDA(cudaMemcpyToSymbol(p_l2_ahead, &ahead, sizeof(ahead)));
+      const char* e4 = getenv("HS_DSTACK_KVPF");
+      const int kvpf = e4 ? atoi(e4) : 1;
+      HS_CUDA(cudaMemcpyToSymbol(p_kv_prefetch, &kvpf, sizeof(kvpf)));
       const char* e3 = getenv("HS_DSTACK_NOMMA");
       const int nomma = e3 ? atoi(e3) : 0;
       HS_CUDA(cudaMemcpyToSymbol(p_nomma, &nomma, sizeof(nomma)));
