@@ -774,24 +774,21 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
               }
             }
             __syncwarp();
-            // token row 0 of each k-block's tile (rows >= N are never drained); 4 k-blocks per
-            // warp pass, 8 lanes (128 bytes) each
-            const int grp = lane >> 3, gl = lane & 7;
-            for (int x0 = beg; x0 < end; x0 += 4, i += 4) {
-              const int x = x0 + grp, ii = i + grp;
-              const bool mine = x < end;
-              const int s = ii % C::STAGES;
-              if (mine && gl == 0) mbar_wait(&empty[s], ((ii / C::STAGES) & 1) ^ 1);
+            // token row 0 of each k-block's tile (rows >= N are never drained), one slot at a
+            // time, 8 lanes (128 bytes): a slot is completed the moment it is free, so the MMA
+            // never waits on later slots (a 4-slot batch here cost ~3 slots of ring depth)
+            for (int x = beg; x < end; ++x, ++i) {
+              const int s = i % C::STAGES;
+              if (lane == 0) mbar_wait(&empty[s], ((i / C::STAGES) & 1) ^ 1);
               __syncwarp();
-              if (mine) {
+              if (lane < 8) {
                 uint4* dst = reinterpret_cast<uint4*>(smem + s * C::STAGE_BYTES + C::A_BYTES);
-                dst[gl] = s_xn[(x % nkb) * 8 + gl];  // row 0: 16-byte chunk c at c ^ 0
+                dst[lane] = s_xn[(x % nkb) * 8 + lane];  // row 0: 16-byte chunk c at c ^ 0
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
               }
               __syncwarp();
-              if (mine && gl == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+              if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
             }
-            i -= (4 - (end - beg) % 4) % 4;  // the last pass may have covered fewer than 4 k-blocks
             continue;
           }
         } else if (k == 0 || k == 2) {  // the row norm feeding this GEMM: every CTA's slice written
