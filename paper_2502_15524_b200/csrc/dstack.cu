@@ -1068,7 +1068,11 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
       for (int i = 0; i < a.N; ++i) u += (size_t)a.nh * (((a.ctx[i] + 15) / 16 + ch - 1) / ch);
       return u;
     };
-    int ch = 1;
+    static const int min_ch = [] {  // A/B knob: fewer, longer units (HS_DSTACK_MINCH=64: one unit per head)
+      const char* e = getenv("HS_DSTACK_MINCH");
+      return e && atoi(e) > 0 ? std::min(atoi(e), DS_SPLIT) : 1;
+    }();
+    int ch = min_ch;
     while (ch < DS_SPLIT && units_of(ch) > (size_t)s->G) ++ch;
     if (units_of(ch) > s->attn_items_max) HS_FAIL(HS_E_INVAL, "dstack: context longer than the workspace was sized for");
     p.ch = ch;
