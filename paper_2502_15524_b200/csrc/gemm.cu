@@ -1252,7 +1252,11 @@ hs_status gemm(const GemmArgs& a, cudaStream_t st) {
         const long long pairs256 = (long long)(a.M / 256) * cdiv(a.N, 256);
         // only when the pairs fill less than half the clusters and K is long (down-proj): the
         // reduction's traffic (S x N x M x 4 B) outweighs the gain otherwise (measured)
-        for (int sk = 2; sk <= 4 && pairs256 * 2 <= G / 2 && a.K / 64 >= 128; ++sk) {
+        static const int split_min_kb = [] {  // A/B knob: K blocks needed before pairs split K
+          const char* e = getenv("HS_TP2_SPLIT_MINKB");
+          return e && atoi(e) > 0 ? atoi(e) : 128;
+        }();
+        for (int sk = 2; sk <= 4 && pairs256 * 2 <= G / 2 && a.K / 64 >= split_min_kb; ++sk) {
           if (!a.workspace || (uint64_t)sk * a.N * a.M * 4 > a.workspace_bytes) break;
           const double c = (double)cdiv(pairs256 * sk, G / 2) * 2.0 / kTp2Rate256 / sk + 0.1 * sk;
           if (c < best) { best = c; best_s = sk; }
