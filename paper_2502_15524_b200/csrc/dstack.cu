@@ -148,8 +148,8 @@ __device__ __constant__ int p_l2_ahead = 0;
 // every barrier, load and flag, to separate MMA issue/completion cost from the memory stream.
 __device__ __constant__ int p_nomma = 0;
 // L2 prefetch of each attention unit's cached K / V before the unit waits for its q, k, v tiles
-// (HS_DSTACK_KVPF=0 disables it: A/B)
-__device__ __constant__ int p_kv_prefetch = 1;
+// (HS_DSTACK_KVPF=1; measured r02: no gain at B = 1, 2 % slower at 13B B = 16: off)
+__device__ __constant__ int p_kv_prefetch = 0;
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
@@ -1090,7 +1090,7 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
       const int ahead = e2 ? atoi(e2) : 0;
       HS_CUDA(cudaMemcpyToSymbol(p_l2_ahead, &ahead, sizeof(ahead)));
       const char* e4 = getenv("HS_DSTACK_KVPF");
-      const int kvpf = e4 ? atoi(e4) : 1;
+      const int kvpf = e4 ? atoi(e4) : 0;
       HS_CUDA(cudaMemcpyToSymbol(p_kv_prefetch, &kvpf, sizeof(kvpf)));
       const char* e3 = getenv("HS_DSTACK_NOMMA");
       const int nomma = e3 ? atoi(e3) : 0;
