@@ -22,12 +22,21 @@ model's result"):
                     requests to that worker along with their key-value cache", PAPER.md:
                     602-606; "Blocks are gathered to the worker with whole model and placed
                     at different layers, according to which worker it comes from",
-                    PAPER.md:633-634).
+                    PAPER.md:633-634) and scale-up (every worker becomes an endpoint,
+                    PAPER.md:608-612).  ``Worker.attention_half`` / ``mlp_half`` are the two
+                    halves of ``layer_forward`` (the layer-level parity harness feeds each the
+                    GPU's own input).
   * ``plan``      — stage planning: contiguous layer split, stage byte counts, the paper's
                     predictors Eq. 1, Eq. 2, Eq. 5
-                     and server selection.
+                    (PAPER.md:579-584), server selection, Algorithm 1
+                    (PAPER.md:424-452), the Eq. 3 / Eq. 4 contention registry (PAPER.md:
+                    469-502) and the contention-aware placement of a cold start (R20).
 
-Pins (tests/test_oracle_*.py): HF transformers' Llama in float64 (architecture), torch fp64
-library routines, closed forms, brute-force dense recompute, PP-split == unsplit, the
-paper's printed sizes (12.5 GB / 24.2 GB, 8 KB/token) and SPEC.md's worked predictor values.
+Pins (tests/test_oracle_*.py, test_placement.py, test_layerwise_harness.py): HF transformers'
+Llama in float64 (architecture), torch fp64 library routines, closed forms, brute-force dense
+recompute, PP-split == unsplit, consolidation and scale-up == the single worker, the paper's
+printed sizes (12.5 GB / 24.2 GB, 8 KB/token), SPEC.md's worked predictor and Eq. 3/4 values,
+an exhaustive Alg. 1.  ``place_cold_start`` is our reading R20 written out step by step: pinned
+through its parts (Alg. 1's selection and Eq. 3/4, both pinned) and hand-checkable cases (a
+burst on equal links), not by a value the paper prints.
 """
