@@ -319,7 +319,7 @@ def run_ours(args):
         dec_gemm = [prof["decode_stack.decode"]]
         kname = ("dstack_kernel<16> (decode stack: all decoder layers of the stage in one persistent tcgen05/TMA "
                  "kernel per step; weights + KV read/write per launch)")
-        traffic_file = "r01_decode_stack_traffic.json"
+        traffic_file = "r02_decode_stack_traffic.json"
     else:
         dec_gemm = [v for k, v in prof.items() if k.startswith("gemm_") and k.endswith(".decode") and "lm_head" not in k]
         kname = "gemm_sk_kernel<16> (tcgen05 stream-K weight-streaming decode GEMM: qkv/o/gate_up/down, fused epilogues)"
