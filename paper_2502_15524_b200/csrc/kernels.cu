@@ -417,6 +417,8 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(
 
 void launch_attn_prefill(const bf16* q, const bf16* pool, const SeqDesc* seqs, int n_seqs, int max_nq,
                          const int* tables, int max_blocks, bf16* o, int nh, int d, int nblocks, cudaStream_t st) {
+  if (attn_tc_enabled())
+    return launch_attn_prefill_tc(q, pool, seqs, n_seqs, max_nq, tables, max_blocks, o, nh, d, nblocks, st);
   count_launch();
   dim3 grid((max_nq + PF_Q - 1) / PF_Q, nh, n_seqs);
   const size_t smem = (size_t)2 * 2 * PF_KC * d * 2;  // 2 buffers x (K, V) x 64 rows x d bf16
@@ -779,6 +781,7 @@ void warm_kernels() {
   cudaFuncGetAttributes(&a, rope_kv_kernel);
   cudaFuncGetAttributes(&a, attn_prefill_kernel<64>);
   cudaFuncGetAttributes(&a, attn_prefill_kernel<128>);
+  warm_attn_tc();
   cudaFuncGetAttributes(&a, attn_decode_kernel<64>);
   cudaFuncGetAttributes(&a, attn_decode_kernel<128>);
   cudaFuncGetAttributes(&a, argmax_kernel);
