@@ -249,10 +249,14 @@ __global__ void __launch_bounds__(128, 1) attn_prefill_tc_kernel(
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
 }
 
+// Off by default (HS_ATTN_TC=1 enables it): parity-green, but this synchronous two-pass design
+// measured 78 / 374 us per 7B layer at 512 / 2048 tokens against the mma.sync kernel's 41 / 183
+// (profiles/r02/attn_tc_ab.txt): every chunk serialises load -> MMA -> TMEM read -> softmax ->
+// MMA, K is loaded twice and V is transposed through scalar shared-memory stores.
 bool attn_tc_enabled() {
   static const bool on = [] {
     const char* e = getenv("HS_ATTN_TC");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return on;
 }
