@@ -8,12 +8,13 @@
 //   O += P V           tcgen05.mma (M = 128 queries, N = head_dim, K = 128 keys) into TMEM,
 //                      P as two bf16 halves (hi + lo: fp32 probabilities to ~2^-16, the numerics
 //                      contract's fp32 P, as the mma.sync kernel does).
-// Two passes over the chunks: the first finds each row's exact max m and the sum
-// l = Σ exp2(s - m) (rescaled when m grows), the second forms p = exp2(s - m) with the final m
-// and accumulates P V in TMEM without any rescaling; o = O / l, one bf16 rounding.  Operands
-// live in shared memory in the tcgen05 K-major 128B-swizzled layout: Q and K rows straight from
-// the q buffer / the paged pool, V transposed on the way in (V^T [head_dim][keys]), P written
-// row by row by its owner thread.  Deterministic; causal mask and ragged tails by position.
+// One pass with an online softmax per row (flash attention): each chunk's P V lands in a fresh
+// TMEM block and is added to the row's fp32 accumulator in registers, O = O * corr + P V; the
+// next chunk's K and V rows stream in with cp.async while this chunk computes; o = O / l, one
+// bf16 rounding.  Operands live in shared memory in the tcgen05 K-major 128B-swizzled layout:
+// Q and K rows straight from the q buffer / the paged pool, V transposed from its staged rows
+// (V^T [head_dim][keys]) while the tensor core computes S, P written row by row by its owner
+// thread.  Deterministic; causal mask and ragged tails by position.
 #include <cmath>
 #include <cstdlib>
 
@@ -30,10 +31,11 @@ struct TaCfg {
   static constexpr int KB = D / 64;                    // 64-wide k-blocks of head_dim
   static constexpr int Q_BYTES = KB * TA_Q * 128;      // Q: KB tiles [128 q][64 d]
   static constexpr int K_BYTES = KB * TA_KC * 128;     // K: KB tiles [128 keys][64 d]
+  static constexpr int VS_BYTES = KB * TA_KC * 128;    // V staging, same layout as K
   static constexpr int V_BYTES = 2 * D * 128;          // V^T: 2 tiles [D d][64 keys]
   static constexpr int P_BYTES = 2 * TA_Q * 128;       // P half: 2 tiles [128 q][64 keys]
-  static constexpr int SMEM = Q_BYTES + K_BYTES + V_BYTES + 2 * P_BYTES + 1024 + 64;
-  static constexpr uint32_t TMEM_COLS = 256;           // S: 128 columns, O: D columns (at 128)
+  static constexpr int SMEM = Q_BYTES + K_BYTES + VS_BYTES + V_BYTES + 2 * P_BYTES + 1024 + 64;
+  static constexpr uint32_t TMEM_COLS = 256;           // S: 128 columns, O block: D columns (at 128)
 };
 
 // 16-byte chunk c (0..7) of row r of a [rows][64] bf16 tile in the 128B-swizzled layout
@@ -49,10 +51,11 @@ __global__ void __launch_bounds__(128, 1) attn_prefill_tc_kernel(
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + C::Q_BYTES;
-  uint8_t* sV = sK + C::K_BYTES;
-  uint8_t* sP = sV + C::V_BYTES;  // [hi | lo]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + 2 * C::P_BYTES);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+  uint8_t* sVs = sK + C::K_BYTES;   // V rows as loaded
+  uint8_t* sV = sVs + C::VS_BYTES;  // V^T
+  uint8_t* sP = sV + C::V_BYTES;    // [hi | lo]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + 2 * C::P_BYTES);  // [0] S, [1] P V
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2);
   const int t = threadIdx.x, warp = t >> 5;
   const SeqDesc s = seqs[blockIdx.z];
   const int head = blockIdx.y;
@@ -60,7 +63,8 @@ __global__ void __launch_bounds__(128, 1) attn_prefill_tc_kernel(
   if (q0 >= s.n_q) return;
   const int H = nh * D;
   if (t == 0) {
-    mbar_init(bar, 1);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -68,7 +72,36 @@ __global__ void __launch_bounds__(128, 1) attn_prefill_tc_kernel(
                  "r"(C::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  const int* tab = tables + (size_t)s.table * max_blocks;
+  const int n_keys = s.pos0 + min(q0 + TA_Q, s.n_q);  // keys any row of the tile sees
+  const int n_chunks = (n_keys + TA_KC - 1) / TA_KC;
+  // K and V rows of chunk kc into sK / sVs (swizzled): thread t copies key kc + t with 16-byte
+  // cp.async (zero-filled past the keys), no registers held
+  auto issue = [&](int kc, bool k_part, bool v_part) {
+    const int j = kc + t;
+    const bf16* kp = pool;
+    int bytes = 0;
+    if (j < n_keys) {
+      int b = tab[j >> 4];
+      if (b < 0 || b >= nblocks) b = 0;
+      kp = pool + ((((size_t)b * 2) * nh + head) * 16 + (j & 15)) * D;
+      bytes = 16;
+    }
+#pragma unroll
+    for (int c = 0; c < D / 8; ++c) {
+      const uint32_t off = (c >> 3) * (TA_KC * 128) + sw128(t, c & 7);
+      if (k_part)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sK + off)), "l"(kp + c * 8), "r"(bytes)
+                     : "memory");
+      if (v_part)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sVs + off)),
+                     "l"(kp + (size_t)nh * 16 * D + c * 8), "r"(bytes)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
   PDL_WAIT();
+  issue(0, true, true);
   // Q rows: thread t loads query q0 + t (rows past n_q repeat the last row: never stored)
   const int qi = min(q0 + t, s.n_q - 1);
   const int pos = s.pos0 + q0 + t;  // this row's position (causal bound)
@@ -84,47 +117,21 @@ __global__ void __launch_bounds__(128, 1) attn_prefill_tc_kernel(
   const uint32_t tmem = *tmem_slot;
   const uint32_t tS = tmem, tO = tmem + 128;
   const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-  const int* tab = tables + (size_t)s.table * max_blocks;
-  const int n_keys = s.pos0 + min(q0 + TA_Q, s.n_q);  // keys any row of the tile sees
-  const int n_chunks = (n_keys + TA_KC - 1) / TA_KC;
   const float sl2 = 1.4426950408889634f / sqrtf((float)D);
   constexpr uint32_t idS = instr_desc<TA_KC>();  // M = 128, N = 128 keys
   constexpr uint32_t idO = instr_desc<D>();      // M = 128, N = head_dim
-  uint32_t phase = 0;
+  uint32_t ph_s = 0, ph_o = 0;
+  float m = -INFINITY, l = 0.f, acc[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) acc[d] = 0.f;
 
-  // K rows (and V^T columns) of chunk kc: thread t takes key kc + t (zeros past the keys)
-  auto load_chunk = [&](int kc, bool with_v) {
-    const int j = kc + t;
-    const uint4* kp = nullptr;
-    if (j < n_keys) {
-      int b = tab[j >> 4];
-      if (b < 0 || b >= nblocks) b = 0;
-      kp = reinterpret_cast<const uint4*>(pool + ((((size_t)b * 2) * nh + head) * 16 + (j & 15)) * D);
-    }
-#pragma unroll
-    for (int c = 0; c < D / 8; ++c) {
-      const uint4 kv = kp ? __ldcg(kp + c) : make_uint4(0, 0, 0, 0);
-      *reinterpret_cast<uint4*>(sK + (c >> 3) * (TA_KC * 128) + sw128(t, c & 7)) = kv;
-    }
-    if (with_v) {  // V^T: element (d, key t) of k-block t / 64, row d, chunk (t % 64) / 8
-      const uint4* vp = kp ? kp + (size_t)nh * 16 * D / 8 : nullptr;
-      const int kb = t >> 6, kl = t & 63;
-      uint8_t* vt = sV + kb * (D * 128);
-#pragma unroll 4
-      for (int c = 0; c < D / 8; ++c) {
-        const uint4 vv = vp ? __ldcg(vp + c) : make_uint4(0, 0, 0, 0);
-        const bf16* e = reinterpret_cast<const bf16*>(&vv);
-#pragma unroll
-        for (int x = 0; x < 8; ++x) {
-          const int d = c * 8 + x;
-          *reinterpret_cast<bf16*>(vt + sw128(d, kl >> 3) + (kl & 7) * 2) = e[x];
-        }
-      }
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
-  };
-  auto mma_S = [&]() {  // S = Q K^T over head_dim
-    if (t == 0) {
+  for (int ci = 0; ci < n_chunks; ++ci) {
+    const int kc = ci * TA_KC;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // cp.async (generic) -> tensor core
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();  // K_c and V_c rows landed; the previous chunk's TMEM reads are done
+    if (t == 0) {  // S = Q K^T over head_dim
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
       for (int kb = 0; kb < C::KB; ++kb) {
@@ -132,49 +139,41 @@ __global__ void __launch_bounds__(128, 1) attn_prefill_tc_kernel(
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) umma_bf16(tS, da + 2 * kk, db + 2 * kk, idS, (kb | kk) ? 1u : 0u);
       }
-      umma_commit(bar);
+      umma_commit(&bar[0]);
     }
-    mbar_wait(bar, phase);
-    phase ^= 1;
+    {  // V^T from the staged rows while the tensor core computes S (thread t: key t)
+      const int kbv = t >> 6, kl = t & 63;
+      uint8_t* vt = sV + kbv * (D * 128);
+#pragma unroll 2
+      for (int c = 0; c < D / 8; ++c) {
+        const uint4 vv = *reinterpret_cast<const uint4*>(sVs + (c >> 3) * (TA_KC * 128) + sw128(t, c & 7));
+        const bf16* e = reinterpret_cast<const bf16*>(&vv);
+#pragma unroll
+        for (int x = 0; x < 8; ++x) *reinterpret_cast<bf16*>(vt + sw128(c * 8 + x, kl >> 3) + (kl & 7) * 2) = e[x];
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();  // V^T complete; the staging buffer is free
+    if (ci + 1 < n_chunks) issue(kc + TA_KC, false, true);
+    mbar_wait(&bar[0], ph_s);
+    ph_s ^= 1;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  };
-
-  // ---- pass 1: row max m and l = sum exp2(s - m)
-  float m = -INFINITY, l = 0.f;
-  for (int ci = 0; ci < n_chunks; ++ci) {
-    const int kc = ci * TA_KC;
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");  // S reads before the next MMA
-    __syncthreads();  // the previous chunk's MMA has read sK
-    load_chunk(kc, false);
-    __syncthreads();
-    mma_S();
+    if (ci + 1 < n_chunks) issue(kc + TA_KC, true, false);  // sK was read by the finished MMA
+    // online softmax of this row's 128 scores: the chunk max first, then p = exp2(s - m)
+    float mx = m;
 #pragma unroll 1
     for (int c0 = 0; c0 < TA_KC; c0 += 32) {
       float v[32];
       tmem_ld32(tS + lane_base + c0, v);
-      float mx = m;
 #pragma unroll
       for (int x = 0; x < 32; ++x) {
         const int kp = kc + c0 + x;
-        v[x] = (kp <= pos && kp < n_keys) ? v[x] * sl2 : -INFINITY;
-        mx = fmaxf(mx, v[x]);
-      }
-      if (mx != -INFINITY) {
-        l *= exp2f(m - mx);  // m = -inf: l = 0 stays 0
-        m = mx;
-#pragma unroll
-        for (int x = 0; x < 32; ++x) l += exp2f(v[x] - m);
+        if (kp <= pos && kp < n_keys) mx = fmaxf(mx, v[x] * sl2);
       }
     }
-  }
-  // ---- pass 2: p = exp2(s - m) (final m), O += P V (no rescaling)
-  for (int ci = 0; ci < n_chunks; ++ci) {
-    const int kc = ci * TA_KC;
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();  // the previous chunk's MMAs have read sK / sV / sP
-    load_chunk(kc, true);
-    __syncthreads();
-    mma_S();
+    const float corr = (m == -INFINITY) ? 0.f : exp2f(m - mx);  // mx is finite: key kc <= pos
+    m = mx;
+    float ls = 0.f;
 #pragma unroll 1
     for (int c0 = 0; c0 < TA_KC; c0 += 32) {
       float v[32];
@@ -185,6 +184,7 @@ __global__ void __launch_bounds__(128, 1) attn_prefill_tc_kernel(
         const int kp = kc + c0 + x;
         const float p0 = (kp <= pos && kp < n_keys) ? exp2f(v[x] * sl2 - m) : 0.f;
         const float p1 = (kp + 1 <= pos && kp + 1 < n_keys) ? exp2f(v[x + 1] * sl2 - m) : 0.f;
+        ls += p0 + p1;
         const __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
         const float2 hf = __bfloat1622float2(h);
         const __nv_bfloat162 lw = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
@@ -200,10 +200,11 @@ __global__ void __launch_bounds__(128, 1) attn_prefill_tc_kernel(
         *reinterpret_cast<uint4*>(sP + C::P_BYTES + off) = make_uint4(lo[4 * g], lo[4 * g + 1], lo[4 * g + 2], lo[4 * g + 3]);
       }
     }
+    l = l * corr + ls;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (t == 0) {
+    if (t == 0) {  // this chunk's P V (hi + lo halves) into a fresh TMEM block
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
       for (int half = 0; half < 2; ++half)
@@ -212,36 +213,35 @@ __global__ void __launch_bounds__(128, 1) attn_prefill_tc_kernel(
           const uint64_t da = umma_desc_sw128(sP + half * C::P_BYTES + kb * (TA_Q * 128));
           const uint64_t db = umma_desc_sw128(sV + kb * (D * 128));
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            umma_bf16(tO, da + 2 * kk, db + 2 * kk, idO, (ci | half | kb | kk) ? 1u : 0u);
+          for (int kk = 0; kk < 4; ++kk) umma_bf16(tO, da + 2 * kk, db + 2 * kk, idO, (half | kb | kk) ? 1u : 0u);
         }
-      umma_commit(bar);
+      umma_commit(&bar[1]);
     }
-    mbar_wait(bar, phase);
-    phase ^= 1;
+    mbar_wait(&bar[1], ph_o);
+    ph_o ^= 1;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+    for (int c0 = 0; c0 < D; c0 += 32) {  // O = O * corr + P V
+      float v[32];
+      tmem_ld32(tO + lane_base + c0, v);
+#pragma unroll
+      for (int x = 0; x < 32; ++x) acc[c0 + x] = acc[c0 + x] * corr + v[x];
+    }
   }
   // ---- o = O / l (one bf16 rounding); rows past n_q are not stored
-  const float il = 1.f / l;
-  bf16* orow = o + (size_t)(s.q_start + qi) * H + head * D;
-  const bool store = q0 + t < s.n_q;
-#pragma unroll 1
-  for (int c0 = 0; c0 < D; c0 += 32) {
-    float v[32];
-    tmem_ld32(tO + lane_base + c0, v);
-    if (store) {
-      uint4* dst = reinterpret_cast<uint4*>(orow + c0);
+  if (q0 + t < s.n_q) {
+    const float il = 1.f / l;
+    uint4* dst = reinterpret_cast<uint4*>(o + (size_t)(s.q_start + qi) * H + head * D);
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        uint4 w;
-        uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+    for (int g = 0; g < D / 8; ++g) {
+      uint4 w;
+      uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
 #pragma unroll
-        for (int x = 0; x < 4; ++x) {
-          const __nv_bfloat162 b = __floats2bfloat162_rn(v[8 * g + 2 * x] * il, v[8 * g + 2 * x + 1] * il);
-          wp[x] = *reinterpret_cast<const uint32_t*>(&b);
-        }
-        dst[g] = w;
+      for (int x = 0; x < 4; ++x) {
+        const __nv_bfloat162 b = __floats2bfloat162_rn(acc[8 * g + 2 * x] * il, acc[8 * g + 2 * x + 1] * il);
+        wp[x] = *reinterpret_cast<const uint32_t*>(&b);
       }
+      dst[g] = w;
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
