@@ -196,6 +196,8 @@ def run_ours(args):
         r["loaded_bytes"] = g.load_stats(stage).bytes
         if consolidate and args.bg_load:
             g.load_background_async(0, args.chunk_mb << 20)
+        if consolidate and args.bg_pull:  # weights over NVLink before the pause: it moves KV only
+            g.pull_background_async(0)
         dev = 0.0
         t2 = time.perf_counter()
         if args.micro > 1 and pp > 1:  # pipelined decode: micro-batches through the stages at once
@@ -242,6 +244,7 @@ def run_ours(args):
             r["cons_bytes"] = st.weight_bytes + st.kv_bytes
             r["cons_w"], r["cons_kv"] = st.weight_bytes, st.kv_bytes
             r["cons_w_host"] = st.weight_bytes_host
+            r["cons_w_bg"] = st.weight_bytes_background
             if rank == 0:
                 dev2 = 0.0
                 t3 = time.perf_counter()
@@ -395,6 +398,7 @@ def run_ours(args):
             out["consolidation"] = {"mode": "scale-up (all-gather to every stage)" if args.scale_up else "scale-down to stage 0",
                                     "bytes": int(cb), "weight_bytes": int(steps[0]["cons_w"]), "kv_bytes": int(steps[0]["cons_kv"]),
                                     "weight_bytes_via_host_background": int(steps[0]["cons_w_host"]),
+                                    "weight_bytes_pulled_before_pause": int(steps[0].get("cons_w_bg", 0)),
                                     "seconds": round(cs, 5), "gbs": round(cb / cs / 1e9, 1),
                                     "frac_of_nvlink_900": round(cb / cs / 1e9 / NVLINK_GBS, 4),
                                     "pause_s": round(statistics.median(s["cons_pause"] for s in steps), 4)}
@@ -591,6 +595,9 @@ def main():
     ap.add_argument("--scale-up", action="store_true",
                     help="N>1: every stage becomes a standalone endpoint (scale-up consolidation) instead of "
                          "scale-down into stage 0")
+    ap.add_argument("--bg-pull", action="store_true",
+                    help="N>1: the target pulls the other stages' weights over NVLink in the background after "
+                         "the first token; the consolidation pause then moves KV only")
     ap.add_argument("--bg-load", action="store_true",
                     help="N>1: the target loads the other stages' weights over its own PCIe link in the "
                          "background after the first token (paper's mechanism); consolidation moves KV only")

@@ -330,6 +330,7 @@ typedef struct {
   double seconds;        /* device time of the migration (first copy start .. last end) */
   double pause_seconds;  /* host time from call entry to return (drain + migrate + rebind) */
   uint64_t weight_bytes_host; /* weight bytes that arrived by the background host load */
+  uint64_t weight_bytes_background; /* weight bytes pulled from peers before the call (hs_pull_background_async) */
 } hs_consolidate_stats;
 
 /* Paper-faithful background load ("the
@@ -340,6 +341,17 @@ typedef struct {
  * (and any region not covered) over NVLink.  The target's image must cover the whole model.
  * Errors: HS_E_INVAL (target not full-memory / not owned / image too small), HS_E_STATE. */
 hs_status hs_load_background_async(hs_group* g, int32_t target_stage, uint64_t chunk_bytes);
+
+/* The same background step with the other stages' HBM as the source ("allowing
+ * only one of them to fetch the unloaded model parts in background"): the full-memory target
+ * pulls every other stage's weight slice over NVLink with copy-engine peer copies on its
+ * low-priority copy stream (chunk_bytes per copy, 0 = 64 MiB) while the group keeps serving
+ * pipelined; hs_consolidate then waits for it and moves only the KV blocks, so its pause is the
+ * KV copy alone (stats.weight_bytes_background reports the pulled bytes).  Call it after the
+ * first hs_prefill has returned (every source slice is then resident; SPMD: on every rank, only
+ * the target's rank copies).  Errors: HS_E_INVAL (target not full-memory), HS_E_STATE (no call
+ * yet, or a background load already issued). */
+hs_status hs_pull_background_async(hs_group* g, int32_t target_stage, uint64_t chunk_bytes);
 
 /* Scale-down consolidation: drain in-flight work, copy the
  * weight regions the target lacks and gather the used KV blocks of every live sequence

@@ -96,7 +96,8 @@ struct Stage {
   cudaEvent_t ev_embed = nullptr, ev_final = nullptr, ev_l0 = nullptr, ev_l1 = nullptr;
   cudaEvent_t ev_c0 = nullptr, ev_c1 = nullptr;  // start / end of the last call on comp
   cudaEvent_t ev_bg0 = nullptr, ev_bg = nullptr; // background (host path) load start / end
-  bool bg_issued = false;
+  bool bg_issued = false;   // weights the target lacks are being loaded in the background
+  bool bg_from_peers = false;  // ... from the other stages' HBM over NVLink (else its host image)
   uint64_t bg_bytes = 0;
   bool called = false;
   std::vector<cudaEvent_t> ev_layer;
@@ -642,6 +643,38 @@ static hs_status load_background(hs_group* g, int tgt, uint64_t chunk) {
   }
   HS_CUDA(cudaEventRecord(T.ev_bg, T.copy));
   T.bg_issued = true;
+  return HS_OK;
+}
+
+// Background NVLink pull of the weight regions a full-memory target lacks (the paper's "allowing
+// only one of them to fetch the unloaded model parts in background", with the other
+// stages' HBM as the source): copy-engine peer copies on the target's low-priority copy stream
+// while the group keeps serving pipelined; a later consolidation then moves only the KV blocks.
+static hs_status pull_background(hs_group* g, int tgt, uint64_t chunk) {
+  if (tgt < 0 || tgt >= (int)g->st.size()) HS_FAIL(HS_E_INVAL, "bad stage %d", tgt);
+  Stage& T = g->st[tgt];
+  if (!T.owned) return HS_OK;  // SPMD: only the target's process works
+  if (!T.full_memory) HS_FAIL(HS_E_INVAL, "stage %d is not a full-memory worker", tgt);
+  if (!T.load_issued || !T.called) HS_FAIL(HS_E_STATE, "load and run one prefill first (the sources' slices must be resident)");
+  if (T.bg_issued) HS_FAIL(HS_E_STATE, "a background load of the target was already issued");
+  if (chunk == 0) chunk = 64ull << 20;
+  DeviceGuard dg(T.device);
+  HS_CUDA(cudaEventRecord(T.ev_bg0, T.copy));
+  T.bg_bytes = 0;
+  for (int k : g->active) {
+    if (k == tgt) continue;
+    Stage& S = g->st[k];
+    HS_TRY(open_peer_memory(g, S));
+    const uint8_t* src = S.arena + (S.slice_begin - S.arena_off0);
+    uint8_t* dst = T.wptr(S.slice_begin);
+    const uint64_t bytes = S.slice_end - S.slice_begin;
+    for (uint64_t o = 0; o < bytes; o += chunk)
+      HS_CUDA(cudaMemcpyAsync(dst + o, src + o, std::min(chunk, bytes - o), cudaMemcpyDeviceToDevice, T.copy));
+    T.bg_bytes += g->plan.stage_bytes[k];
+  }
+  HS_CUDA(cudaEventRecord(T.ev_bg, T.copy));
+  T.bg_issued = true;
+  T.bg_from_peers = true;
   return HS_OK;
 }
 
@@ -1581,8 +1614,9 @@ static hs_status consolidate(hs_group* g, int tgt, hs_consolidate_stats* out) {
     const int first = T.bg_issued ? T.cons_nw : 0;
     const int n = T.cons_nw + (int)kv.size() - first;
     if (T.bg_issued) {
-      HS_CUDA(cudaStreamWaitEvent(s2, T.ev_bg, 0));  // background host-path load must be complete
-      stats.weight_bytes_host = T.bg_bytes;
+      HS_CUDA(cudaStreamWaitEvent(s2, T.ev_bg, 0));  // the background load must be complete
+      if (T.bg_from_peers) stats.weight_bytes_background = T.bg_bytes;
+      else stats.weight_bytes_host = T.bg_bytes;
     }
     t_listed = clk::now();
     if (getenv("HS_DEBUG_CONS_SYNC")) {
@@ -2143,4 +2177,12 @@ extern "C" hs_status hs_decode_steps(hs_group* g, int32_t n_seqs, const int64_t*
                                      int32_t n_steps, int32_t n_micro, int32_t* out_tokens) {
   if (!g) HS_FAIL(HS_E_INVAL, "null group");
   return decode_steps(g, n_seqs, seq_ids, in_tokens, n_steps, n_micro, out_tokens);
+}
+
+extern "C" hs_status hs_pull_background_async(hs_group* g, int32_t target_stage, uint64_t chunk_bytes) {
+  if (!g) HS_FAIL(HS_E_INVAL, "null group");
+  if (g->dead) HS_FAIL(HS_E_CUDA, "group is dead");
+  if (std::find(g->active.begin(), g->active.end(), target_stage) == g->active.end())
+    HS_FAIL(HS_E_INVAL, "stage %d is not active", target_stage);
+  return pull_background(g, target_stage, chunk_bytes);
 }

@@ -104,7 +104,8 @@ class ProfEntry(C.Structure):
 
 class ConsolidateStats(C.Structure):
     _fields_ = [("weight_bytes", C.c_uint64), ("kv_bytes", C.c_uint64), ("seconds", C.c_double),
-                ("pause_seconds", C.c_double), ("weight_bytes_host", C.c_uint64)]
+                ("pause_seconds", C.c_double), ("weight_bytes_host", C.c_uint64),
+                ("weight_bytes_background", C.c_uint64)]
 
 
 # exported symbols (include/hs.h + include/hs_kernels.h); tests check every one is present
@@ -119,7 +120,7 @@ SYMBOLS = ["hs_image_layout", "hs_plan_stages", "hs_predict_ttft_eq1", "hs_predi
            "hs_links_settle", "hs_links_complete", "hs_links_pending", "hs_links_destroy",
            "hs_load_background_async", "hs_scale_up", "hs_release_peer_memory", "hs_debug_capture",
            "hs_debug_read_hidden", "hs_debug_set_prefill_chunking", "hs_prefetch_start", "hs_prefetch_wait",
-           "hs_prefetch_destroy", "hs_decode_steps", "hs_place_cold_start"]
+           "hs_prefetch_destroy", "hs_decode_steps", "hs_place_cold_start", "hs_pull_background_async"]
 
 _lib = None
 
@@ -180,6 +181,7 @@ def lib():
     L.hs_links_pending.argtypes = [VP, I32, I32, P(I32), P(C.c_double), P(C.c_int64)]
     L.hs_links_destroy.argtypes = [VP]
     L.hs_load_background_async.argtypes = [VP, I32, U64]
+    L.hs_pull_background_async.argtypes = [VP, I32, U64]
     L.hs_scale_up.argtypes = [VP, P(I32), I32, P(VP), P(ConsolidateStats)]
     L.hs_debug_capture.argtypes = [VP, I32]
     L.hs_debug_read_hidden.argtypes = [VP, I32, I32, I32, VP]
@@ -404,6 +406,10 @@ class Group:
 
     def load_background_async(self, target: int = 0, chunk_bytes: int = 0):
         check(lib().hs_load_background_async(self.h, target, chunk_bytes))
+
+    def pull_background_async(self, target: int = 0, chunk_bytes: int = 0):
+        """The target pulls the other stages' weight slices over NVLink in the background."""
+        check(lib().hs_pull_background_async(self.h, target, chunk_bytes))
 
     def load_stats(self, stage: int, wait: bool = True) -> LoadStats:
         s = LoadStats()

@@ -532,3 +532,40 @@ def test_decode_steps_micro_batched_equals_stepwise(image, pp, n, m):
     assert np.array_equal(toks2, ref2)
     ga.destroy()
     gb.destroy()
+
+
+@pytest.mark.parametrize("pp", [2, 4])
+def test_background_nvlink_pull_then_kv_only_consolidation(image, oracle_run, pp):
+    """PAPER.md:602 with the other stages' HBM as the source: the full-memory target pulls every
+    other stage's weight slice over NVLink (copy engines, low-priority stream) while the group
+    decodes pipelined (bitwise equal to PP=1 throughout); consolidation then moves only KV and
+    the target's weights equal the host image."""
+    prompts, hist, _ = oracle_run
+    g1 = make_group(image, 1)
+    g1.load_stage_async(-1)
+    g = make_group(image, pp)
+    g.load_stage_async(-1)
+    with pytest.raises(hs.HsError) as e:  # before any call: the sources may still be loading
+        g.pull_background_async(0)
+    assert e.value.code == 5
+    g.prefill([0, 1], prompts)
+    g1.prefill([0, 1], prompts)
+    g.pull_background_async(0, chunk_bytes=256 << 10)
+    for step in range(1, 9):
+        a = g.decode_step([0, 1], hist[step - 1][0], want_logits=True)
+        b = g1.decode_step([0, 1], hist[step - 1][0], want_logits=True)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    kv_before = {(s_, l): g.read_kv(s_, l, 0, 40) for s_ in (0, 1) for l in range(L)}
+    st = g.consolidate(0)
+    sb = hs.plan_stages(CFG, [dict(device=d, h2d_gbps=50.0, free_bytes=8 << 30) for d in range(pp)], pp, 1).as_dict()["stage_bytes"]
+    assert st.weight_bytes == 0 and st.weight_bytes_background == sum(sb) - sb[0] and st.kv_bytes > 0
+    for k, v in kv_before.items():
+        assert np.array_equal(g.read_kv(k[0], k[1], 0, 40), v)
+    h = hs.image_layout(CFG)
+    assert np.array_equal(g.read_weights(0, h.embed_off, h.total_bytes - h.embed_off), image.buf.numpy()[h.embed_off:])
+    for step in range(9, 20):
+        a = g.decode_step([0, 1], hist[step - 1][0], want_logits=True)
+        b = g1.decode_step([0, 1], hist[step - 1][0], want_logits=True)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    g.destroy()
+    g1.destroy()
