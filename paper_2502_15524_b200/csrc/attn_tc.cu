@@ -24,31 +24,35 @@
 namespace hs {
 
 constexpr int TA_Q = 128;   // queries per CTA
-constexpr int TA_KC = 128;  // keys per chunk
+constexpr int TA_KC = 64;   // keys per chunk: 112 KB of shared memory (D = 128), two CTAs per SM
 
 template <int D>
 struct TaCfg {
+  static constexpr int KK = TA_KC / 64;                // 64-wide k-blocks of a key chunk
   static constexpr int KB = D / 64;                    // 64-wide k-blocks of head_dim
   static constexpr int Q_BYTES = KB * TA_Q * 128;      // Q: KB tiles [128 q][64 d]
   static constexpr int K_BYTES = KB * TA_KC * 128;     // K: KB tiles [128 keys][64 d]
   static constexpr int VS_BYTES = KB * TA_KC * 128;    // V staging, same layout as K
-  static constexpr int V_BYTES = 2 * D * 128;          // V^T: 2 tiles [D d][64 keys]
-  static constexpr int P_BYTES = 2 * TA_Q * 128;       // P half: 2 tiles [128 q][64 keys]
-  static constexpr int SMEM = Q_BYTES + K_BYTES + VS_BYTES + V_BYTES + 2 * P_BYTES + 1024 + 64;
-  static constexpr uint32_t TMEM_COLS = 256;           // S: 128 columns, O block: D columns (at 128)
+  static constexpr int V_BYTES = KK * D * 128;         // V^T: KK tiles [D d][64 keys]
+  static constexpr int P_BYTES = KK * TA_Q * 128;      // P half: KK tiles [128 q][64 keys]
+  // no alignment slack: the dynamic window starts 1024-aligned (no static shared memory), which
+  // keeps two CTAs within one SM's 228 KB at D = 128
+  static constexpr int SMEM = Q_BYTES + K_BYTES + VS_BYTES + V_BYTES + 2 * P_BYTES + 64;
+  static constexpr uint32_t TMEM_COLS = 256;           // S: TA_KC columns, O block: D columns (at 128)
 };
 
 // 16-byte chunk c (0..7) of row r of a [rows][64] bf16 tile in the 128B-swizzled layout
 __device__ __forceinline__ uint32_t sw128(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
 
 template <int D>
-__global__ void __launch_bounds__(128, 1) attn_prefill_tc_kernel(
+__global__ void __launch_bounds__(128, TA_KC == 64 ? 2 : 1) attn_prefill_tc_kernel(
     const bf16* __restrict__ q, const bf16* __restrict__ pool, const SeqDesc* __restrict__ seqs,
     const int* __restrict__ tables, int max_blocks, bf16* __restrict__ o, int nh, int nblocks) {
   using C = TaCfg<D>;
   PDL_LAUNCH();
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if (threadIdx.x == 0 && (smem_u32(smem) & 1023)) __trap();  // the SW128 tiles need 1024-byte alignment
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + C::Q_BYTES;
   uint8_t* sVs = sK + C::K_BYTES;   // V rows as loaded
@@ -77,8 +81,11 @@ __global__ void __launch_bounds__(128, 1) attn_prefill_tc_kernel(
   const int n_chunks = (n_keys + TA_KC - 1) / TA_KC;
   // K and V rows of chunk kc into sK / sVs (swizzled): thread t copies key kc + t with 16-byte
   // cp.async (zero-filled past the keys), no registers held
+  constexpr int TPK = 128 / TA_KC;            // threads per key row
+  constexpr int CPT = (D / 8) / TPK;           // 16-byte chunks per thread and row
+  const int krow = t % TA_KC, cpart = t / TA_KC;
   auto issue = [&](int kc, bool k_part, bool v_part) {
-    const int j = kc + t;
+    const int j = kc + krow;
     const bf16* kp = pool;
     int bytes = 0;
     if (j < n_keys) {
@@ -88,8 +95,9 @@ __global__ void __launch_bounds__(128, 1) attn_prefill_tc_kernel(
       bytes = 16;
     }
 #pragma unroll
-    for (int c = 0; c < D / 8; ++c) {
-      const uint32_t off = (c >> 3) * (TA_KC * 128) + sw128(t, c & 7);
+    for (int cc = 0; cc < CPT; ++cc) {
+      const int c = cpart * CPT + cc;
+      const uint32_t off = (c >> 3) * (TA_KC * 128) + sw128(krow, c & 7);
       if (k_part)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sK + off)), "l"(kp + c * 8), "r"(bytes)
                      : "memory");
@@ -118,7 +126,7 @@ __global__ void __launch_bounds__(128, 1) attn_prefill_tc_kernel(
   const uint32_t tS = tmem, tO = tmem + 128;
   const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
   const float sl2 = 1.4426950408889634f / sqrtf((float)D);
-  constexpr uint32_t idS = instr_desc<TA_KC>();  // M = 128, N = 128 keys
+  constexpr uint32_t idS = instr_desc<TA_KC>();  // M = 128, N = TA_KC keys
   constexpr uint32_t idO = instr_desc<D>();      // M = 128, N = head_dim
   uint32_t ph_s = 0, ph_o = 0;
   float m = -INFINITY, l = 0.f, acc[D];
@@ -141,12 +149,13 @@ __global__ void __launch_bounds__(128, 1) attn_prefill_tc_kernel(
       }
       umma_commit(&bar[0]);
     }
-    {  // V^T from the staged rows while the tensor core computes S (thread t: key t)
-      const int kbv = t >> 6, kl = t & 63;
+    {  // V^T from the staged rows while the tensor core computes S (key krow, this thread's chunks)
+      const int kbv = krow >> 6, kl = krow & 63;
       uint8_t* vt = sV + kbv * (D * 128);
 #pragma unroll 2
-      for (int c = 0; c < D / 8; ++c) {
-        const uint4 vv = *reinterpret_cast<const uint4*>(sVs + (c >> 3) * (TA_KC * 128) + sw128(t, c & 7));
+      for (int cc = 0; cc < CPT; ++cc) {
+        const int c = cpart * CPT + cc;
+        const uint4 vv = *reinterpret_cast<const uint4*>(sVs + (c >> 3) * (TA_KC * 128) + sw128(krow, c & 7));
         const bf16* e = reinterpret_cast<const bf16*>(&vv);
 #pragma unroll
         for (int x = 0; x < 8; ++x) *reinterpret_cast<bf16*>(vt + sw128(c * 8 + x, kl >> 3) + (kl & 7) * 2) = e[x];
@@ -209,7 +218,7 @@ __global__ void __launch_bounds__(128, 1) attn_prefill_tc_kernel(
 #pragma unroll
       for (int half = 0; half < 2; ++half)
 #pragma unroll
-        for (int kb = 0; kb < 2; ++kb) {
+        for (int kb = 0; kb < C::KK; ++kb) {
           const uint64_t da = umma_desc_sw128(sP + half * C::P_BYTES + kb * (TA_Q * 128));
           const uint64_t db = umma_desc_sw128(sV + kb * (D * 128));
 #pragma unroll
