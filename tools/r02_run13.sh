@@ -9,4 +9,4 @@ for V in "HS_ATTN_TC=1" "HS_ATTN_TC=0"; do
   env $V timeout 300 python tools/prefill_prof.py 512 >> gpurun_out/exp13.txt 2>&1
   env $V timeout 300 python tools/prefill_prof.py 2048 >> gpurun_out/exp13.txt 2>&1
 done
-HS_ATTN_TC=1 timeout 1200 python -m pytest tests/test_fullsize_gpu.py -q -rA --timeout 1000 -k "7b_layerwise and 1" > gpurun_out/gputest13b.log 2>&1; echo "pytest rc=$?" >> gpurun_out/gputest13b.log
+true
