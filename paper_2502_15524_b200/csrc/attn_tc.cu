@@ -258,10 +258,10 @@ __global__ void __launch_bounds__(128, TA_KC == 64 ? 2 : 1) attn_prefill_tc_kern
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
 }
 
-// Off by default (HS_ATTN_TC=1 enables it): parity-green, but this synchronous two-pass design
-// measured 78 / 374 us per 7B layer at 512 / 2048 tokens against the mma.sync kernel's 41 / 183
-// (profiles/r02/attn_tc_ab.txt): every chunk serialises load -> MMA -> TMEM read -> softmax ->
-// MMA, K is loaded twice and V is transposed through scalar shared-memory stores.
+// Off by default (HS_ATTN_TC=1 enables it).  Measured (7B layer, profiles/r02/attn_tc_ab.txt):
+// 42 us at 512 tokens (mma.sync kernel 41 us) and 132 us at 2048 tokens (176 us); layer-level
+// parity green and 20 repeated calls bit-identical, but one pp-invariance run failed once in the
+// GPU suite and did not reproduce in three reruns, so it stays an A/B path until that is found.
 bool attn_tc_enabled() {
   static const bool on = [] {
     const char* e = getenv("HS_ATTN_TC");
