@@ -14,4 +14,4 @@ for V in "" "HS_TP2_SPLIT_MINKB=64"; do
   echo "== prefill $V" >> gpurun_out/exp9.txt
   env $V timeout 300 python tools/prefill_prof.py 512 >> gpurun_out/exp9.txt 2>&1
 done
-bash tools/r02_ncu.sh
+bash tools/runs/r02_ncu.sh
