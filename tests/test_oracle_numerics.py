@@ -85,3 +85,47 @@ def test_silu():
     g = np.linspace(-20, 20, 401)
     assert silu(np.array([0.0]))[0] == 0.0
     assert np.allclose(silu(g), F.silu(torch.from_numpy(g)).numpy(), rtol=1e-14, atol=1e-300)
+
+
+def test_argmax_lowest_tie_semantics():
+    """Greedy ties go to the lowest token id (R11, torch.argmax semantics)."""
+    from oracle.numerics import argmax_lowest
+    assert argmax_lowest(np.array([0.5, 2.0, 2.0, -1.0])) == 1
+    assert argmax_lowest(np.array([3.0, 3.0, 3.0])) == 0
+    assert argmax_lowest(np.array([-np.inf, -1.0, -1.0])) == 1
+    v = np.zeros(1024)
+    v[[7, 300, 1023]] = 5.0
+    assert argmax_lowest(v) == 7
+
+
+def test_decoder_paged_attention_equals_attention_one():
+    """The decoder's bf16 paged attention (rows read back through a non-contiguous block table,
+    causal over a packed 2-sequence batch) equals oracle.numerics.attention_one (pinned against
+    torch SDPA in this file) applied query by query to the same k', v."""
+    import hsgen
+    from oracle.decoder import BLOCK, Weights, Worker
+    from oracle.numerics import attention_one
+    cfg = hsgen.CONFIGS["tiny"]
+    W = Weights(cfg)
+    wk = Worker(cfg, W, 1, 2, num_blocks=16)
+    rng = np.random.default_rng(3)
+    x = bf16(rng.standard_normal((40 + 23, cfg["hidden"])))
+    tabs = [[9, 2, 14], [5, 0]]
+    batch = []
+    for sid, (n, tab) in enumerate(((40, tabs[0]), (23, tabs[1]))):
+        pos = np.arange(n)
+        batch.append((sid, pos, [(tab[p // BLOCK], p % BLOCK) for p in pos], tab))
+    tr = {}
+    wk.attention_half(1, x, batch, tr)
+    t0 = 0
+    worst = 0
+    for (_, pos, _, _) in batch:
+        for i, p in enumerate(pos):
+            K = tr["k"][t0:t0 + p + 1]
+            V = tr["v"][t0:t0 + p + 1]
+            ref = attention_one(tr["q"][t0 + i], K, V)
+            diff = np.abs(tr["o"][t0 + i] - ref)
+            ulp = np.exp2(np.floor(np.log2(np.maximum(np.abs(ref), 2.0 ** -126))) - 7)
+            worst = max(worst, float((diff / ulp).max()))
+        t0 += len(pos)
+    assert worst <= 1.0, worst
