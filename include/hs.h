@@ -318,7 +318,8 @@ hs_status hs_decode_step(hs_group* g, int32_t n_seqs, const int64_t* seq_ids,
  * on the ranks owning the first and the last stage only.  Afterwards the group is in the same
  * state as after n_steps hs_decode_step calls (device feedback continues).  Each micro-batch's
  * decode stack launch sees only its own sequences, so its per-sequence results equal an
- * hs_decode_step call on the same micro-batch.  Errors as hs_decode_step. */
+ * hs_decode_step call on the same micro-batch.  Layer-boundary capture (hs_debug_capture) does not
+ * record this call.  Errors as hs_decode_step. */
 hs_status hs_decode_steps(hs_group* g, int32_t n_seqs, const int64_t* seq_ids, const int32_t* in_tokens,
                           int32_t n_steps, int32_t n_micro, int32_t* out_tokens);
 

@@ -1351,6 +1351,13 @@ static hs_status decode_steps(hs_group* g, int n, const int64_t* ids, const int3
   if (!feedback)
     for (int i = 0; i < n; ++i)
       if (in_tokens[i] < 0 || in_tokens[i] >= c.vocab) HS_FAIL(HS_E_INVAL, "token id out of range");
+  // layer-boundary capture covers hs_prefill / hs_decode_step calls only (one row layout per call)
+  struct CaptureOff {
+    hs_group* g; bool was;
+    ~CaptureOff() { g->capture = was; }
+  } capture_off{g, g->capture};
+  g->capture = false;
+  g->cap_rowmap.clear();
   // micro-batches on 4-sequence boundaries (token hand-offs move 16-byte words)
   const int quads = (n + 3) / 4;
   const int m = std::max(1, std::min({m_req, quads, kMaxMicro}));
