@@ -1363,16 +1363,10 @@ static hs_status decode_steps(hs_group* g, int n, const int64_t* ids, const int3
   const int m = std::max(1, std::min({m_req, quads, kMaxMicro}));
   std::vector<int> s0(m + 1);
   for (int j = 0; j <= m; ++j) s0[j] = std::min(n, 4 * (int)((int64_t)quads * j / m));
-  std::vector<int> ctx0(n);
-  for (int i = 0; i < n; ++i) {
-    ctx0[i] = g->seqs[ids[i]].ctx;
-    HS_TRY(alloc_tokens(g, ids[i], n_steps));  // every step's slot, up front (blocks checked above)
-  }
   const int first = g->active.front(), last = g->active.back();
   const unsigned ep_prev = g->epoch;
   const unsigned base = g->epoch;
   auto ep = [&](int t, int j) { return base + (unsigned)(t * m + j) + 1; };
-  g->epoch += (unsigned)(n_steps * m);
   const int H = c.hidden;
   const size_t row_ints = align_up((size_t)n, 4);
   CallMeta mx;
@@ -1387,6 +1381,13 @@ static hs_status decode_steps(hs_group* g, int n, const int64_t* ids, const int3
     if (!s.owned) continue;
     if (!s.load_issued) HS_FAIL(HS_E_STATE, "stage %d: no load issued", s.idx);
     HS_TRY(ve_reserve(g, s, g->ve[s.idx], slot_bytes, R, (size_t)n_steps * row_ints));
+  }
+  g->epoch += (unsigned)(n_steps * m);  // (no failure path left before the items are enqueued)
+  // every step's KV slot, up front (capacity checked above; nothing can fail after this but CUDA)
+  std::vector<int> ctx0(n);
+  for (int i = 0; i < n; ++i) {
+    ctx0[i] = g->seqs[ids[i]].ctx;
+    HS_TRY(alloc_tokens(g, ids[i], n_steps));
   }
   int item = 0;
   for (int t = 0; t < n_steps; ++t)
