@@ -341,8 +341,14 @@ def run_ours(args):
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if not pk.get("_fallback") else "fallback"}
     try:  # dram__bytes_read + write per launch of this kernel from the committed ncu --set full capture
         tr = json.load(open(os.path.join(ROOT, "profiles", traffic_file)))
-        roof["traffic"] = round(tr["mean_bytes_per_launch"])
-        roof["traffic_source"] = tr["source"]
+        alg = tr.get("algorithmic_bytes_per_launch")
+        bpl = roof["bytes_per_launch"]
+        if alg and bpl and abs(bpl - alg) <= 0.02 * alg:  # the captured launch is this workload's launch
+            roof["traffic"] = round(tr["mean_bytes_per_launch"])
+            roof["traffic_source"] = tr["source"]
+        else:
+            roof["traffic_note"] = ("no ncu --set full capture of this workload's launch (the committed one, " +
+                                    tr["source"] + ", is " + tr["launches"][0] + ")")
     except Exception:  # noqa
         pass
     pre_gemm = [v for k, v in prof.items() if k.startswith("gemm_") and k.endswith(".prefill")]

@@ -59,6 +59,11 @@ struct DsParams {
   int ch;
   float* ws_attn;
   unsigned *c_tile[4], *c_ih, *c_h, *f_qkv, *f_attn, *f_gu;
+  // single-sequence decode with a split context (N = 1, nsp1 = splits per head >= 2): each unit
+  // publishes its partial on f_unit[u] and the O GEMM's activation producer merges the splits of
+  // a k-block's head itself (no last-unit merge, no o round trip); 0 = the merge in the units
+  int nsp1;
+  unsigned* f_unit;
   // distributed row norms: residual tiles publish sum-of-squares partials ssq[tile][64] and
   // bump c_rows (cumulative); every CTA then normalises its column slice and bumps c_norm
   // (cumulative).  Targets are launch bases + counts (wrap-safe compares).
@@ -396,6 +401,13 @@ __device__ __forceinline__ void ds_attn_unit(const DsParams& p, int l, unsigned 
     orow[t] = __float2bfloat16_rn(A / L);
   }
   named_bar(2, 256);
+  if (p.nsp1) {  // the O GEMM's producer merges: publish this split's partial and leave
+    if (t == 0) {
+      if (p.trace) DS_TR(TR_AT_END);
+      publish(p.f_unit + u, tag);
+    }
+    return;  // sm is free: every read of it precedes the barrier above
+  }
   // one arrival per unit on the head's counter; the last unit of the head merges the splits
   // of every sequence (split order) and publishes the head
   if (t == 0) {
@@ -791,6 +803,40 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
             }
             continue;
           }
+          if (k == 1 && p.nsp1) {
+            // split-context decode: the splits of each k-block's head are merged here, in split
+            // order (the arithmetic of the units' last-arriver merge), into row 0 of the slot;
+            // lane l owns columns 2l, 2l + 1 of the k-block
+            const int D = p.hd, nsp = p.nsp1;
+            for (int x = beg; x < end; ++x, ++i) {
+              const int kc = (x % nkb) * 64, h = kc / D, d = kc % D + 2 * lane;
+              for (int q = lane; q < nsp; q += 32) wait_tag(p.f_unit + h * nsp + q, tag);
+              __syncwarp();
+              if (p.trace && lane == 0 && x == beg) DS_TR(1);
+              const float* w0 = p.ws_attn + (size_t)(h * nsp) * (D + 4);
+              float MM = -INFINITY;
+              for (int q = 0; q < nsp; ++q) MM = fmaxf(MM, __ldcg(w0 + (size_t)q * (D + 4)));
+              float LL = 0.f, A0 = 0.f, A1 = 0.f;
+              for (int q = 0; q < nsp; ++q) {
+                const float* wq = w0 + (size_t)q * (D + 4);
+                const float ms = __ldcg(wq);
+                const float f = ms == -INFINITY ? 0.f : exp2f(ms - MM);
+                LL += __ldcg(wq + 1) * f;
+                A0 += __ldcg(wq + 4 + d) * f;
+                A1 += __ldcg(wq + 5 + d) * f;
+              }
+              const __nv_bfloat162 ov = __floats2bfloat162_rn(A0 / LL, A1 / LL);
+              const int s = i % C::STAGES;
+              if (lane == 0) mbar_wait(&empty[s], ((i / C::STAGES) & 1) ^ 1);
+              __syncwarp();
+              // row 0 of the SW128 tile: byte 4 l of the row is chunk l / 4 at position l / 4
+              reinterpret_cast<__nv_bfloat162*>(smem + s * C::STAGE_BYTES + C::A_BYTES)[lane] = ov;
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              __syncwarp();
+              if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+            }
+            continue;
+          }
         } else if (k == 0 || k == 2) {  // the row norm feeding this GEMM: every CTA's slice written
           if (lane == 0) wait_tag(p.c_norm, p.base_norm + (unsigned)(2 * l + (k == 0 ? 1 : 2)) * (unsigned)G);
           __syncwarp();
@@ -983,7 +1029,8 @@ hs_status dstack_create(DstackState** out, int H, int F, int nh, int hd, int max
   cudaError_t e = cudaMalloc(&s->ws, off * 4);
   s->attn_items_max = std::max((size_t)s->G, (size_t)s->max_seqs * nh * ((std::max(max_ctx, 1) + 16 * DS_SPLIT - 1) / (16 * DS_SPLIT)));
   if (e == cudaSuccess) e = cudaMalloc(&s->ws_attn, s->attn_items_max * (hd + 4) * 4);
-  s->ctr_words = 4096 + (size_t)DS_MAXSEQ * nh + 4 * (size_t)(s->tiles[0] + s->tiles[1] + s->tiles[2] + s->tiles[3]);
+  s->ctr_words = 4096 + (size_t)DS_MAXSEQ * nh + 4 * (size_t)(s->tiles[0] + s->tiles[1] + s->tiles[2] + s->tiles[3]) +
+                 s->attn_items_max;
   if (e == cudaSuccess) e = cudaMalloc(&s->ctr, s->ctr_words * 4);
   if (e == cudaSuccess) e = cudaMemset(s->ctr, 0, s->ctr_words * 4);
   if (e == cudaSuccess) e = cudaMalloc(&s->ssq, (size_t)(H / 128) * DS_MAXSEQ * 4);
@@ -1076,6 +1123,12 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
     while (ch < DS_SPLIT && units_of(ch) > (size_t)s->G) ++ch;
     if (units_of(ch) > s->attn_items_max) HS_FAIL(HS_E_INVAL, "dstack: context longer than the workspace was sized for");
     p.ch = ch;
+    static const bool omerge = [] {  // A/B knob: HS_DSTACK_OMERGE=0 keeps the merge in the units
+      const char* e = getenv("HS_DSTACK_OMERGE");
+      return !(e && atoi(e) == 0);
+    }();
+    const int nsp = (a.ctx[0] + 15) / 16 > 0 ? (((a.ctx[0] + 15) / 16) + ch - 1) / ch : 0;
+    p.nsp1 = (a.N == 1 && BN == 16 && omerge && nsp >= 2) ? nsp : 0;
   }
   p.ws_attn = s->ws_attn;
   p.cap = a.cap;
@@ -1110,6 +1163,7 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
   p.f_qkv = c + o; o += s->tiles[0];
   p.f_attn = c + o; o += s->nh;
   p.f_gu = c + o; o += s->tiles[2];
+  p.f_unit = c + o; o += s->attn_items_max;
   p.ssq = s->ssq;
   p.base_rows = s->base_rows;
   p.base_norm = s->base_norm;
