@@ -59,11 +59,11 @@ struct DsParams {
   int ch;
   float* ws_attn;
   unsigned *c_tile[4], *c_ih, *c_h, *f_qkv, *f_attn, *f_gu;
-  // single-sequence decode with a split context (N = 1, nsp1 = splits per head >= 2): each unit
-  // publishes its partial on f_unit[u] and the O GEMM's activation producer merges the splits of
-  // a k-block's head itself (no last-unit merge, no o round trip); 0 = the merge in the units
-  int nsp1;
-  unsigned* f_unit;
+  // stream-K fix-up (finisher = 1): the owner of a tile's first k-block keeps its partial in
+  // TMEM and sums the other parts once their per-part flags f_part[k][t * maxp + part] carry the
+  // layer's tag (no arrival atomic, no store + reload of its own part); 0 = last arriver
+  int finisher;
+  unsigned* f_part[4];
   // distributed row norms: residual tiles publish sum-of-squares partials ssq[tile][64] and
   // bump c_rows (cumulative); every CTA then normalises its column slice and bumps c_norm
   // (cumulative).  Targets are launch bases + counts (wrap-safe compares).
@@ -401,13 +401,6 @@ __device__ __forceinline__ void ds_attn_unit(const DsParams& p, int l, unsigned 
     orow[t] = __float2bfloat16_rn(A / L);
   }
   named_bar(2, 256);
-  if (p.nsp1) {  // the O GEMM's producer merges: publish this split's partial and leave
-    if (t == 0) {
-      if (p.trace) DS_TR(TR_AT_END);
-      publish(p.f_unit + u, tag);
-    }
-    return;  // sm is free: every read of it precedes the barrier above
-  }
   // one arrival per unit on the head's counter; the last unit of the head merges the splits
   // of every sequence (split order) and publishes the head
   if (t == 0) {
@@ -463,6 +456,26 @@ __device__ __forceinline__ void ds_part_sums(const float* tws, int np, int n0, i
   }
 }
 
+// As ds_part_sums, with part 0 read from the TMEM accumulator (row ml of the warp's lane
+// quarter at taddr) instead of the workspace: the same additions in the same order.
+template <int NC>
+__device__ __forceinline__ void ds_part_sums_tm(const float* tws, int np, int n0, int N, int ml, float* a, int BN,
+                                                uint32_t taddr) {
+  float v0[16];
+  tmem_ld16(taddr + (uint32_t)(n0 & ~15), v0);
+#pragma unroll
+  for (int j = 0; j < NC; ++j) a[j] = 0.f + (n0 + j < N ? v0[(n0 & 15) + j] : 0.f);
+#pragma unroll 2
+  for (int pt = 1; pt < np; ++pt) {
+    float v[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j)
+      v[j] = n0 + j < N ? __ldcg(tws + (size_t)pt * BN * 128 + (size_t)(n0 + j) * 128 + ml) : 0.f;
+#pragma unroll
+    for (int j = 0; j < NC; ++j) a[j] += v[j];
+  }
+}
+
 // The epilogue warps' part of GEMM kind k (0 qkv, 1 o, 2 gate_up, 3 down) of layer l: drains
 // the CTA's stream-K segments; the last arriver of a tile applies the epilogue.  Returns the
 // running segment count (TMEM double-buffer phase).
@@ -477,6 +490,7 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
   ds_range(blockIdx.x, W, p.G, beg, end, Gk);
   const int ml = et;
   int lastt[4], nlast = 0;
+  int held_t = -1, held_buf = 0;  // finisher mode: the tile whose part 0 stays in TMEM
   // pass 1: drain every segment of the phase and arrive on its tile
   for (int cur = beg; cur < end; ++seg) {
     const int t = cur / nkb, kb_lo = cur % nkb, kb_hi = min(nkb, kb_lo + (end - cur));
@@ -488,6 +502,18 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
     const int np = sk_owner((long long)(t + 1) * nkb - 1, W, Gk) - first + 1;
     const int part = blockIdx.x - first;
     float* tws = p.ws[k] + (size_t)t * p.maxp[k] * BN * 128;
+    // the phase's last segment, when it starts its tile, stays in TMEM: its epilogue (pass 2,
+    // right after) reads it there; every other segment is drained to the workspace
+    const bool hold = p.finisher && part == 0 && cur + (kb_hi - kb_lo) == end;
+    if (hold) {
+      held_t = t;
+      held_buf = buf;
+      if (nlast == 4) __trap();
+      lastt[nlast++] = t;
+      if (k == 0 && et == 0 && cur == beg) DS_TR(TR_Q_DRAIN);
+      cur += kb_hi - kb_lo;
+      continue;
+    }
     {
       float* dst = tws + (size_t)part * BN * 128 + ml;
       const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + buf * BN;
@@ -508,6 +534,19 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
     const bool first_seg = cur == beg;
     if (k == 0 && et == 0 && first_seg) DS_TR(TR_Q_DRAIN);
     cur += kb_hi - kb_lo;
+    if (p.finisher) {
+      if (np == 1) {
+        if (nlast == 4) __trap();
+        lastt[nlast++] = t;
+      } else {  // a later part: publish it for the tile's finisher (part 0's owner)
+        named_bar(1, 128);
+        if (et == 0) {
+          publish(p.f_part[k] + (size_t)t * p.maxp[k] + part, tag);
+          if (k == 0 && first_seg) DS_TR(TR_Q_ATOM);
+        }
+      }
+      continue;
+    }
     named_bar(1, 128);
     if (et == 0) {
       int last = 1;
@@ -527,18 +566,30 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
   }
   // pass 2: the epilogues of the tiles this CTA completed (after every arrival of the phase,
   // so a CTA's later segments never wait behind its earlier tiles' epilogues)
-  for (int q = 0; q < nlast; ++q) {
+  // (the held tile first: its TMEM buffer is released as soon as its epilogue is done)
+  for (int q0 = 0; q0 < nlast; ++q0) {
+    const int q = held_t >= 0 ? (q0 == 0 ? nlast - 1 : q0 - 1) : q0;
     const int t = lastt[q];
     const int first = sk_owner((long long)t * nkb, W, Gk);
     const int np = sk_owner((long long)(t + 1) * nkb - 1, W, Gk) - first + 1;
     float* tws = p.ws[k] + (size_t)t * p.maxp[k] * BN * 128;
+    const bool held = t == held_t;
+    const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(held_buf * BN);
+    if (held && np > 1) {  // the other parts' flags (usually long set: their segments come first)
+      if (et >= 1 && et < np) wait_tag(p.f_part[k] + (size_t)t * p.maxp[k] + et, tag);
+      named_bar(1, 128);
+    }
+    auto sums = [&](int n0, float* a) {
+      if (held) ds_part_sums_tm<NC>(tws, np, n0, p.N, ml, a, BN, taddr);
+      else ds_part_sums<NC>(tws, np, n0, p.N, ml, a, BN);
+    };
     if (k == 0 && et == 0) DS_TR(TR_Q_LAST);
     const int m = t * 128 + ml;
     const int H = p.H;
     if (k == 0) {  // bf16(q, k, v); RoPE of q, k; k', v -> paged pool; q' -> q
       for (int n0 = 0; n0 < p.N; n0 += NC) {
         float a[NC];
-        ds_part_sums<NC>(tws, np, n0, p.N, ml, a, BN);
+        sums(n0, a);
 #pragma unroll
         for (int j = 0; j < NC; ++j)
           if (n0 + j < p.N) vals[ml * DsCfg<BN, NC>::VS + n0 + j] = __bfloat162float(__float2bfloat16_rn(a[j]));
@@ -579,7 +630,7 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
     } else if (k == 2) {  // a = bf16(silu(g) * u): lanes 0-15 gate rows, 16-31 their up rows
       for (int n0 = 0; n0 < p.N; n0 += NC) {
         float a[NC];
-        ds_part_sums<NC>(tws, np, n0, p.N, ml, a, BN);
+        sums(n0, a);
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
           const float u = __shfl_xor_sync(0xffffffffu, a[j], 16);
@@ -597,7 +648,7 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
 #pragma unroll
         for (int j = 0; j < NC; ++j)
           r[j] = n0 + j < p.N ? __bfloat162float(__ldcg(resid + (size_t)(n0 + j) * H + m)) : 0.f;
-        ds_part_sums<NC>(tws, np, n0, p.N, ml, a, BN);
+        sums(n0, a);
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
           const bf16 y = __float2bfloat16_rn(a[j] + r[j]);
@@ -610,6 +661,11 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
         ds_ssq_chunk<NC>(a, n0, p.N, et, vals, p.ssq + (size_t)t * DS_MAXSEQ);
       }
       if (et == 0) red_release_add(p.c_rows, 1u);  // rows of this tile + their partial sums
+    }
+    if (held) {  // every read of the held accumulator done: the MMA may reuse the buffer
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[held_buf])) : "memory");
     }
   }
   return seg;
@@ -798,40 +854,6 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
                 dst[lane] = s_xn[(x % nkb) * 8 + lane];  // row 0: 16-byte chunk c at c ^ 0
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
               }
-              __syncwarp();
-              if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
-            }
-            continue;
-          }
-          if (k == 1 && p.nsp1) {
-            // split-context decode: the splits of each k-block's head are merged here, in split
-            // order (the arithmetic of the units' last-arriver merge), into row 0 of the slot;
-            // lane l owns columns 2l, 2l + 1 of the k-block
-            const int D = p.hd, nsp = p.nsp1;
-            for (int x = beg; x < end; ++x, ++i) {
-              const int kc = (x % nkb) * 64, h = kc / D, d = kc % D + 2 * lane;
-              for (int q = lane; q < nsp; q += 32) wait_tag(p.f_unit + h * nsp + q, tag);
-              __syncwarp();
-              if (p.trace && lane == 0 && x == beg) DS_TR(1);
-              const float* w0 = p.ws_attn + (size_t)(h * nsp) * (D + 4);
-              float MM = -INFINITY;
-              for (int q = 0; q < nsp; ++q) MM = fmaxf(MM, __ldcg(w0 + (size_t)q * (D + 4)));
-              float LL = 0.f, A0 = 0.f, A1 = 0.f;
-              for (int q = 0; q < nsp; ++q) {
-                const float* wq = w0 + (size_t)q * (D + 4);
-                const float ms = __ldcg(wq);
-                const float f = ms == -INFINITY ? 0.f : exp2f(ms - MM);
-                LL += __ldcg(wq + 1) * f;
-                A0 += __ldcg(wq + 4 + d) * f;
-                A1 += __ldcg(wq + 5 + d) * f;
-              }
-              const __nv_bfloat162 ov = __floats2bfloat162_rn(A0 / LL, A1 / LL);
-              const int s = i % C::STAGES;
-              if (lane == 0) mbar_wait(&empty[s], ((i / C::STAGES) & 1) ^ 1);
-              __syncwarp();
-              // row 0 of the SW128 tile: byte 4 l of the row is chunk l / 4 at position l / 4
-              reinterpret_cast<__nv_bfloat162*>(smem + s * C::STAGE_BYTES + C::A_BYTES)[lane] = ov;
-              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
               __syncwarp();
               if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
             }
@@ -1029,8 +1051,8 @@ hs_status dstack_create(DstackState** out, int H, int F, int nh, int hd, int max
   cudaError_t e = cudaMalloc(&s->ws, off * 4);
   s->attn_items_max = std::max((size_t)s->G, (size_t)s->max_seqs * nh * ((std::max(max_ctx, 1) + 16 * DS_SPLIT - 1) / (16 * DS_SPLIT)));
   if (e == cudaSuccess) e = cudaMalloc(&s->ws_attn, s->attn_items_max * (hd + 4) * 4);
-  s->ctr_words = 4096 + (size_t)DS_MAXSEQ * nh + 4 * (size_t)(s->tiles[0] + s->tiles[1] + s->tiles[2] + s->tiles[3]) +
-                 s->attn_items_max;
+  s->ctr_words = 4096 + (size_t)DS_MAXSEQ * nh + 4 * (size_t)(s->tiles[0] + s->tiles[1] + s->tiles[2] + s->tiles[3]);
+  for (int k = 0; k < 4; ++k) s->ctr_words += (size_t)s->tiles[k] * s->maxp[k] + 32;
   if (e == cudaSuccess) e = cudaMalloc(&s->ctr, s->ctr_words * 4);
   if (e == cudaSuccess) e = cudaMemset(s->ctr, 0, s->ctr_words * 4);
   if (e == cudaSuccess) e = cudaMalloc(&s->ssq, (size_t)(H / 128) * DS_MAXSEQ * 4);
@@ -1123,12 +1145,6 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
     while (ch < DS_SPLIT && units_of(ch) > (size_t)s->G) ++ch;
     if (units_of(ch) > s->attn_items_max) HS_FAIL(HS_E_INVAL, "dstack: context longer than the workspace was sized for");
     p.ch = ch;
-    static const bool omerge = [] {  // A/B knob: HS_DSTACK_OMERGE=0 keeps the merge in the units
-      const char* e = getenv("HS_DSTACK_OMERGE");
-      return !(e && atoi(e) == 0);
-    }();
-    const int nsp = (a.ctx[0] + 15) / 16 > 0 ? (((a.ctx[0] + 15) / 16) + ch - 1) / ch : 0;
-    p.nsp1 = (a.N == 1 && BN == 16 && omerge && nsp >= 2) ? nsp : 0;
   }
   p.ws_attn = s->ws_attn;
   p.cap = a.cap;
@@ -1163,7 +1179,18 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
   p.f_qkv = c + o; o += s->tiles[0];
   p.f_attn = c + o; o += s->nh;
   p.f_gu = c + o; o += s->tiles[2];
-  p.f_unit = c + o; o += s->attn_items_max;
+  for (int k = 0; k < 4; ++k) {
+    o = align_up(o, 32);
+    p.f_part[k] = c + o;
+    o += (size_t)s->tiles[k] * s->maxp[k];
+  }
+  {
+    static const int fin = [] {  // A/B knob: HS_DSTACK_FINISHER=0 selects the last-arriver fix-up
+      const char* e = getenv("HS_DSTACK_FINISHER");
+      return e && atoi(e) == 0 ? 0 : 1;
+    }();
+    p.finisher = fin;
+  }
   p.ssq = s->ssq;
   p.base_rows = s->base_rows;
   p.base_norm = s->base_norm;

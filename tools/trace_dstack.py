@@ -69,5 +69,8 @@ for l in (10, 20):
     th = (per[l, 128:128 + cfg["n_heads"]] - ref[l]) / 1e3
     print(json.dumps({"layer": l, "qkv_tile_pub_us": [round(float(x), 1) for x in tq]}))
     print(json.dumps({"layer": l, "head_attn_pub_us": [round(float(x), 1) for x in th]}))
+out = os.environ.get("TRACE_NPZ")
+if out:  # raw stamps for offline analysis: tr[G][L][32] (ns), per-tile / per-head publish times, ref
+    np.savez_compressed(out, tr=tr, per=per, ref=ref)
 hs.dstack_trace(False)
 g.destroy()
