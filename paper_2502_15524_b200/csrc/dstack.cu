@@ -43,7 +43,7 @@ struct DsParams {
   float eps;
   unsigned tag0;
   int tiles[4], nkb[4], maxp[4];
-  float* ws[4];
+  unsigned long long* ws[4];  // stream-K parts: tagged words (st_part)
   const bf16 *attn_norm, *ffn_norm;
   long long norm_stride;
   const bf16* final_norm;
@@ -58,12 +58,7 @@ struct DsParams {
   const float2* rope;
   int ch;
   float* ws_attn;
-  unsigned *c_tile[4], *c_ih, *c_h, *f_qkv, *f_attn, *f_gu;
-  // stream-K fix-up (finisher = 1): the owner of a tile's first k-block keeps its partial in
-  // TMEM and sums the other parts once their per-part flags f_part[k][t * maxp + part] carry the
-  // layer's tag (no arrival atomic, no store + reload of its own part); 0 = last arriver
-  int finisher;
-  unsigned* f_part[4];
+  unsigned *c_ih, *c_h, *f_qkv, *f_attn, *f_gu;
   // distributed row norms: residual tiles publish sum-of-squares partials ssq[tile][64] and
   // bump c_rows (cumulative); every CTA then normalises its column slice and bumps c_norm
   // (cumulative).  Targets are launch bases + counts (wrap-safe compares).
@@ -155,6 +150,10 @@ __device__ __constant__ int p_nomma = 0;
 // L2 prefetch of each attention unit's cached K / V before the unit waits for its q, k, v tiles
 // (HS_DSTACK_KVPF=1; measured r02: no gain at B = 1, 2 % slower at 13B B = 16: off)
 __device__ __constant__ int p_kv_prefetch = 0;
+// Early reads of the held tile's later parts and residual (HS_DSTACK_EARLYPARTS=0: A/B)
+__device__ __constant__ int p_early_parts = 1;
+// Trace only (HS_DSTACK_TRACE_K): the GEMM kind whose stream-K fix-up the TR_Q_* stamps follow
+__device__ __constant__ int p_trace_k = 0;
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
@@ -251,6 +250,21 @@ __device__ __forceinline__ void ds_norm_slice(const DsParams& p, const bf16* __r
   }
   named_bar(2, 256);
   if (t == 0) red_release_add(p.c_norm, 1u);
+}
+
+// Stream-K parts travel as tagged words: the value's bits and the layer's tag in one 8-byte
+// single-copy-atomic store, so the writer needs no fence and no flag, and the tile's finisher
+// polls exactly the words it sums (a stale word carries an older tag; the workspace starts
+// zeroed and tags are never 0).
+__device__ __forceinline__ void st_part(unsigned long long* a, float v, unsigned tag) {
+  const unsigned long long w = ((unsigned long long)tag << 32) | __float_as_uint(v);
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(w) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_part(const unsigned long long* a) {
+  unsigned long long w;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(a));
+  return w;
 }
 
 // One attention unit: sequence i, head h, KV blocks [sp * DS_SPLIT, (sp + 1) * DS_SPLIT) of the
@@ -439,49 +453,59 @@ __device__ __forceinline__ void ds_attn_unit(const DsParams& p, int l, unsigned 
   named_bar(2, 256);  // sm reusable
 }
 
-// Sum of the np stream-K parts (in part order) of tile row ml for tokens n0 .. n0 + NC - 1,
-// with every load of a part group in flight together (the tail of each tile is latency bound).
-template <int NC>
-__device__ __forceinline__ void ds_part_sums(const float* tws, int np, int n0, int N, int ml, float* a, int BN) {
-#pragma unroll
-  for (int j = 0; j < NC; ++j) a[j] = 0.f;
-#pragma unroll 2
-  for (int pt = 0; pt < np; ++pt) {
-    float v[NC];
-#pragma unroll
-    for (int j = 0; j < NC; ++j)
-      v[j] = n0 + j < N ? __ldcg(tws + (size_t)pt * BN * 128 + (size_t)(n0 + j) * 128 + ml) : 0.f;
-#pragma unroll
-    for (int j = 0; j < NC; ++j) a[j] += v[j];
+// Slow path of an early read: the part was not written yet.  Traps after ~2 s (protocol bug).
+__device__ __noinline__ float wait_part(const unsigned long long* a, unsigned tag) {
+  const unsigned long long t0 = gtimer();
+  for (;;) {
+    const unsigned long long w = ld_part(a);
+    if ((unsigned)(w >> 32) == tag) return __uint_as_float((unsigned)w);
+    __nanosleep(64);
+    if (gtimer() - t0 > 2000000000ull) __trap();
   }
 }
 
-// As ds_part_sums, with part 0 read from the TMEM accumulator (row ml of the warp's lane
-// quarter at taddr) instead of the workspace: the same additions in the same order.
+// a[j] += the stream-K parts p0 .. np - 1 (in part order) of tile row ml, tokens n0 + j, with
+// every load of a part group in flight together (the tail of each tile is latency bound).  A
+// group not written yet is re-read as a whole (one round trip per poll, not one per word);
+// traps after ~2 s (protocol bug).
 template <int NC>
-__device__ __forceinline__ void ds_part_sums_tm(const float* tws, int np, int n0, int N, int ml, float* a, int BN,
-                                                uint32_t taddr) {
-  float v0[16];
-  tmem_ld16(taddr + (uint32_t)(n0 & ~15), v0);
-#pragma unroll
-  for (int j = 0; j < NC; ++j) a[j] = 0.f + (n0 + j < N ? v0[(n0 & 15) + j] : 0.f);
+__device__ __forceinline__ void ds_add_parts(const unsigned long long* tws, int p0, int np, int n0, int N, int ml,
+                                             float* a, int BN, unsigned tag) {
 #pragma unroll 2
-  for (int pt = 1; pt < np; ++pt) {
-    float v[NC];
+  for (int pt = p0; pt < np; ++pt) {
+    const unsigned long long* src = tws + ((size_t)pt * BN + n0) * 128 + ml;
+    unsigned long long w[NC];
+    bool ok = true;
 #pragma unroll
-    for (int j = 0; j < NC; ++j)
-      v[j] = n0 + j < N ? __ldcg(tws + (size_t)pt * BN * 128 + (size_t)(n0 + j) * 128 + ml) : 0.f;
+    for (int j = 0; j < NC; ++j) w[j] = n0 + j < N ? ld_part(src + (size_t)j * 128) : (unsigned long long)tag << 32;
 #pragma unroll
-    for (int j = 0; j < NC; ++j) a[j] += v[j];
+    for (int j = 0; j < NC; ++j) ok = ok && (unsigned)(w[j] >> 32) == tag;
+    if (!ok) {
+      const unsigned long long t0 = gtimer();
+      do {
+        __nanosleep(64);
+        if (gtimer() - t0 > 2000000000ull) __trap();
+#pragma unroll
+        for (int j = 0; j < NC; ++j)
+          if (n0 + j < N && (unsigned)(w[j] >> 32) != tag) w[j] = ld_part(src + (size_t)j * 128);
+        ok = true;
+#pragma unroll
+        for (int j = 0; j < NC; ++j) ok = ok && (unsigned)(w[j] >> 32) == tag;
+      } while (!ok);
+    }
+#pragma unroll
+    for (int j = 0; j < NC; ++j) a[j] += __uint_as_float((unsigned)w[j]);
   }
 }
 
 // The epilogue warps' part of GEMM kind k (0 qkv, 1 o, 2 gate_up, 3 down) of layer l: drains
-// the CTA's stream-K segments; the last arriver of a tile applies the epilogue.  Returns the
-// running segment count (TMEM double-buffer phase).
+// the CTA's stream-K segments.  A tile's finisher is the owner of its first k-block: that
+// segment is the last of the owner's range, so its accumulator stays in TMEM and the epilogue
+// adds the later parts (tagged words, written by the CTAs whose ranges start in the tile) in
+// part order.  Returns the running segment count (TMEM double-buffer phase).
 template <int BN, int NC>
 __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsigned tag, int seg, uint32_t tmem,
-                                           uint64_t* tfull, uint64_t* tempty, float* vals, volatile int* flag,
+                                           uint64_t* tfull, uint64_t* tempty, float* vals,
                                            int et, int lane, int quad,
                                            const int* s_pos, const int* s_slot, const float2* s_rope) {
   const int nkb = p.nkb[k], tiles = p.tiles[k];
@@ -490,32 +514,47 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
   ds_range(blockIdx.x, W, p.G, beg, end, Gk);
   const int ml = et;
   int lastt[4], nlast = 0;
-  int held_t = -1, held_buf = 0;  // finisher mode: the tile whose part 0 stays in TMEM
-  // pass 1: drain every segment of the phase and arrive on its tile
+  int held_t = -1, held_buf = 0;  // the tile whose part 0 stays in TMEM
+  // single-sequence decode: the held tile's later parts (and its residual) are read while its
+  // own MMAs still run, so its epilogue starts without a round trip (re-read if not yet written)
+  constexpr int NPRE = 8;
+  unsigned long long pre[NPRE];
+  float pre_r = 0.f;
+  // pass 1: drain every segment of the phase
   for (int cur = beg; cur < end; ++seg) {
     const int t = cur / nkb, kb_lo = cur % nkb, kb_hi = min(nkb, kb_lo + (end - cur));
     const int buf = seg & 1;
-    mbar_wait(&tfull[buf], (seg >> 1) & 1);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (k == 0 && et == 0 && cur == beg) DS_TR(TR_Q_TFULL);
     const int first = sk_owner((long long)t * nkb, W, Gk);
     const int np = sk_owner((long long)(t + 1) * nkb - 1, W, Gk) - first + 1;
     const int part = blockIdx.x - first;
-    float* tws = p.ws[k] + (size_t)t * p.maxp[k] * BN * 128;
+    unsigned long long* tws = p.ws[k] + (size_t)t * p.maxp[k] * BN * 128;
     // the phase's last segment, when it starts its tile, stays in TMEM: its epilogue (pass 2,
     // right after) reads it there; every other segment is drained to the workspace
-    const bool hold = p.finisher && part == 0 && cur + (kb_hi - kb_lo) == end;
+    const bool hold = part == 0 && cur + (kb_hi - kb_lo) == end;
+    if constexpr (NC == 1) {
+      if (hold && p_early_parts) {
+#pragma unroll
+        for (int q = 0; q < NPRE; ++q)
+          if (q + 1 < np) pre[q] = ld_part(tws + (size_t)(q + 1) * BN * 128 + ml);
+        if (k == 1 || k == 3)
+          pre_r = __bfloat162float(__ldcg((k == 1 ? (l == 0 ? p.x_in : p.x) : p.hbuf) + (size_t)t * 128 + ml));
+      }
+    }
+    mbar_wait(&tfull[buf], (seg >> 1) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (k == p_trace_k && et == 0 && cur == beg) DS_TR(TR_Q_TFULL);
+    if (k == p_trace_k && k != 0 && et == 0 && cur + (kb_hi - kb_lo) == end) DS_TR(TR_Q_STORES);  // last segment's MMAs done
     if (hold) {
       held_t = t;
       held_buf = buf;
       if (nlast == 4) __trap();
       lastt[nlast++] = t;
-      if (k == 0 && et == 0 && cur == beg) DS_TR(TR_Q_DRAIN);
+      if (k == p_trace_k && et == 0 && cur == beg) DS_TR(TR_Q_DRAIN);
       cur += kb_hi - kb_lo;
       continue;
     }
     {
-      float* dst = tws + (size_t)part * BN * 128 + ml;
+      unsigned long long* dst = tws + (size_t)part * BN * 128 + ml;
       const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + buf * BN;
       constexpr int CH = BN < 32 ? 16 : 32;
 #pragma unroll
@@ -525,65 +564,56 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
         else tmem_ld16(taddr + c0, v);
 #pragma unroll
         for (int j = 0; j < CH; ++j)
-          if (c0 + j < p.N) dst[(size_t)(c0 + j) * 128] = v[j];
+          if (c0 + j < p.N) st_part(dst + (size_t)(c0 + j) * 128, v[j], tag);
       }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf])) : "memory");
     const bool first_seg = cur == beg;
-    if (k == 0 && et == 0 && first_seg) DS_TR(TR_Q_DRAIN);
+    if (k == p_trace_k && et == 0 && first_seg) DS_TR(TR_Q_DRAIN);
     cur += kb_hi - kb_lo;
-    if (p.finisher) {
-      if (np == 1) {
-        if (nlast == 4) __trap();
-        lastt[nlast++] = t;
-      } else {  // a later part: publish it for the tile's finisher (part 0's owner)
-        named_bar(1, 128);
-        if (et == 0) {
-          publish(p.f_part[k] + (size_t)t * p.maxp[k] + part, tag);
-          if (k == 0 && first_seg) DS_TR(TR_Q_ATOM);
-        }
-      }
-      continue;
-    }
-    named_bar(1, 128);
-    if (et == 0) {
-      int last = 1;
-      if (np > 1) {  // a tile held by one CTA needs no arrival
-        const unsigned old = atom_add_acq_rel(&p.c_tile[k][t], 1u);
-        last = old == (unsigned)(np - 1);
-        if (last) p.c_tile[k][t] = 0;
-      }
-      *flag = last;
-      if (k == 0 && first_seg) DS_TR(TR_Q_ATOM);
-    }
-    named_bar(1, 128);
-    if (__shfl_sync(0xffffffffu, *flag, 0)) {  // (warp-uniform for the compiler)
+    if (np == 1) {  // a whole tile inside the range, not its last segment
       if (nlast == 4) __trap();
       lastt[nlast++] = t;
     }
   }
-  // pass 2: the epilogues of the tiles this CTA completed (after every arrival of the phase,
-  // so a CTA's later segments never wait behind its earlier tiles' epilogues)
+  // pass 2: the epilogues of the tiles this CTA finishes (after every drain of the phase, so a
+  // CTA's later segments never wait behind its earlier tiles' epilogues)
   // (the held tile first: its TMEM buffer is released as soon as its epilogue is done)
   for (int q0 = 0; q0 < nlast; ++q0) {
     const int q = held_t >= 0 ? (q0 == 0 ? nlast - 1 : q0 - 1) : q0;
     const int t = lastt[q];
     const int first = sk_owner((long long)t * nkb, W, Gk);
     const int np = sk_owner((long long)(t + 1) * nkb - 1, W, Gk) - first + 1;
-    float* tws = p.ws[k] + (size_t)t * p.maxp[k] * BN * 128;
+    const unsigned long long* tws = p.ws[k] + (size_t)t * p.maxp[k] * BN * 128;
     const bool held = t == held_t;
     const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(held_buf * BN);
-    if (held && np > 1) {  // the other parts' flags (usually long set: their segments come first)
-      if (et >= 1 && et < np) wait_tag(p.f_part[k] + (size_t)t * p.maxp[k] + et, tag);
-      named_bar(1, 128);
-    }
+    // the parts summed in part order from 0.f (part 0 from TMEM when held)
     auto sums = [&](int n0, float* a) {
-      if (held) ds_part_sums_tm<NC>(tws, np, n0, p.N, ml, a, BN, taddr);
-      else ds_part_sums<NC>(tws, np, n0, p.N, ml, a, BN);
+      if (held) {
+        float v0[16];
+        tmem_ld16(taddr + (uint32_t)(n0 & ~15), v0);
+#pragma unroll
+        for (int j = 0; j < NC; ++j) a[j] = 0.f + (n0 + j < p.N ? v0[(n0 & 15) + j] : 0.f);
+        if (NC == 1 && p_early_parts) {  // parts 1 .. NPRE from the early reads
+#pragma unroll
+          for (int q = 0; q < NPRE; ++q) {
+            if (q + 1 >= np) break;
+            const unsigned long long w = pre[q];
+            a[0] += (unsigned)(w >> 32) == tag ? __uint_as_float((unsigned)w)
+                                               : wait_part(tws + (size_t)(q + 1) * BN * 128 + ml, tag);
+          }
+          if (np > NPRE + 1) ds_add_parts<1>(tws, NPRE + 1, np, n0, p.N, ml, a, BN, tag);
+          return;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < NC; ++j) a[j] = 0.f;
+      }
+      ds_add_parts<NC>(tws, held ? 1 : 0, np, n0, p.N, ml, a, BN, tag);
     };
-    if (k == 0 && et == 0) DS_TR(TR_Q_LAST);
+    if (k == p_trace_k && et == 0) DS_TR(TR_Q_LAST);
     const int m = t * 128 + ml;
     const int H = p.H;
     if (k == 0) {  // bf16(q, k, v); RoPE of q, k; k', v -> paged pool; q' -> q
@@ -595,7 +625,7 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
           if (n0 + j < p.N) vals[ml * DsCfg<BN, NC>::VS + n0 + j] = __bfloat162float(__float2bfloat16_rn(a[j]));
       }
       named_bar(1, 128);
-      if (et == 0) DS_TR(TR_Q_VALS);
+      if (p_trace_k == 0 && et == 0) DS_TR(TR_Q_VALS);
       const int half = p.hd >> 1;
       const int region = (t * 128) / H, r0 = (t * 128) % H;  // 0 q, 1 k, 2 v
       if (et < 64) {
@@ -622,10 +652,10 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
           }
         }
       }
-      if (et == 0) DS_TR(TR_Q_STORES);
+      if (p_trace_k == 0 && et == 0) DS_TR(TR_Q_STORES);
       named_bar(1, 128);
       if (et == 0) publish(p.f_qkv + t, tag);
-      if (et == 0) DS_TR(TR_Q_PUB);
+      if (p_trace_k == 0 && et == 0) DS_TR(TR_Q_PUB);
       if (et == 0 && p.trace && t < 128) p.trace[(size_t)p.G * p.nl * 32 + (size_t)l * 256 + t] = gtimer();
     } else if (k == 2) {  // a = bf16(silu(g) * u): lanes 0-15 gate rows, 16-31 their up rows
       for (int n0 = 0; n0 < p.N; n0 += NC) {
@@ -639,7 +669,9 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
         }
       }
       named_bar(1, 128);
+      if (k == p_trace_k && et == 0) DS_TR(TR_Q_VALS);
       if (et == 0) publish(p.f_gu + t, tag);
+      if (k == p_trace_k && et == 0) DS_TR(TR_Q_PUB);
     } else {  // residual: h = bf16(x + o W_o^T) (k = 1) / x' = bf16(h + a W_d^T) (k = 3)
       const bf16* resid = k == 1 ? (l == 0 ? p.x_in : p.x) : p.hbuf;
       bf16* out = k == 1 ? p.hbuf : p.x;
@@ -647,7 +679,9 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
         float r[NC], a[NC];
 #pragma unroll
         for (int j = 0; j < NC; ++j)
-          r[j] = n0 + j < p.N ? __bfloat162float(__ldcg(resid + (size_t)(n0 + j) * H + m)) : 0.f;
+          r[j] = n0 + j >= p.N ? 0.f
+                 : (NC == 1 && held && p_early_parts) ? pre_r
+                                     : __bfloat162float(__ldcg(resid + (size_t)(n0 + j) * H + m));
         sums(n0, a);
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
@@ -660,7 +694,9 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
         }
         ds_ssq_chunk<NC>(a, n0, p.N, et, vals, p.ssq + (size_t)t * DS_MAXSEQ);
       }
+      if (k == p_trace_k && et == 0) DS_TR(TR_Q_VALS);
       if (et == 0) red_release_add(p.c_rows, 1u);  // rows of this tile + their partial sums
+      if (k == p_trace_k && et == 0) DS_TR(TR_Q_PUB);
     }
     if (held) {  // every read of the held accumulator done: the MMA may reuse the buffer
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -691,7 +727,6 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  volatile int* flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
   float* red = reinterpret_cast<float*>(tmem_slot + 4);                                // [8]
   int* s_nc = reinterpret_cast<int*>(red + 8);                                         // [64]
   int* s_base = s_nc + DS_MAXSEQ;                                                      // [65]
@@ -962,7 +997,7 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
           for (int c = c0 & ~7; c < c1; c += 8) asm volatile("prefetch.global.L2 [%0];" ::"l"(w + (size_t)c * 8));
         }
       }
-      if (epi) seg = ds_segments<BN, NC>(p, k, l, tag, seg, tmem, tfull, tempty, vals, flag, t256, lane, quad,
+      if (epi) seg = ds_segments<BN, NC>(p, k, l, tag, seg, tmem, tfull, tempty, vals, t256, lane, quad,
                                      s_pos, s_slot, s_rope);
       if (t256 == 0) DS_TR(TR_E_QKV + (k == 0 ? 0 : k == 1 ? 2 : k == 2 ? 4 : 5));
       if (k == 0) {
@@ -1001,7 +1036,7 @@ struct DstackState {
   int device = 0, G = 0;
   int H = 0, F = 0, nh = 0, hd = 0, max_seqs = 0, bn_max = 16;
   int tiles[4] = {}, nkb[4] = {}, maxp[4] = {};
-  float* ws = nullptr;
+  unsigned long long* ws = nullptr;  // stream-K parts (tagged words), per GEMM kind at ws_off[k]
   size_t ws_off[4] = {};
   float* ws_attn = nullptr;
   size_t attn_items_max = 0;
@@ -1048,11 +1083,12 @@ hs_status dstack_create(DstackState** out, int H, int F, int nh, int hd, int max
     s->ws_off[k] = off;
     off += align_up((size_t)s->tiles[k] * s->maxp[k] * s->bn_max * 128, 64);
   }
-  cudaError_t e = cudaMalloc(&s->ws, off * 4);
+  cudaError_t e = cudaMalloc(&s->ws, off * 8);
+  if (e == cudaSuccess) e = cudaMemset(s->ws, 0, off * 8);  // no word carries a tag yet
+
   s->attn_items_max = std::max((size_t)s->G, (size_t)s->max_seqs * nh * ((std::max(max_ctx, 1) + 16 * DS_SPLIT - 1) / (16 * DS_SPLIT)));
   if (e == cudaSuccess) e = cudaMalloc(&s->ws_attn, s->attn_items_max * (hd + 4) * 4);
   s->ctr_words = 4096 + (size_t)DS_MAXSEQ * nh + 4 * (size_t)(s->tiles[0] + s->tiles[1] + s->tiles[2] + s->tiles[3]);
-  for (int k = 0; k < 4; ++k) s->ctr_words += (size_t)s->tiles[k] * s->maxp[k] + 32;
   if (e == cudaSuccess) e = cudaMalloc(&s->ctr, s->ctr_words * 4);
   if (e == cudaSuccess) e = cudaMemset(s->ctr, 0, s->ctr_words * 4);
   if (e == cudaSuccess) e = cudaMalloc(&s->ssq, (size_t)(H / 128) * DS_MAXSEQ * 4);
@@ -1068,6 +1104,7 @@ void dstack_destroy(DstackState* s) {
   if (!s) return;
   DeviceGuard dg(s->device);
   if (s->ws) cudaFree(s->ws);
+
   if (s->ws_attn) cudaFree(s->ws_attn);
   if (s->ctr) cudaFree(s->ctr);
   if (s->ssq) cudaFree(s->ssq);
@@ -1161,6 +1198,12 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
       const char* e4 = getenv("HS_DSTACK_KVPF");
       const int kvpf = e4 ? atoi(e4) : 0;
       HS_CUDA(cudaMemcpyToSymbol(p_kv_prefetch, &kvpf, sizeof(kvpf)));
+      const char* e6 = getenv("HS_DSTACK_EARLYPARTS");
+      const int ep = e6 ? atoi(e6) : 1;
+      HS_CUDA(cudaMemcpyToSymbol(p_early_parts, &ep, sizeof(ep)));
+      const char* e5 = getenv("HS_DSTACK_TRACE_K");
+      const int tk = e5 ? atoi(e5) : 0;
+      HS_CUDA(cudaMemcpyToSymbol(p_trace_k, &tk, sizeof(tk)));
       const char* e3 = getenv("HS_DSTACK_NOMMA");
       const int nomma = e3 ? atoi(e3) : 0;
       HS_CUDA(cudaMemcpyToSymbol(p_nomma, &nomma, sizeof(nomma)));
@@ -1170,7 +1213,6 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
   p.trace = g_ds_trace && (size_t)s->G * a.nl * 32 + (size_t)a.nl * 256 <= kTraceWords ? g_ds_trace : nullptr;
   unsigned* c = s->ctr;
   size_t o = 0;
-  for (int k = 0; k < 4; ++k) { p.c_tile[k] = c + o; o += s->tiles[k]; }
   p.c_ih = c + o; o += (size_t)DS_MAXSEQ * s->nh;
   p.c_h = c + o; o += s->nh;
   o = align_up(o, 32);
@@ -1179,18 +1221,6 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
   p.f_qkv = c + o; o += s->tiles[0];
   p.f_attn = c + o; o += s->nh;
   p.f_gu = c + o; o += s->tiles[2];
-  for (int k = 0; k < 4; ++k) {
-    o = align_up(o, 32);
-    p.f_part[k] = c + o;
-    o += (size_t)s->tiles[k] * s->maxp[k];
-  }
-  {
-    static const int fin = [] {  // A/B knob: HS_DSTACK_FINISHER=0 selects the last-arriver fix-up
-      const char* e = getenv("HS_DSTACK_FINISHER");
-      return e && atoi(e) == 0 ? 0 : 1;
-    }();
-    p.finisher = fin;
-  }
   p.ssq = s->ssq;
   p.base_rows = s->base_rows;
   p.base_norm = s->base_norm;
