@@ -27,7 +27,7 @@ import numpy as np
 
 import hsgen
 
-from .numerics import (argmax_lowest, bf16, bf16_bits, bf16_value, linear, rmsnorm, rope,
+from .numerics import (argmax_lowest, bf16, bf16_bits, bf16_value, linear, rmsnorm, rmsnorm_split, rope,
                        rope_cos_sin, silu)
 
 BLOCK = 16  # tokens per KV block (reading R6)
@@ -173,10 +173,10 @@ class Worker:
         cfg, rnd, W = self.cfg, self.rnd, self.w.layer(l)
         nh, d, eps = cfg["n_heads"], cfg["head_dim"], cfg["rms_eps"]
         T = x.shape[0]
-        n = rmsnorm(x, W["attn_norm"], eps, rnd)                                   # step 4.1
-        q = rnd(self.lin(n, W["wq"])).reshape(T, nh, d)                               # step 4.2
-        k = rnd(self.lin(n, W["wk"])).reshape(T, nh, d)
-        v = rnd(self.lin(n, W["wv"])).reshape(T, nh, d)
+        n, r = rmsnorm_split(x, W["attn_norm"], eps, rnd)                          # step 4.1 (R10b)
+        q = rnd(r * self.lin(n, W["wq"])).reshape(T, nh, d)                           # step 4.2
+        k = rnd(r * self.lin(n, W["wk"])).reshape(T, nh, d)
+        v = rnd(r * self.lin(n, W["wv"])).reshape(T, nh, d)
         pos = np.concatenate([np.asarray(p) for (_, p, _, _) in batch])
         c, s = rope_cos_sin(pos, d, cfg["rope_theta"], table_f32=rnd is bf16)      # step 4.3
         q, k = rope(q, c, s, rnd), rope(k, c, s, rnd)
@@ -217,10 +217,11 @@ class Worker:
         return h
 
     def mlp_half(self, l: int, h: np.ndarray, trace: dict | None = None) -> np.ndarray:
-        """Steps 4.7-4.9 of layer l: x' = h + (silu(n2 W_g^T) * (n2 W_u^T)) W_d^T, n2 = RMSNorm(h)."""
+        """Steps 4.7-4.9 of layer l: x' = h + (silu(n2 W_g^T) * (n2 W_u^T)) W_d^T, n2 = RMSNorm(h)
+        (as r2 (h * w) W^T: reading R10b)."""
         rnd, W = self.rnd, self.w.layer(l)
-        n2 = rmsnorm(h, W["ffn_norm"], self.cfg["rms_eps"], rnd)                    # step 4.7
-        a = rnd(silu(self.lin(n2, W["wg"])) * self.lin(n2, W["wu"]))                    # step 4.8
+        n2, r2 = rmsnorm_split(h, W["ffn_norm"], self.cfg["rms_eps"], rnd)         # step 4.7
+        a = rnd(silu(r2 * self.lin(n2, W["wg"])) * (r2 * self.lin(n2, W["wu"])))      # step 4.8
         out = rnd(h + self.lin(a, W["wd"]))                                           # step 4.9
         if trace is not None:
             trace.update(n2=n2, a=a, out=out)

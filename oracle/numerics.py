@@ -49,6 +49,16 @@ def rmsnorm(x: np.ndarray, w: np.ndarray, eps: float, rnd=bf16) -> np.ndarray:
     return rnd(x * r * w)
 
 
+def rmsnorm_split(x: np.ndarray, w: np.ndarray, eps: float, rnd=bf16):
+    """The RMSNorm that feeds a linear layer (steps 4.1 and 4.7, reading R10b): in
+    real arithmetic (x r w) W^T = r ((x w) W^T) with r = 1/sqrt(mean_j x_j^2 + eps), so the
+    materialised operand is a = rnd(x_i * w_i) and the per-row scale r multiplies the product
+    before its rounding (the consumer computes rnd(r * linear(a, W))).  Returns (a, r[.., 1])."""
+    ms = np.mean(x * x, axis=-1, keepdims=True)
+    r = 1.0 / np.sqrt(ms + eps)
+    return rnd(x * w), r
+
+
 def linear(x: np.ndarray, W: np.ndarray, acc=np.float64) -> np.ndarray:
     """x [T,K] @ W[N,K]^T accumulated in float64, unrounded (the consumer rounds).
     ``acc=np.float32`` gives the same product accumulated in float32: it is only used to

@@ -59,12 +59,15 @@ struct DsParams {
   int ch;
   float* ws_attn;
   unsigned *c_ih, *c_h, *f_qkv, *f_attn, *f_gu;
-  // distributed row norms: residual tiles publish sum-of-squares partials ssq[tile][64] and
-  // bump c_rows (cumulative); every CTA then normalises its column slice and bumps c_norm
-  // (cumulative).  Targets are launch bases + counts (wrap-safe compares).
+  // row norms (reading R10b): a residual tile (and the stage input pass) writes the next
+  // GEMM's operand nrm = bf16(x * w) for its 128 columns and publishes f_nrm[0 / 1][tile]
+  // (QKV / gate_up operand, the consuming layer's tag), plus its sum-of-squares partials
+  // ssq[tile][64] and a release-add on c_rows (cumulative, launch base + count); the row scale
+  // rs = 1/sqrt(sum / H + eps) multiplies the QKV / gate_up accumulators in their epilogues.
   float* ssq;
-  unsigned *c_rows, *c_norm;
-  unsigned base_rows, base_norm;
+  unsigned* c_rows;
+  unsigned* f_nrm[2];
+  unsigned base_rows;
   unsigned long long* trace;  // optional: [G][nl][16] globaltimer stamps (hs_debug_dstack_trace)
   bf16* cap;                  // optional capture: layer l's h at cap + 2l * cap_stride, its output at (2l + 1)
   long long cap_stride;
@@ -131,12 +134,11 @@ struct DsCfg {
   static constexpr int VALS_BYTES = 128 * VS * 4 < 64 ? 64 : 128 * VS * 4;  // RoPE pairing + Σx² scratch
   static constexpr int ROPE_BYTES = VS * 64 * 8;   // cos/sin of the call's positions (head_dim <= 128)
   static constexpr int ATT_BYTES = (2 * 8 + 8 * 128) * 4 + 128;  // attention warp merge
-  static constexpr int XN_BYTES = NC == 1 ? 10240 : 0;  // single-sequence decode: the normalised row (H <= 5120)
   static constexpr int MISC = 2048;
-  static constexpr int FIT = (232448 - 1024 - MISC - VALS_BYTES - ROPE_BYTES - ATT_BYTES - XN_BYTES) / STAGE_BYTES;
+  static constexpr int FIT = (232448 - 1024 - MISC - VALS_BYTES - ROPE_BYTES - ATT_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = FIT > 12 ? 12 : FIT;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + VALS_BYTES + ROPE_BYTES + ATT_BYTES + XN_BYTES + 1024 + MISC;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + VALS_BYTES + ROPE_BYTES + ATT_BYTES + 1024 + MISC;
 };
 
 __device__ __constant__ unsigned p_backoff_ns = 256;
@@ -210,9 +212,10 @@ __device__ __forceinline__ void ds_wait_count(const unsigned* c, unsigned target
   named_bar(2, 256);
 }
 
-// One row-norm event of the decode stack, by warps 4-11 of EVERY CTA: rs[n] from the tile
-// partials (tile order), then this CTA's column slice of y = bf16(x * rs * w) for all rows,
-// then one release-add on c_norm.  dst == nullptr: nothing to normalise (count only).
+// The model's final RMSNorm (last layer of the last stage), by warps 4-11 of EVERY CTA: rs[n]
+// from the tile partials (tile order, the arithmetic of ds_row_scales), then this CTA's column
+// slice of y = bf16(x * rs * w) for all rows (one rounding: its consumer is the lm_head after
+// the kernel).
 __device__ __forceinline__ void ds_norm_slice(const DsParams& p, const bf16* __restrict__ src,
                                               const bf16* __restrict__ w, bf16* __restrict__ dst, int t, float* s_rs) {
   const int T = p.H / 128;
@@ -249,7 +252,31 @@ __device__ __forceinline__ void ds_norm_slice(const DsParams& p, const bf16* __r
     }
   }
   named_bar(2, 256);
-  if (t == 0) red_release_add(p.c_norm, 1u);
+}
+
+// rs[n] = 1/sqrt(sum_t ssq[t][n] / H + eps) for the N rows, by one warp: lane l sums tiles
+// t = l (mod 32) in order, then a fixed xor tree (the same arithmetic as ds_norm_slice).
+// Eight rows per batch with every load in flight.
+__device__ __forceinline__ void ds_row_scales(const DsParams& p, float* rs, int lane) {
+  const int T = p.H / 128;
+  for (int n0 = 0; n0 < p.N; n0 += 8) {
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    for (int tt = lane; tt < T; tt += 32) {
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = n0 + j < p.N ? __ldcg(p.ssq + (size_t)tt * DS_MAXSEQ + n0 + j) : 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += v[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+      if (lane == 0 && n0 + j < p.N) rs[n0 + j] = 1.0f / sqrtf(acc[j] / (float)p.H + p.eps);
+    }
+  }
 }
 
 // Stream-K parts travel as tagged words: the value's bits and the layer's tag in one 8-byte
@@ -507,7 +534,8 @@ template <int BN, int NC>
 __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsigned tag, int seg, uint32_t tmem,
                                            uint64_t* tfull, uint64_t* tempty, float* vals,
                                            int et, int lane, int quad,
-                                           const int* s_pos, const int* s_slot, const float2* s_rope) {
+                                           const int* s_pos, const int* s_slot, const float2* s_rope,
+                                           const float* s_rs, const volatile unsigned* s_rs_tag) {
   const int nkb = p.nkb[k], tiles = p.tiles[k];
   const long long W = (long long)tiles * nkb;
   int beg, end, Gk;
@@ -616,13 +644,18 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
     if (k == p_trace_k && et == 0) DS_TR(TR_Q_LAST);
     const int m = t * 128 + ml;
     const int H = p.H;
-    if (k == 0) {  // bf16(q, k, v); RoPE of q, k; k', v -> paged pool; q' -> q
+    const float* rs = s_rs + (k >> 1) * DS_MAXSEQ;  // QKV / gate_up: the operand's row scales (R10b)
+    if (k == 0 || k == 2) {  // computed by this CTA's activation producer (warp 2) once c_rows completed
+      while (s_rs_tag[k >> 1] != tag) __nanosleep(32);
+      __threadfence_block();
+    }
+    if (k == 0) {  // bf16(rs q, rs k, rs v); RoPE of q, k; k', v -> paged pool; q' -> q
       for (int n0 = 0; n0 < p.N; n0 += NC) {
         float a[NC];
         sums(n0, a);
 #pragma unroll
         for (int j = 0; j < NC; ++j)
-          if (n0 + j < p.N) vals[ml * DsCfg<BN, NC>::VS + n0 + j] = __bfloat162float(__float2bfloat16_rn(a[j]));
+          if (n0 + j < p.N) vals[ml * DsCfg<BN, NC>::VS + n0 + j] = __bfloat162float(__float2bfloat16_rn(rs[n0 + j] * a[j]));
       }
       named_bar(1, 128);
       if (p_trace_k == 0 && et == 0) DS_TR(TR_Q_VALS);
@@ -663,6 +696,7 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
         sums(n0, a);
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
+          a[j] *= n0 + j < p.N ? rs[n0 + j] : 1.0f;
           const float u = __shfl_xor_sync(0xffffffffu, a[j], 16);
           if (lane < 16 && n0 + j < p.N)
             p.act[(size_t)(n0 + j) * p.F + (m >> 5) * 16 + lane] = __float2bfloat16_rn(silu_f(a[j]) * u);
@@ -675,6 +709,10 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
     } else {  // residual: h = bf16(x + o W_o^T) (k = 1) / x' = bf16(h + a W_d^T) (k = 3)
       const bf16* resid = k == 1 ? (l == 0 ? p.x_in : p.x) : p.hbuf;
       bf16* out = k == 1 ? p.hbuf : p.x;
+      // the next GEMM's operand bf16(y * w) (gate_up's ffn_norm / the next layer's attn_norm)
+      const bf16* wn = k == 1 ? p.ffn_norm + (size_t)l * p.norm_stride
+                              : (l + 1 < p.nl ? p.attn_norm + (size_t)(l + 1) * p.norm_stride : nullptr);
+      const float gw = wn ? __bfloat162float(__ldg(wn + m)) : 0.f;
       for (int n0 = 0; n0 < p.N; n0 += NC) {
         float r[NC], a[NC];
 #pragma unroll
@@ -689,6 +727,7 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
           a[j] = n0 + j < p.N ? __bfloat162float(y) : 0.f;
           if (n0 + j < p.N) {
             out[(size_t)(n0 + j) * H + m] = y;
+            if (wn) p.nrm[(size_t)(n0 + j) * H + m] = __float2bfloat16_rn(a[j] * gw);
             if (p.cap) p.cap[(size_t)(2 * l + (k == 3 ? 1 : 0)) * p.cap_stride + (size_t)(n0 + j) * H + m] = y;
           }
         }
@@ -696,6 +735,7 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
       }
       if (k == p_trace_k && et == 0) DS_TR(TR_Q_VALS);
       if (et == 0) red_release_add(p.c_rows, 1u);  // rows of this tile + their partial sums
+      if (et == 0 && wn) publish(p.f_nrm[k == 1 ? 1 : 0] + t, k == 1 ? tag : tag + 1);  // consumer's layer
       if (k == p_trace_k && et == 0) DS_TR(TR_Q_PUB);
     }
     if (held) {  // every read of the held accumulator done: the MMA may reuse the buffer
@@ -720,8 +760,7 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
   float* vals = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES);
   float2* s_rope = reinterpret_cast<float2*>(smem + C::STAGES * C::STAGE_BYTES + C::VALS_BYTES);
   float* s_att = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + C::VALS_BYTES + C::ROPE_BYTES);
-  uint4* s_xn = reinterpret_cast<uint4*>(smem + C::STAGES * C::STAGE_BYTES + C::VALS_BYTES + C::ROPE_BYTES + C::ATT_BYTES);
-  uint8_t* misc = smem + C::STAGES * C::STAGE_BYTES + C::VALS_BYTES + C::ROPE_BYTES + C::ATT_BYTES + C::XN_BYTES;
+  uint8_t* misc = smem + C::STAGES * C::STAGE_BYTES + C::VALS_BYTES + C::ROPE_BYTES + C::ATT_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(misc);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
@@ -733,11 +772,17 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
   int* s_pos = s_base + DS_MAXSEQ + 4;                                                 // [64]
   int* s_slot = s_pos + DS_MAXSEQ;                                                     // [64]
   volatile int* s_prog = s_slot + DS_MAXSEQ;                                           // [1] k-blocks issued
+  volatile unsigned* s_rs_tag = reinterpret_cast<volatile unsigned*>(s_prog + 1);       // [2] tag of s_rs[0 / 1]
+  float* s_rs = reinterpret_cast<float*>(const_cast<int*>(s_prog) + 4);                // [2][64] row scales
+  static_assert(DsCfg<BN, NC>::STAGES * 16 + 32 + 16 + 32 + (64 + 68 + 64 + 64 + 4 + 128) * 4 <= DsCfg<BN, NC>::MISC,
+                "misc shared memory");
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int G = p.G;
 
   if (threadIdx.x == 0) {
     *s_prog = 0;
+    s_rs_tag[0] = 0;
+    s_rs_tag[1] = 0;
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 2); mbar_init(&empty[s], 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -834,80 +879,17 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
         int beg, end, Gk;
         ds_range(blockIdx.x, W, G, beg, end, Gk);
         if (beg == end) continue;
-        if constexpr (NC == 1) {
-          if (k == 0 || k == 2) {
-            // single-sequence decode: this warp normalises the row itself (tile partial sums ->
-            // rs, then bf16(x * rs * w) into shared memory) and writes each k-block's activation
-            // tile straight into its ring slot: no global round trip, no TMA for these phases
-            const int T = p.H / 128, n8 = p.H >> 3;
-            if (lane == 0) wait_tag(p.c_rows, p.base_rows + (unsigned)T * (unsigned)(2 * l + (k == 0 ? 1 : 2)));
-            __syncwarp();
-            if (p.trace && lane == 0) DS_TR(k);
-            const bf16* src = k == 0 ? (l == 0 ? p.x_in : p.x) : p.hbuf;
-            const uint4* x4 = reinterpret_cast<const uint4*>(src);
-            const uint4* w4 = reinterpret_cast<const uint4*>(k == 0 ? p.attn_norm + (size_t)l * p.norm_stride
-                                                                    : p.ffn_norm + (size_t)l * p.norm_stride);
-            float acc = 0.f;
-            for (int tt = lane; tt < T; tt += 32) acc += __ldcg(p.ssq + (size_t)tt * DS_MAXSEQ);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            const float rs = 1.0f / sqrtf(acc / (float)p.H + p.eps);
-            for (int c0 = 0; c0 < n8; c0 += 256) {
-              uint4 xv[8], wv[8];
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const int c = c0 + j * 32 + lane;
-                if (c < n8) { xv[j] = __ldcg(x4 + c); wv[j] = __ldg(w4 + c); }
-              }
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const int c = c0 + j * 32 + lane;
-                if (c < n8) {
-                  uint4 o;
-                  const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(&xv[j]);
-                  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&wv[j]);
-                  __nv_bfloat162* rr = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-                  for (int q = 0; q < 4; ++q) {
-                    const float2 xa = __bfloat1622float2(a[q]), g = __bfloat1622float2(b[q]);
-                    rr[q] = __floats2bfloat162_rn(xa.x * rs * g.x, xa.y * rs * g.y);
-                  }
-                  s_xn[c] = o;
-                }
-              }
-            }
-            __syncwarp();
-            // token row 0 of each k-block's tile (rows >= N are never drained), one slot at a
-            // time, 8 lanes (128 bytes): a slot is completed the moment it is free, so the MMA
-            // never waits on later slots (a 4-slot batch here cost ~3 slots of ring depth)
-            for (int x = beg; x < end; ++x, ++i) {
-              const int s = i % C::STAGES;
-              if (lane == 0) mbar_wait(&empty[s], ((i / C::STAGES) & 1) ^ 1);
-              __syncwarp();
-              if (lane < 8) {
-                uint4* dst = reinterpret_cast<uint4*>(smem + s * C::STAGE_BYTES + C::A_BYTES);
-                dst[lane] = s_xn[(x % nkb) * 8 + lane];  // row 0: 16-byte chunk c at c ^ 0
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-              }
-              __syncwarp();
-              if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
-            }
-            continue;
-          }
-        } else if (k == 0 || k == 2) {  // the row norm feeding this GEMM: every CTA's slice written
-          if (lane == 0) wait_tag(p.c_norm, p.base_norm + (unsigned)(2 * l + (k == 0 ? 1 : 2)) * (unsigned)G);
-          __syncwarp();
-        }
-
         for (int x0 = beg; x0 < end; x0 += 32) {
           const int cnt = min(32, end - x0);
           const int kbl = (x0 + lane) % nkb;
-          const unsigned* f = k == 1 ? p.f_attn + (kbl * 64) / p.hd : p.f_gu + kbl;
+          // QKV / gate_up: the operand tile (128 columns = 2 k-blocks) of the residual tile that
+          // produced it; O: the head; down: the gate_up tile
+          const unsigned* f = k == 1 ? p.f_attn + (kbl * 64) / p.hd : k == 3 ? p.f_gu + kbl : p.f_nrm[k >> 1] + (kbl >> 1);
           int issued = 0;
           unsigned long long t_spin = 0;
           while (issued < cnt) {
             bool ok = lane < issued || lane >= cnt;
-            if (!ok) ok = (k == 0 || k == 2) || (int)(ld_acquire(f) - tag) >= 0;
+            if (!ok) ok = (int)(ld_acquire(f) - tag) >= 0;
             const unsigned mask = __ballot_sync(0xffffffffu, ok);
             const int upto = min(cnt, mask == 0xffffffffu ? 32 : __ffs(~mask) - 1);
             __syncwarp();
@@ -933,6 +915,18 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
         }
         i += end - beg;
         if (k == 3 && lane == 0) DS_TR(TR_B3_END);
+        if (k == 0 || k == 2) {
+          // the row scales of this operand for the QKV / gate_up epilogues (they run after this
+          // CTA's last k-block of the phase): every residual tile's partials are in once c_rows
+          // reached the event's count (events: stage input, then O / down of each layer)
+          const int T = p.H / 128;
+          if (lane == 0) wait_tag(p.c_rows, p.base_rows + (unsigned)T * (unsigned)(2 * l + (k == 0 ? 1 : 2)));
+          __syncwarp();
+          ds_row_scales(p, s_rs + (k >> 1) * DS_MAXSEQ, lane);
+          __syncwarp();
+          __threadfence_block();
+          if (lane == 0) s_rs_tag[k >> 1] = tag;
+        }
       }
     }
   } else if (warp >= 4) {
@@ -969,19 +963,25 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
     // stays resident in the instruction cache): step (l, k) = [pending row norm] -> GEMM k's
     // segments (epilogue warps) -> attention (k = 0) -> grid-last check (k = 1, 3).
     const int T = p.H / 128;
-    {  // the stage input's RMSNorm (layer 0): CTA c < T publishes tile c's partial sums of x_in
+    {  // the stage input (layer 0's QKV operand): CTA c < T writes tile c of bf16(x_in * w) and
+       // its partial sums of squares, as a residual tile does for the later layers
       if (blockIdx.x < T && epi) {
+        const int m = blockIdx.x * 128 + t256;
+        const float gw = __bfloat162float(__ldg(p.attn_norm + m));
         for (int n0 = 0; n0 < p.N; n0 += NC) {
           float v[NC];
 #pragma unroll
-          for (int j = 0; j < NC; ++j)
-            v[j] = n0 + j < p.N ? __bfloat162float(__ldcg(p.x_in + (size_t)(n0 + j) * p.H + blockIdx.x * 128 + t256)) : 0.f;
+          for (int j = 0; j < NC; ++j) {
+            v[j] = n0 + j < p.N ? __bfloat162float(__ldcg(p.x_in + (size_t)(n0 + j) * p.H + m)) : 0.f;
+            if (n0 + j < p.N) p.nrm[(size_t)(n0 + j) * p.H + m] = __float2bfloat16_rn(v[j] * gw);
+          }
           ds_ssq_chunk<NC>(v, n0, p.N, t256, vals, p.ssq + (size_t)blockIdx.x * DS_MAXSEQ);
         }
-        if (t256 == 0) red_release_add(p.c_rows, 1u);
+        if (t256 == 0) {
+          red_release_add(p.c_rows, 1u);
+          publish(p.f_nrm[0] + blockIdx.x, p.tag0);
+        }
       }
-      ds_wait_count(p.c_rows, p.base_rows + (unsigned)T, t256);
-      ds_norm_slice(p, p.x_in, p.attn_norm, NC == 1 ? nullptr : p.nrm, t256, s_att);  // NC == 1: the B producer normalises
       const int l = 0;
       if (t256 == 0) DS_TR(TR_E_NA);
     }
@@ -998,7 +998,7 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
         }
       }
       if (epi) seg = ds_segments<BN, NC>(p, k, l, tag, seg, tmem, tfull, tempty, vals, t256, lane, quad,
-                                     s_pos, s_slot, s_rope);
+                                     s_pos, s_slot, s_rope, s_rs, s_rs_tag);
       if (t256 == 0) DS_TR(TR_E_QKV + (k == 0 ? 0 : k == 1 ? 2 : k == 2 ? 4 : 5));
       if (k == 0) {
         // units (seq, head, split) over the CTAs; every CTA loops uniformly
@@ -1011,17 +1011,11 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
           else ds_attn_unit<64>(p, l, tag, i, r / nsp, r % nsp, nsp, u, t256, s_att, total / p.nh, s_nc, s_base);
         }
         if (t256 == 0) DS_TR(TR_E_ATTN);
-      } else if (k == 1 || k == 3) {  // row-norm event 2l+1 (ffn) / 2l+2 (next attn or final)
-        const unsigned ev = (unsigned)(2 * l + (k == 1 ? 1 : 2));
-        ds_wait_count(p.c_rows, p.base_rows + (unsigned)T * (ev + 1), t256);
-        if (t256 == 0) DS_TR(k == 1 ? TR_O_LAST : TR_D_LAST);
-        if (k == 1)
-          ds_norm_slice(p, p.hbuf, p.ffn_norm + (size_t)l * p.norm_stride, NC == 1 ? nullptr : p.nrm, t256, s_att);
-        else if (l + 1 < p.nl)
-          ds_norm_slice(p, p.x, p.attn_norm + (size_t)(l + 1) * p.norm_stride, NC == 1 ? nullptr : p.nrm, t256, s_att);
-        else
-          ds_norm_slice(p, p.x, p.final_norm, p.final_norm ? p.fin : nullptr, t256, s_att);
-        if (t256 == 0) DS_TR(k == 1 ? TR_E_NF : TR_E_NA);
+      } else if (k == 3 && l + 1 == p.nl && p.final_norm) {  // the model's final norm (event 2l+2)
+        ds_wait_count(p.c_rows, p.base_rows + (unsigned)T * (unsigned)(2 * l + 3), t256);
+        if (t256 == 0) DS_TR(TR_D_LAST);
+        ds_norm_slice(p, p.x, p.final_norm, p.fin, t256, s_att);
+        if (t256 == 0) DS_TR(TR_E_NA);
       }
     }
   }
@@ -1044,7 +1038,7 @@ struct DstackState {
   size_t ctr_words = 0;
   unsigned seq_no = 0;
   float* ssq = nullptr;                 // [H / 128][64] row sum-of-squares partials
-  unsigned base_rows = 0, base_norm = 0;  // cumulative counter values at the next launch
+  unsigned base_rows = 0;  // cumulative c_rows value at the next launch
 };
 
 // HS debug: per-CTA phase timestamps of the last launch (hs_debug_dstack_trace)
@@ -1217,15 +1211,14 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
   p.c_h = c + o; o += s->nh;
   o = align_up(o, 32);
   p.c_rows = c + o; o += 32;
-  p.c_norm = c + o; o += 32;
+  p.f_nrm[0] = c + o; o += align_up((size_t)(s->H / 128), 32);
+  p.f_nrm[1] = c + o; o += align_up((size_t)(s->H / 128), 32);
   p.f_qkv = c + o; o += s->tiles[0];
   p.f_attn = c + o; o += s->nh;
   p.f_gu = c + o; o += s->tiles[2];
   p.ssq = s->ssq;
   p.base_rows = s->base_rows;
-  p.base_norm = s->base_norm;
   s->base_rows += (unsigned)(s->H / 128) * (unsigned)(2 * a.nl + 1);
-  s->base_norm += (unsigned)s->G * (unsigned)(2 * a.nl + 1);
   if (o > s->ctr_words) HS_FAIL(HS_E_INVAL, "dstack: counter layout overflow");
   switch (BN) {
     case 16: return a.N == 1 ? launch_bn<16, 1>(s, a, p, bi, st) : launch_bn<16, 8>(s, a, p, bi, st);

@@ -26,6 +26,16 @@
 
 namespace hs {
 
+// R10b: the accumulator of token n scaled by the RMSNorm row scale before a bf16 / SiLU
+// epilogue (rs == null: unchanged, x * 1.0f is exact)
+template <int CH>
+__device__ __forceinline__ void scale_rows(float* v, const float* rs, int n0, int ncol) {
+  if (!rs) return;
+#pragma unroll
+  for (int j = 0; j < CH; ++j)
+    if (j < ncol) v[j] *= __ldg(rs + n0 + j);
+}
+
 struct KParams {
   int M, N, K;
   int kb_per_split;  // K blocks (of 64) per split
@@ -36,6 +46,7 @@ struct KParams {
   const bf16* resid;
   int ldr;
   float* ws;
+  const float* rs;
 };
 
 template <int BN>
@@ -138,6 +149,7 @@ __global__ void __launch_bounds__(128, 1)
     else tmem_ld16(trow + c0, v);
     if (n0 + c0 >= p.N) break;  // warp-uniform
     const int ncol = min(CH, p.N - n0 - c0);
+    if (p.epi == EPI_BF16 || p.epi == EPI_SILU_MUL) scale_rows<CH>(v, p.rs, n0 + c0, ncol);
     if (p.epi < 0) {
       float* ws = p.ws + ((size_t)blockIdx.z * p.N + n0 + c0) * p.M;
       if (m < p.M)
@@ -188,7 +200,7 @@ __global__ void __launch_bounds__(128, 1)
 // Deterministic split-K reduction: sums the partials in split order, then the epilogue.
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N,
                                      int epi, void* out, int ldo, const bf16* __restrict__ resid,
-                                     int ldr) {
+                                     int ldr, const float* __restrict__ rs) {
   PDL_LAUNCH();
   PDL_WAIT();
   const int n = blockIdx.y;
@@ -196,6 +208,8 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
   if (m >= M) return;
   float acc = 0.f;
   for (int s = 0; s < splits; ++s) acc += ws[((size_t)s * N + n) * M + m];
+  const float rsn = (rs && (epi == EPI_BF16 || epi == EPI_SILU_MUL)) ? rs[n] : 1.0f;
+  acc *= rsn;
   if (epi == EPI_F32) {
     reinterpret_cast<float*>(out)[(size_t)n * ldo + m] = acc;
   } else if (epi == EPI_BF16) {
@@ -208,6 +222,7 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
     if (j < 16) {
       float u = 0.f;
       for (int s = 0; s < splits; ++s) u += ws[((size_t)s * N + n) * M + m + 16];
+      u *= rsn;
       reinterpret_cast<bf16*>(out)[(size_t)n * ldo + (m >> 5) * 16 + j] =
           __float2bfloat16_rn(silu_f(acc) * u);
     }
@@ -241,6 +256,8 @@ struct SkParams {
   int fuse;
   const bf16* norm_w;
   bf16* norm_out;
+  float* rs_out;
+  const float* rs;
   float eps;
   const int* pos;
   const int* slot;
@@ -256,7 +273,8 @@ struct SkParams {
 // so the GEMM epilogue and the standalone decode row-norm run the very same code (PP = s
 // stays bitwise equal to PP = 1 across the stage boundary).
 __device__ __noinline__ void row_norm128(const bf16* __restrict__ h, int M, const bf16* __restrict__ w,
-                                         bf16* __restrict__ y, float eps, int tid, float* red, int bar_id) {
+                                         bf16* __restrict__ y, float* rs_out, float eps, int tid, float* red,
+                                         int bar_id) {
   // 16-byte loads (8 values), all issued before use; fixed per-thread summation order
   const int n8 = M >> 3;
   const uint4* h4 = reinterpret_cast<const uint4*>(h);
@@ -285,7 +303,9 @@ __device__ __noinline__ void row_norm128(const bf16* __restrict__ h, int M, cons
   if ((tid & 31) == 0) red[tid >> 5] = ss;
   named_bar(bar_id, 128);
   const float tot = (red[0] + red[1]) + (red[2] + red[3]);
-  const float rs = 1.0f / sqrtf(tot / (float)M + eps);
+  const float rs_row = 1.0f / sqrtf(tot / (float)M + eps);
+  if (rs_out && tid == 0) *rs_out = rs_row;
+  const float rs = rs_out ? 1.0f : rs_row;  // R10b: the operand is bf16(x * w), rs scales the product
   const uint4* w4 = reinterpret_cast<const uint4*>(w);
   uint4* y4 = reinterpret_cast<uint4*>(y);
   for (int c = tid; c < n8; c += 128) {
@@ -459,6 +479,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int n = 0; n < p.N; ++n) {
           float a = 0.f;
           for (int pt = 0; pt < np; ++pt) a += __ldcg(tws + (size_t)pt * BN * 128 + (size_t)n * 128 + ml);
+          if (p.rs) a *= __ldg(p.rs + n);
           vals[ml * BN + n] = __bfloat162float(__float2bfloat16_rn(a));
         }
         named_bar(1, 128);
@@ -493,6 +514,7 @@ __global__ void __launch_bounds__(192, 1)
       for (int n = 0; n < p.N; ++n) {
         float a = 0.f;
         for (int pt = 0; pt < np; ++pt) a += __ldcg(tws + (size_t)pt * BN * 128 + (size_t)n * 128 + ml);
+        if (p.rs && (p.epi == EPI_BF16 || p.epi == EPI_SILU_MUL)) a *= __ldg(p.rs + n);
         if (p.epi == EPI_F32) {
           reinterpret_cast<float*>(p.out)[(size_t)n * p.ldo + m] = a;
         } else if (p.epi == EPI_BF16) {
@@ -521,7 +543,7 @@ __global__ void __launch_bounds__(192, 1)
         if (*flag) {
           for (int n = 0; n < p.N; ++n)
             row_norm128(reinterpret_cast<const bf16*>(p.out) + (size_t)n * p.ldo, p.M, p.norm_w,
-                        p.norm_out + (size_t)n * p.ldo, p.eps, et, red, 1);
+                        p.norm_out + (size_t)n * p.ldo, p.rs_out ? p.rs_out + n : nullptr, p.eps, et, red, 1);
         }
       }
     }
@@ -548,6 +570,7 @@ struct TpParams {
   int ldr;
   int splits = 1, kbps = 0;  // split-K (tp2 only): work item = tile * splits + split
   float* ws = nullptr;       // fp32 partials [split][N][M] when splits > 1
+  const float* rs = nullptr;
 };
 
 template <int BN>
@@ -660,6 +683,7 @@ __global__ void __launch_bounds__(192, 1)
         tmem_ld32(trow + c0, v);
         if (n0 + c0 < p.N) {
           const int ncol = min(32, p.N - n0 - c0);
+          if (p.epi == EPI_BF16 || p.epi == EPI_SILU_MUL) scale_rows<32>(v, p.rs, n0 + c0, ncol);
           if (p.epi == EPI_F32) {
             float* o = reinterpret_cast<float*>(p.out) + (size_t)(n0 + c0) * p.ldo;
 #pragma unroll
@@ -701,11 +725,12 @@ __global__ void __launch_bounds__(192, 1)
 
 // Decode RMSNorm with the exact arithmetic of the fused epilogue (one 128-thread CTA per row).
 __global__ void __launch_bounds__(128) rownorm_kernel(const bf16* __restrict__ x, const bf16* __restrict__ w,
-                                                      bf16* __restrict__ y, int H, float eps) {
+                                                      bf16* __restrict__ y, float* rs_out, int H, float eps) {
   PDL_LAUNCH();
   PDL_WAIT();
   __shared__ float red[4];
-  row_norm128(x + (size_t)blockIdx.x * H, H, w, y + (size_t)blockIdx.x * H, eps, threadIdx.x, red, 1);
+  row_norm128(x + (size_t)blockIdx.x * H, H, w, y + (size_t)blockIdx.x * H, rs_out ? rs_out + blockIdx.x : nullptr,
+              eps, threadIdx.x, red, 1);
 }
 
 // ------------------------------------------------------------------ host side -----------
@@ -847,14 +872,14 @@ static hs_status launch(const GemmArgs& a, int splits, int kbps, cudaStream_t st
   p.nkb = a.K / 64;
   p.kb_per_split = kbps;
   p.epi = splits > 1 ? -1 : a.epi;
-  p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr; p.ws = a.workspace;
+  p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr; p.ws = a.workspace; p.rs = a.rs;
   dim3 grid(cdiv(a.M, 128), cdiv(a.N, BN), splits);
   launchk(gemm_kernel<BN>, grid, 128, C::SMEM, st, a.A->map, tb.map, p);
   count_launch();
   HS_CUDA(cudaGetLastError());
   if (splits > 1) {
     dim3 g2(cdiv(a.M, 256), a.N);
-    launchk(splitk_reduce_kernel, g2, 256, 0, st, (const float*)a.workspace, splits, a.M, a.N, a.epi, a.out, a.ldo, a.resid, a.ldr);
+    launchk(splitk_reduce_kernel, g2, 256, 0, st, (const float*)a.workspace, splits, a.M, a.N, a.epi, a.out, a.ldo, a.resid, a.ldr, a.rs);
     count_launch();
     HS_CUDA(cudaGetLastError());
   }
@@ -928,8 +953,8 @@ static hs_status launch_sk(const GemmArgs& a, cudaStream_t st, bool* done) {
   SkParams p{};
   p.M = a.M; p.N = a.N; p.nkb = nkb; p.tiles = tiles; p.G = G; p.maxp = maxp;
   p.ws = a.workspace; p.ctr = a.counters;
-  p.epi = a.epi; p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr;
-  p.fuse = f.kind; p.norm_w = f.norm_w; p.norm_out = f.norm_out; p.eps = f.eps;
+  p.epi = a.epi; p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr; p.rs = a.rs;
+  p.fuse = f.kind; p.norm_w = f.norm_w; p.norm_out = f.norm_out; p.rs_out = f.rs_out; p.eps = f.eps; p.rs = a.rs;
   p.pos = f.pos; p.slot = f.slot; p.tab = f.rope_tab; p.q_out = f.q_out; p.pool = f.pool;
   p.nh = f.n_heads; p.hd = f.head_dim; p.nslots = f.nslots;
   p.trace = g_sk_trace;
@@ -957,7 +982,7 @@ static hs_status launch_tp(const GemmArgs& a, cudaStream_t st) {
   if (a.B[bi].box_rows != BN) HS_FAIL(HS_E_INVAL, "TMA box mismatch");
   TpParams p{};
   p.M = a.M; p.N = a.N; p.nkb = a.K / 64; p.m_tiles = a.M / 128; p.n_tiles = (int)cdiv(a.N, BN);
-  p.epi = a.epi; p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr;
+  p.epi = a.epi; p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr; p.rs = a.rs;
   const int tiles = p.m_tiles * p.n_tiles;
   const int grid = std::min(tiles, num_sms(dev));
   launchk(gemm_tp_kernel<BN>, grid, 192, C::SMEM, st, a.A->map, a.B[bi].map, p);
@@ -1106,6 +1131,7 @@ __global__ void __launch_bounds__(192, 1)
         tmem_ld32(trow + c0, v);
         if (n0 + c0 < p.N) {
           const int ncol = min(32, p.N - n0 - c0);
+          if (p.splits <= 1 && (p.epi == EPI_BF16 || p.epi == EPI_SILU_MUL)) scale_rows<32>(v, p.rs, n0 + c0, ncol);
           if (p.splits > 1) {  // fp32 partial of this split (reduced by splitk_reduce_kernel)
             float* o = p.ws + ((size_t)sp * p.N + n0 + c0) * p.M;
 #pragma unroll
@@ -1166,7 +1192,7 @@ static hs_status launch_tp2(const GemmArgs& a, cudaStream_t st, int splits = 1) 
   if (a.B[bi].box_rows != BN / 2) HS_FAIL(HS_E_INVAL, "TMA box mismatch");
   TpParams p{};
   p.M = a.M; p.N = a.N; p.nkb = a.K / 64; p.m_tiles = a.M / 256; p.n_tiles = (int)cdiv(a.N, BN);
-  p.epi = a.epi; p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr;
+  p.epi = a.epi; p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr; p.rs = a.rs;
   p.kbps = (int)cdiv(p.nkb, splits);
   p.splits = (int)cdiv(p.nkb, p.kbps);
   p.ws = a.workspace;
@@ -1197,15 +1223,16 @@ static hs_status launch_tp2(const GemmArgs& a, cudaStream_t st, int splits = 1) 
   if (p.splits > 1) {
     dim3 g2(cdiv(a.M, 256), a.N);
     launchk(splitk_reduce_kernel, g2, 256, 0, st, (const float*)a.workspace, p.splits, a.M, a.N, a.epi, a.out, a.ldo,
-            a.resid, a.ldr);
+            a.resid, a.ldr, a.rs);
     count_launch();
     HS_CUDA(cudaGetLastError());
   }
   return HS_OK;
 }
 
-void launch_rownorm_decode(const bf16* x, const bf16* w, bf16* y, int T, int H, float eps, cudaStream_t st) {
-  launchk(rownorm_kernel, T, 128, 0, st, x, w, y, H, eps);
+void launch_rownorm_decode(const bf16* x, const bf16* w, bf16* y, float* rs_out, int T, int H, float eps,
+                           cudaStream_t st) {
+  launchk(rownorm_kernel, T, 128, 0, st, x, w, y, rs_out, H, eps);
   count_launch();
 }
 

@@ -9,6 +9,8 @@
 
 namespace hs {
 
+// rs (optional, GemmArgs::rs): the RMSNorm row scale of reading R10b — the activations are
+// bf16(x * w) and EPI_BF16 / EPI_SILU_MUL (and FUSE_ROPE) use rs[n] * acc in place of acc.
 enum GemmEpi : int {
   EPI_BF16 = 0,      // out = bf16(acc)
   EPI_RESID = 1,     // out = bf16(acc + resid)            (O-proj, down: single rounding)
@@ -41,6 +43,7 @@ hs_status make_tma_w3(TmaMat* t, const void* ptr, int64_t layers, int64_t layer_
 // Decode-path fusions applied by the stream-K reduction (the whole output row of a token is
 // available there):
 //   FUSE_NORM : out = bf16(acc + resid) (as EPI_RESID) and norm_out = RMSNorm(out) * norm_w
+//               (rs_out != null: norm_out = bf16(out * norm_w), rs_out[n] = the row scale, R10b)
 //   FUSE_ROPE : (QKV GEMM, EPI_BF16) q, k, v = bf16(acc); q' / k' rotated (RoPE table), q' to
 //               q_out, k' and v written into the paged KV pool at slot[n]
 enum GemmFuse : int { FUSE_NONE = 0, FUSE_NORM = 1, FUSE_ROPE = 2 };
@@ -48,6 +51,7 @@ struct GemmFusion {
   int kind = FUSE_NONE;
   const bf16* norm_w = nullptr;
   bf16* norm_out = nullptr;
+  float* rs_out = nullptr;
   float eps = 0.f;
   const int* pos = nullptr;
   const int* slot = nullptr;
@@ -68,6 +72,7 @@ struct GemmArgs {
   int ldo;           // elements
   const bf16* resid; // EPI_RESID: resid[n * ldr + m]
   int ldr;
+  const float* rs = nullptr;  // EPI_BF16 / EPI_SILU_MUL: per-token scale of the accumulator (R10b)
   float* workspace;  // split-K / stream-K partials (may be null => no split)
   uint64_t workspace_bytes;
   unsigned* counters;  // stream-K arrival counters: >= M/128 + 1 zeroed words (null => no stream-K)
@@ -85,7 +90,8 @@ hs_status gemm(const GemmArgs& a, cudaStream_t stream);
 
 // RMSNorm of T rows with exactly the arithmetic of the FUSE_NORM epilogue (decode path: a
 // stage's first layer normalises its input like the previous layer's fused epilogue would,
-// so PP = s stays bitwise equal to PP = 1).  H <= 8192.
-void launch_rownorm_decode(const bf16* x, const bf16* w, bf16* y, int T, int H, float eps, cudaStream_t st);
+// so PP = s stays bitwise equal to PP = 1).  H <= 8192.  rs_out: as GemmFusion::rs_out.
+void launch_rownorm_decode(const bf16* x, const bf16* w, bf16* y, float* rs_out, int T, int H, float eps,
+                           cudaStream_t st);
 
 }  // namespace hs

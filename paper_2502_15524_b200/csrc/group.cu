@@ -82,6 +82,7 @@ struct Stage {
   bool ipc_arena_open = false, ipc_comm_open = false;
   Share share{};
   // work buffers (owned)
+  float* nrm_rs = nullptr;  // row scales of s.nrm's rows (reading R10b: s.nrm = bf16(x * w))
   bf16 *xa = nullptr, *xb = nullptr, *nrm = nullptr, *qkv = nullptr, *q = nullptr, *o = nullptr,
        *act = nullptr, *fin = nullptr;
   float *logits = nullptr, *ws = nullptr, *attn_ws = nullptr;
@@ -267,7 +268,7 @@ static void free_stage(Stage& s, bool keep_exported = false) {
   auto F = [](void* p) { if (p) cudaFree(p); };
   if (s.owned) {
     if (!keep_exported) { F(s.arena); F(s.kv_mem); F(s.comm); }
-    F(s.xa); F(s.xb); F(s.nrm); F(s.qkv); F(s.q); F(s.o);
+    F(s.xa); F(s.xb); F(s.nrm); F(s.nrm_rs); F(s.qkv); F(s.q); F(s.o);
     F(s.act); F(s.fin); F(s.cap); F(s.logits); F(s.ws); F(s.attn_ws); F(s.ctr); F(s.rope); F(s.d_meta); F(s.d_tok_out);
     F(s.cons_d);
     if (s.cons_h) cudaFreeHost(s.cons_h);
@@ -331,6 +332,7 @@ static hs_status setup_owned_stage(hs_group* g, int k) {
   HS_ALLOC(s.xa, (size_t)T * H * 2);
   HS_ALLOC(s.xb, (size_t)T * H * 2);
   HS_ALLOC(s.nrm, (size_t)T * H * 2);
+  HS_ALLOC(s.nrm_rs, (size_t)T * 4);
   HS_ALLOC(s.qkv, (size_t)T * 3 * H * 2);
   HS_ALLOC(s.q, (size_t)T * H * 2);
   HS_ALLOC(s.o, (size_t)T * H * 2);
@@ -729,13 +731,13 @@ static hs_status run_layer(hs_group* g, Stage& s, int l, const bf16* x, bf16* xo
   const double TH2 = 2.0 * T * H, F = c.ffn;
   if (!normed && !(skip & 32)) {
     ProfScope ps(g, s, PK_RMSNORM, dec, 2 * TH2 + 2.0 * H, 0);
-    if (dec && H <= 8192) launch_rownorm_decode(x, L.attn_norm, s.nrm, T, H, c.rms_eps, st);
-    else launch_rmsnorm(x, nullptr, L.attn_norm, s.nrm, T, H, c.rms_eps, st);
+    if (dec && H <= 8192) launch_rownorm_decode(x, L.attn_norm, s.nrm, s.nrm_rs, T, H, c.rms_eps, st);
+    else launch_rmsnorm(x, nullptr, L.attn_norm, s.nrm, T, H, c.rms_eps, st, s.nrm_rs);
   }
   bool applied = false;
   GemmArgs a{};
   a.N = T; a.K = H; a.workspace = s.ws; a.workspace_bytes = kWorkspace; a.counters = s.ctr;
-  a.A = &L.wqkv; a.B = s.b_nrm; a.M = 3 * H; a.epi = EPI_BF16; a.out = s.qkv; a.ldo = 3 * H;
+  a.A = &L.wqkv; a.B = s.b_nrm; a.M = 3 * H; a.epi = EPI_BF16; a.out = s.qkv; a.ldo = 3 * H; a.rs = s.nrm_rs;
   if (dec) {  // fused bf16 rounding + RoPE + paged KV write in the stream-K reduction
     a.fuse.kind = FUSE_ROPE; a.fuse.pos = pos; a.fuse.slot = slot; a.fuse.rope_tab = s.rope; a.fuse.q_out = s.q;
     a.fuse.pool = pool; a.fuse.n_heads = c.n_heads; a.fuse.head_dim = c.head_dim; a.fuse.applied = &applied;
@@ -762,8 +764,10 @@ static hs_status run_layer(hs_group* g, Stage& s, int l, const bf16* x, bf16* xo
   a.fuse = GemmFusion{};
   applied = false;
   a.A = &L.wo; a.B = s.b_o; a.M = H; a.K = H; a.epi = EPI_RESID; a.out = hbuf; a.ldo = H; a.resid = x; a.ldr = H;
+  a.rs = nullptr;
   if (dec) {  // fused residual + RMSNorm(ffn_norm)
     a.fuse.kind = FUSE_NORM; a.fuse.norm_w = L.ffn_norm; a.fuse.norm_out = s.nrm; a.fuse.eps = c.rms_eps;
+    a.fuse.rs_out = s.nrm_rs;
     a.fuse.applied = &applied;
   }
   if (!(skip & 4)) {
@@ -774,17 +778,17 @@ static hs_status run_layer(hs_group* g, Stage& s, int l, const bf16* x, bf16* xo
   }
   if (!applied) {
     ProfScope ps(g, s, PK_RMSNORM, dec, 2 * TH2 + 2.0 * H, 0);
-    launch_rmsnorm(hbuf, nullptr, L.ffn_norm, s.nrm, T, H, c.rms_eps, st);
+    launch_rmsnorm(hbuf, nullptr, L.ffn_norm, s.nrm, T, H, c.rms_eps, st, s.nrm_rs);
   }
   a.fuse = GemmFusion{};
   a.A = &L.wgu; a.B = s.b_nrm; a.M = 2 * c.ffn; a.K = H; a.epi = EPI_SILU_MUL; a.out = s.act; a.ldo = c.ffn;
-  a.resid = nullptr;
+  a.resid = nullptr; a.rs = s.nrm_rs;
   if (!(skip & 8)) {
     ProfScope ps(g, s, PK_GEMM_GU, dec, gemm_bytes(2 * F, T, H, F, false), 2.0 * 2 * F * T * H);
     HS_TRY(gemm(a, st));
   }
   a.A = &L.wd; a.B = s.b_act; a.M = H; a.K = c.ffn; a.epi = EPI_RESID; a.out = xout; a.ldo = H; a.resid = hbuf;
-  a.ldr = H;
+  a.ldr = H; a.rs = nullptr;
   applied = false;
   const bool next_here = l + 1 < s.le;
   const bool model_last = l + 1 == c.n_layers;
@@ -795,6 +799,7 @@ static hs_status run_layer(hs_group* g, Stage& s, int l, const bf16* x, bf16* xo
     if (next_here) {
       a.fuse.norm_w = s.layers[l + 1].attn_norm;
       a.fuse.norm_out = s.nrm;
+      a.fuse.rs_out = s.nrm_rs;
     } else {  // decode: every row is a sequence's last position -> final norm into s.fin
       a.fuse.norm_w = reinterpret_cast<const bf16*>(s.wptr(g->hdr.final_off + g->hdr.t_final_norm));
       a.fuse.norm_out = s.fin;

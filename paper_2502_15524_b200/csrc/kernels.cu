@@ -57,7 +57,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 template <int MAXV>
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const uint4* __restrict__ x, const int* __restrict__ rows,
                                                       const uint4* __restrict__ w, uint4* __restrict__ y,
-                                                      int H8, float inv_h, float eps) {
+                                                      float* __restrict__ rs_out, int H8, float inv_h, float eps) {
   PDL_LAUNCH();
   PDL_WAIT();
   __shared__ float red[8];
@@ -85,7 +85,9 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const uint4* __restrict__ 
   float tot = 0.f;
 #pragma unroll
   for (int k = 0; k < 8; ++k) tot += red[k];
-  const float rs = 1.0f / sqrtf(tot * inv_h + eps);
+  const float rs_row = 1.0f / sqrtf(tot * inv_h + eps);
+  if (rs_out && threadIdx.x == 0) rs_out[i] = rs_row;
+  const float rs = rs_out ? 1.0f : rs_row;  // R10b: y = bf16(x * w), the scale goes to the GEMM epilogue
 #pragma unroll
   for (int j = 0; j < MAXV; ++j) {
     const int c = threadIdx.x + j * 256;
@@ -105,16 +107,16 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const uint4* __restrict__ 
 }
 
 void launch_rmsnorm(const bf16* x, const int* rows, const bf16* w, bf16* y, int T, int H,
-                    float eps, cudaStream_t st) {
+                    float eps, cudaStream_t st, float* rs_out) {
   count_launch();
   const int H8 = H / 8;
   auto X = reinterpret_cast<const uint4*>(x);
   auto W = reinterpret_cast<const uint4*>(w);
   auto Y = reinterpret_cast<uint4*>(y);
-  if (H8 <= 256) launchk(rmsnorm_kernel<1>, T, 256, 0, st, X, rows, W, Y, H8, 1.0f / H, eps);
-  else if (H8 <= 512) launchk(rmsnorm_kernel<2>, T, 256, 0, st, X, rows, W, Y, H8, 1.0f / H, eps);
-  else if (H8 <= 1024) launchk(rmsnorm_kernel<4>, T, 256, 0, st, X, rows, W, Y, H8, 1.0f / H, eps);
-  else launchk(rmsnorm_kernel<8>, T, 256, 0, st, X, rows, W, Y, H8, 1.0f / H, eps);
+  if (H8 <= 256) launchk(rmsnorm_kernel<1>, T, 256, 0, st, X, rows, W, Y, rs_out, H8, 1.0f / H, eps);
+  else if (H8 <= 512) launchk(rmsnorm_kernel<2>, T, 256, 0, st, X, rows, W, Y, rs_out, H8, 1.0f / H, eps);
+  else if (H8 <= 1024) launchk(rmsnorm_kernel<4>, T, 256, 0, st, X, rows, W, Y, rs_out, H8, 1.0f / H, eps);
+  else launchk(rmsnorm_kernel<8>, T, 256, 0, st, X, rows, W, Y, rs_out, H8, 1.0f / H, eps);
 }
 
 // ------------------------------------------------------------------ RoPE + KV write (a8) -

@@ -18,8 +18,10 @@ void launch_embed(const int* tok, const bf16* E, bf16* x, int T, int H, int V, c
 unsigned debug_bad_bits(bool reset);
 
 // y[i] = bf16(x[row(i)] * rsqrt(mean(x^2)+eps) * w)   (a6; rows = null => row(i) = i)
+// rs_out != null (the norm feeding a GEMM, reading R10b): y[i] = bf16(x[row(i)] * w) and
+// rs_out[i] = rsqrt(mean(x^2)+eps), applied by the GEMM epilogue (GemmArgs::rs)
 void launch_rmsnorm(const bf16* x, const int* rows, const bf16* w, bf16* y, int T, int H,
-                    float eps, cudaStream_t st);
+                    float eps, cudaStream_t st, float* rs_out = nullptr);
 
 // RoPE (rotate-half, fp32 table) on q,k of qkv [T, 3H]; writes q' [T,H] and k', v into the
 // paged pool of this layer: pool[block][K|V][head][16][d]  (a8)

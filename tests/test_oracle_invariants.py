@@ -78,10 +78,12 @@ def brute_force_logits(cfg, W, seq):
     c, s = rope_cos_sin(np.arange(T), d, cfg["rope_theta"])
     for l in range(cfg["n_layers"]):
         w = W.layer(l)
-        n = rmsnorm(x, w["attn_norm"], cfg["rms_eps"])
-        q = rope(bf16(linear(n, w["wq"])).reshape(T, nh, d), c, s)
-        k = rope(bf16(linear(n, w["wk"])).reshape(T, nh, d), c, s)
-        v = bf16(linear(n, w["wv"])).reshape(T, nh, d)
+        # RMSNorm feeding a linear layer: operand bf16(x * w), row scale r after the product (R10b)
+        r = 1.0 / np.sqrt(np.mean(x * x, axis=1, keepdims=True) + cfg["rms_eps"])
+        n = bf16(x * w["attn_norm"])
+        q = rope(bf16(r * linear(n, w["wq"])).reshape(T, nh, d), c, s)
+        k = rope(bf16(r * linear(n, w["wk"])).reshape(T, nh, d), c, s)
+        v = bf16(r * linear(n, w["wv"])).reshape(T, nh, d)
         o = np.zeros((T, nh, d))
         for hh in range(nh):
             S = q[:, hh] @ k[:, hh].T / np.sqrt(d)
@@ -89,8 +91,9 @@ def brute_force_logits(cfg, W, seq):
             P = np.exp(S - S.max(axis=1, keepdims=True))
             o[:, hh] = bf16((P @ v[:, hh]) / P.sum(axis=1, keepdims=True))
         h = bf16(x + linear(o.reshape(T, H), w["wo"]))
-        n2 = rmsnorm(h, w["ffn_norm"], cfg["rms_eps"])
-        x = bf16(h + linear(bf16(silu(linear(n2, w["wg"])) * linear(n2, w["wu"])), w["wd"]))
+        r2 = 1.0 / np.sqrt(np.mean(h * h, axis=1, keepdims=True) + cfg["rms_eps"])
+        n2 = bf16(h * w["ffn_norm"])
+        x = bf16(h + linear(bf16(silu(r2 * linear(n2, w["wg"])) * (r2 * linear(n2, w["wu"]))), w["wd"]))
     nf = rmsnorm(x[-1:], W.final_norm(), cfg["rms_eps"])
     return linear(nf, W.lm_head())[0]
 

@@ -5,7 +5,7 @@ import pytest
 import torch
 import torch.nn.functional as F
 
-from oracle.numerics import (attention_one, bf16, bf16_bits, bf16_value, exact, rmsnorm, rope,
+from oracle.numerics import (attention_one, bf16, bf16_bits, bf16_value, exact, linear, rmsnorm, rmsnorm_split, rope,
                              rope_cos_sin, silu)
 
 
@@ -34,6 +34,24 @@ def test_rmsnorm_vs_torch_and_closed_form():
         y = rmsnorm(np.full((1, 64), c), w, 1e-5)
         assert np.array_equal(y[0], bf16(np.sign(c) * w * (abs(c) / np.sqrt(c * c + 1e-5))))
         assert np.allclose(y[0], np.sign(c) * bf16(w), rtol=2**-7)
+
+
+def test_rmsnorm_split_vs_torch_norm_then_linear():
+    """R10b: the RMSNorm feeding a linear layer as r * ((x * w) W^T).  Exact mode equals torch's
+    rms_norm followed by the matmul (an independent library path); bf16 mode rounds only the
+    operand x * w; constant rows give r = 1/sqrt(c^2 + eps) in closed form."""
+    rng = np.random.default_rng(11)
+    x, w, W = rng.standard_normal((5, 64)), 1 + 0.1 * rng.standard_normal(64), rng.standard_normal((24, 64))
+    a, r = rmsnorm_split(x, w, 1e-5, exact)
+    ref = F.rms_norm(torch.from_numpy(x), (64,), torch.from_numpy(w), eps=1e-5) @ torch.from_numpy(W).T
+    assert np.allclose(r * linear(a, W), ref.numpy(), rtol=1e-12, atol=1e-12)
+    xb, wb = bf16(x), bf16(w)
+    a, r = rmsnorm_split(xb, wb, 1e-5)
+    assert np.array_equal(a, bf16(xb * wb))
+    assert np.array_equal(r[:, 0], 1.0 / np.sqrt(np.mean(xb * xb, axis=1) + 1e-5))
+    for c in (3.0, -250.0):
+        _, r = rmsnorm_split(np.full((1, 64), c), w, 1e-5)
+        assert r[0, 0] == 1.0 / np.sqrt(c * c + 1e-5)
 
 
 def test_rope_identity_norm_and_complex_form():
