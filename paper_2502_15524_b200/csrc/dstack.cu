@@ -547,7 +547,11 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
   // own MMAs still run, so its epilogue starts without a round trip (re-read if not yet written)
   constexpr int NPRE = 8;
   unsigned long long pre[NPRE];
-  float pre_r = 0.f;
+  float pre_r = 0.f, pre_g = 0.f;
+  // O / down: the norm weight of the operand the residual epilogue writes (gate_up's ffn_norm,
+  // the next layer's attn_norm; none after the stage's last layer)
+  const bf16* wn = k == 1 ? p.ffn_norm + (size_t)l * p.norm_stride
+                          : (k == 3 && l + 1 < p.nl ? p.attn_norm + (size_t)(l + 1) * p.norm_stride : nullptr);
   // pass 1: drain every segment of the phase
   for (int cur = beg; cur < end; ++seg) {
     const int t = cur / nkb, kb_lo = cur % nkb, kb_hi = min(nkb, kb_lo + (end - cur));
@@ -566,6 +570,20 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
           if (q + 1 < np) pre[q] = ld_part(tws + (size_t)(q + 1) * BN * 128 + ml);
         if (k == 1 || k == 3)
           pre_r = __bfloat162float(__ldcg((k == 1 ? (l == 0 ? p.x_in : p.x) : p.hbuf) + (size_t)t * 128 + ml));
+        if (wn) pre_g = __bfloat162float(__ldg(wn + (size_t)t * 128 + ml));
+        // while this CTA's own MMAs finish, re-read the parts that were not written yet (one
+        // round trip per probe), so the epilogue rarely pays one after them
+        bool all = false;
+        while (!mbar_test(&tfull[buf], (seg >> 1) & 1)) {
+          if (all) continue;
+          all = true;
+#pragma unroll
+          for (int q = 0; q < NPRE; ++q)
+            if (q + 1 < np && (unsigned)(pre[q] >> 32) != tag) {
+              pre[q] = ld_part(tws + (size_t)(q + 1) * BN * 128 + ml);
+              all = false;
+            }
+        }
       }
     }
     mbar_wait(&tfull[buf], (seg >> 1) & 1);
@@ -710,9 +728,7 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
       const bf16* resid = k == 1 ? (l == 0 ? p.x_in : p.x) : p.hbuf;
       bf16* out = k == 1 ? p.hbuf : p.x;
       // the next GEMM's operand bf16(y * w) (gate_up's ffn_norm / the next layer's attn_norm)
-      const bf16* wn = k == 1 ? p.ffn_norm + (size_t)l * p.norm_stride
-                              : (l + 1 < p.nl ? p.attn_norm + (size_t)(l + 1) * p.norm_stride : nullptr);
-      const float gw = wn ? __bfloat162float(__ldg(wn + m)) : 0.f;
+      const float gw = !wn ? 0.f : (NC == 1 && held && p_early_parts) ? pre_g : __bfloat162float(__ldg(wn + m));
       for (int n0 = 0; n0 < p.N; n0 += NC) {
         float r[NC], a[NC];
 #pragma unroll
