@@ -57,6 +57,8 @@ struct DsParams {
   const SeqDesc* seqs;
   const float2* rope;
   int ch;
+  int ahalf;  // attention units on half CTAs (warps 4-7 / 8-11), 2 G unit slots
+  int fs;     // word stride of the flag arrays f_qkv, f_attn, f_gu, f_nrm and of c_h (1, or 32: a line each)
   float* ws_attn;
   unsigned *c_ih, *c_h, *f_qkv, *f_attn, *f_gu;
   // row norms (reading R10b): a residual tile (and the stage input pass) writes the next
@@ -294,8 +296,10 @@ __device__ __forceinline__ unsigned long long ld_part(const unsigned long long* 
   return w;
 }
 
-// One attention unit: sequence i, head h, KV blocks [sp * DS_SPLIT, (sp + 1) * DS_SPLIT) of the
-// sequence, by the 8 attention warps of a CTA (t = 0..255).  Warp w takes blocks w, w + 8, ...:
+// One attention unit: sequence i, head h, KV blocks [sp * ch, (sp + 1) * ch) of the sequence,
+// by NW attention warps of a CTA (t = 0 .. 32 NW - 1, named barrier `bar`): all 8 (warps 4-11),
+// or, with half-CTA units, warps 4-7 and 8-11 each run their own unit (two units per CTA, so
+// a short context is split finer and each warp reads one block).  Warp w takes blocks w, w + NW, ...:
 // for a 16-token block lane l loads dims [E l, E l + E) of its 16 K and 16 V rows (32
 // independent loads in flight), computes the scores with warp all-reduces and keeps an online
 // softmax (m, l, acc).  The warps are merged through shared memory in warp order; with several
@@ -303,9 +307,10 @@ __device__ __forceinline__ unsigned long long ld_part(const unsigned long long* 
 // order.  The last sequence of head h publishes the head's flag.  Deterministic.
 constexpr int DS_SPLIT = 64;  // KV blocks (1024 tokens) per unit
 
-template <int D>
+template <int D, int NW, int BAR>
 __device__ __forceinline__ void ds_attn_unit(const DsParams& p, int l, unsigned tag, int i, int h, int sp, int nsp,
                                              int u, int t, float* sm, int uph, const int* s_nc, const int* s_base) {
+  constexpr int NT = NW * 32;
   constexpr int E = D / 32;
   const int warp = t >> 5, lane = t & 31;
   const int H = p.nh * D;
@@ -315,8 +320,8 @@ __device__ __forceinline__ void ds_attn_unit(const DsParams& p, int l, unsigned 
   const int q_start = __shfl_sync(0xffffffffu, s.q_start, 0);
   const int* tab = p.tables + (size_t)i * p.max_blocks;
   // block ids of this warp's blocks (call metadata: independent of the flags, fetched first)
-  const int my_blk = (b0 + warp + lane * DS_AWARPS < b1) ? tab[b0 + warp + lane * DS_AWARPS] : 0;
-  if (p_kv_prefetch && t >= 128) {
+  const int my_blk = (b0 + warp + lane * NW < b1) ? tab[b0 + warp + lane * NW] : 0;
+  if (NW == 8 && p_kv_prefetch && t >= 128) {
     // warps 8-11 reach a layer's first unit while warps 4-7 still drain its QKV (they skip that
     // epilogue): they request the unit's cached K / V slabs (4 KiB contiguous each) into L2, so
     // the attention that follows QKV reads them from L2 instead of HBM (only the new token's
@@ -329,8 +334,8 @@ __device__ __forceinline__ void ds_attn_unit(const DsParams& p, int l, unsigned 
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(slab), "r"(16 * D * 2) : "memory");
     }
   }
-  if (t < 3) wait_tag(p.f_qkv + (h * D) / 128 + t * (H / 128), tag);  // q, k, v tiles of head h
-  named_bar(2, 256);
+  if (t < 3) wait_tag(p.f_qkv + (size_t)((h * D) / 128 + t * (H / 128)) * p.fs, tag);  // q, k, v tiles of head h
+  named_bar(BAR, NT);
   if (p.trace && t == 0) DS_TR(TR_AT_FLAGS);
   const float scale = 1.4426950408889634f / sqrtf((float)D);
   float qv[E];
@@ -353,12 +358,12 @@ __device__ __forceinline__ void ds_attn_unit(const DsParams& p, int l, unsigned 
 #pragma unroll
   for (int e = 0; e < E; ++e) acc[e] = 0.f;
   using VT = typename std::conditional<E == 4, uint2, unsigned>::type;
-  for (int b = b0 + warp, bi = 0; b < b1; b += DS_AWARPS, ++bi) {
+  for (int b = b0 + warp, bi = 0; b < b1; b += NW, ++bi) {
     int blk = __shfl_sync(0xffffffffu, my_blk, bi & 31);
     if (bi >= 32) blk = tab[b];
     if (blk < 0 || blk >= p.nblocks) blk = 0;
     const bf16* kb = pool + (((size_t)blk * 2 * p.nh + h) * 16) * D + lane * E;
-    if (b + DS_AWARPS < b1 && bi + 1 < 32) {  // the warp's next block into L2 (no registers held)
+    if (b + NW < b1 && bi + 1 < 32) {  // the warp's next block into L2 (no registers held)
       int nblk = __shfl_sync(0xffffffffu, my_blk, bi + 1);
       if (nblk < 0 || nblk >= p.nblocks) nblk = 0;
       const char* row = reinterpret_cast<const char*>(pool + (((size_t)nblk * 2 * p.nh + h) * 16 + (lane & 15)) * D +
@@ -414,20 +419,20 @@ __device__ __forceinline__ void ds_attn_unit(const DsParams& p, int l, unsigned 
     m = mb;
   }
   if (p.trace && t == 0) DS_TR(TR_AT_KV);
-  // merge the 8 warps through shared memory (warp order)
-  float* sm_m = sm;                 // [8]
-  float* sm_l = sm + DS_AWARPS;     // [8]
-  float* sm_a = sm + 2 * DS_AWARPS; // [8][D]
+  // merge the NW warps through shared memory (warp order)
+  float* sm_m = sm;           // [NW]
+  float* sm_l = sm + NW;      // [NW]
+  float* sm_a = sm + 2 * NW;  // [NW][D]
   if (lane == 0) { sm_m[warp] = m; sm_l[warp] = lsum; }
 #pragma unroll
   for (int e = 0; e < E; ++e) sm_a[warp * D + lane * E + e] = acc[e];
-  named_bar(2, 256);
+  named_bar(BAR, NT);
   float M = -INFINITY, L = 0.f, A = 0.f;
   if (t < D) {
 #pragma unroll
-    for (int w = 0; w < DS_AWARPS; ++w) M = fmaxf(M, sm_m[w]);
+    for (int w = 0; w < NW; ++w) M = fmaxf(M, sm_m[w]);
 #pragma unroll
-    for (int w = 0; w < DS_AWARPS; ++w) {
+    for (int w = 0; w < NW; ++w) {
       const float f = sm_m[w] == -INFINITY ? 0.f : exp2f(sm_m[w] - M);
       L += sm_l[w] * f;
       A += sm_a[w * D + t] * f;
@@ -441,17 +446,17 @@ __device__ __forceinline__ void ds_attn_unit(const DsParams& p, int l, unsigned 
   } else if (t < D) {
     orow[t] = __float2bfloat16_rn(A / L);
   }
-  named_bar(2, 256);
+  named_bar(BAR, NT);
   // one arrival per unit on the head's counter; the last unit of the head merges the splits
   // of every sequence (split order) and publishes the head
   if (t == 0) {
     if (p.trace) DS_TR(TR_AT_END);
-    const unsigned old = atom_add_acq_rel(p.c_h + h, 1u);
+    const unsigned old = atom_add_acq_rel(p.c_h + (size_t)h * p.fs, 1u);
     const int last = old == (unsigned)(uph - 1);
-    if (last) p.c_h[h] = 0;
+    if (last) p.c_h[(size_t)h * p.fs] = 0;
     sm_m[0] = last ? 1.f : 0.f;
   }
-  named_bar(2, 256);
+  named_bar(BAR, NT);
   const bool last = sm_m[0] != 0.f;
   if (last) {
     for (int i2 = 0; i2 < p.N; ++i2) {
@@ -471,13 +476,13 @@ __device__ __forceinline__ void ds_attn_unit(const DsParams& p, int l, unsigned 
       const int qs = p.seqs[i2].q_start;
       p.o[(size_t)qs * H + h * D + t] = __float2bfloat16_rn(AA / LL);
     }
-    named_bar(2, 256);
+    named_bar(BAR, NT);
     if (t == 0) {
-      publish(p.f_attn + h, tag);
+      publish(p.f_attn + (size_t)h * p.fs, tag);
       if (p.trace && h < 64) p.trace[(size_t)p.G * p.nl * 32 + (size_t)l * 256 + 128 + h] = gtimer();
     }
   }
-  named_bar(2, 256);  // sm reusable
+  named_bar(BAR, NT);  // sm reusable
 }
 
 // Slow path of an early read: the part was not written yet.  Traps after ~2 s (protocol bug).
@@ -705,7 +710,7 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
       }
       if (p_trace_k == 0 && et == 0) DS_TR(TR_Q_STORES);
       named_bar(1, 128);
-      if (et == 0) publish(p.f_qkv + t, tag);
+      if (et == 0) publish(p.f_qkv + (size_t)t * p.fs, tag);
       if (p_trace_k == 0 && et == 0) DS_TR(TR_Q_PUB);
       if (et == 0 && p.trace && t < 128) p.trace[(size_t)p.G * p.nl * 32 + (size_t)l * 256 + t] = gtimer();
     } else if (k == 2) {  // a = bf16(silu(g) * u): lanes 0-15 gate rows, 16-31 their up rows
@@ -722,7 +727,7 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
       }
       named_bar(1, 128);
       if (k == p_trace_k && et == 0) DS_TR(TR_Q_VALS);
-      if (et == 0) publish(p.f_gu + t, tag);
+      if (et == 0) publish(p.f_gu + (size_t)t * p.fs, tag);
       if (k == p_trace_k && et == 0) DS_TR(TR_Q_PUB);
     } else {  // residual: h = bf16(x + o W_o^T) (k = 1) / x' = bf16(h + a W_d^T) (k = 3)
       const bf16* resid = k == 1 ? (l == 0 ? p.x_in : p.x) : p.hbuf;
@@ -751,7 +756,7 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
       }
       if (k == p_trace_k && et == 0) DS_TR(TR_Q_VALS);
       if (et == 0) red_release_add(p.c_rows, 1u);  // rows of this tile + their partial sums
-      if (et == 0 && wn) publish(p.f_nrm[k == 1 ? 1 : 0] + t, k == 1 ? tag : tag + 1);  // consumer's layer
+      if (et == 0 && wn) publish(p.f_nrm[k == 1 ? 1 : 0] + (size_t)t * p.fs, k == 1 ? tag : tag + 1);  // consumer's layer
       if (k == p_trace_k && et == 0) DS_TR(TR_Q_PUB);
     }
     if (held) {  // every read of the held accumulator done: the MMA may reuse the buffer
@@ -900,7 +905,8 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
           const int kbl = (x0 + lane) % nkb;
           // QKV / gate_up: the operand tile (128 columns = 2 k-blocks) of the residual tile that
           // produced it; O: the head; down: the gate_up tile
-          const unsigned* f = k == 1 ? p.f_attn + (kbl * 64) / p.hd : k == 3 ? p.f_gu + kbl : p.f_nrm[k >> 1] + (kbl >> 1);
+          const unsigned* f = (k == 1 ? p.f_attn + (size_t)((kbl * 64) / p.hd) * p.fs
+                               : k == 3 ? p.f_gu + (size_t)kbl * p.fs : p.f_nrm[k >> 1] + (size_t)(kbl >> 1) * p.fs);
           int issued = 0;
           unsigned long long t_spin = 0;
           while (issued < cnt) {
@@ -995,7 +1001,7 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
         }
         if (t256 == 0) {
           red_release_add(p.c_rows, 1u);
-          publish(p.f_nrm[0] + blockIdx.x, p.tag0);
+          publish(p.f_nrm[0] + (size_t)blockIdx.x * p.fs, p.tag0);
         }
       }
       const int l = 0;
@@ -1017,14 +1023,36 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
                                      s_pos, s_slot, s_rope, s_rs, s_rs_tag);
       if (t256 == 0) DS_TR(TR_E_QKV + (k == 0 ? 0 : k == 1 ? 2 : k == 2 ? 4 : 5));
       if (k == 0) {
-        // units (seq, head, split) over the CTAs; every CTA loops uniformly
-        for (int u = blockIdx.x; u < total; u += G) {
-          int i = 0;
-          while (i + 1 < p.N && s_base[i + 1] <= u) ++i;
-          i = __shfl_sync(0xffffffffu, i, 0);
-          const int nsp = __shfl_sync(0xffffffffu, s_nc[i], 0), r = u - __shfl_sync(0xffffffffu, s_base[i], 0);
-          if (p.hd == 128) ds_attn_unit<128>(p, l, tag, i, r / nsp, r % nsp, nsp, u, t256, s_att, total / p.nh, s_nc, s_base);
-          else ds_attn_unit<64>(p, l, tag, i, r / nsp, r % nsp, nsp, u, t256, s_att, total / p.nh, s_nc, s_base);
+        // units (seq, head, split) over the CTAs; every CTA (half CTA) loops uniformly
+        // (compiled into the batched kernels only: in the single-sequence kernel the extra code
+        // alone cost 1 % — instruction-cache footprint of the phase loop)
+        if (NC > 1 && p.ahalf) {  // warps 4-7 (barrier 1) and 8-11 (barrier 3) run units u = c, c + G (mod 2G)
+          const int g = t256 >> 7, tg = t256 & 127;
+          float* smg = s_att + g * (2 * 4 + 4 * 128);
+          for (int u = blockIdx.x + g * G; u < total; u += 2 * G) {
+            int i = 0;
+            while (i + 1 < p.N && s_base[i + 1] <= u) ++i;
+            i = __shfl_sync(0xffffffffu, i, 0);
+            const int nsp = __shfl_sync(0xffffffffu, s_nc[i], 0), r = u - __shfl_sync(0xffffffffu, s_base[i], 0);
+            if (p.hd == 128) {
+              if (g) ds_attn_unit<128, 4, 3>(p, l, tag, i, r / nsp, r % nsp, nsp, u, tg, smg, total / p.nh, s_nc, s_base);
+              else ds_attn_unit<128, 4, 1>(p, l, tag, i, r / nsp, r % nsp, nsp, u, tg, smg, total / p.nh, s_nc, s_base);
+            } else {
+              if (g) ds_attn_unit<64, 4, 3>(p, l, tag, i, r / nsp, r % nsp, nsp, u, tg, smg, total / p.nh, s_nc, s_base);
+              else ds_attn_unit<64, 4, 1>(p, l, tag, i, r / nsp, r % nsp, nsp, u, tg, smg, total / p.nh, s_nc, s_base);
+            }
+          }
+        } else {
+          for (int u = blockIdx.x; u < total; u += G) {
+            int i = 0;
+            while (i + 1 < p.N && s_base[i + 1] <= u) ++i;
+            i = __shfl_sync(0xffffffffu, i, 0);
+            const int nsp = __shfl_sync(0xffffffffu, s_nc[i], 0), r = u - __shfl_sync(0xffffffffu, s_base[i], 0);
+            if (p.hd == 128)
+              ds_attn_unit<128, 8, 2>(p, l, tag, i, r / nsp, r % nsp, nsp, u, t256, s_att, total / p.nh, s_nc, s_base);
+            else
+              ds_attn_unit<64, 8, 2>(p, l, tag, i, r / nsp, r % nsp, nsp, u, t256, s_att, total / p.nh, s_nc, s_base);
+          }
         }
         if (t256 == 0) DS_TR(TR_E_ATTN);
       } else if (k == 3 && l + 1 == p.nl && p.final_norm) {  // the model's final norm (event 2l+2)
@@ -1096,9 +1124,10 @@ hs_status dstack_create(DstackState** out, int H, int F, int nh, int hd, int max
   cudaError_t e = cudaMalloc(&s->ws, off * 8);
   if (e == cudaSuccess) e = cudaMemset(s->ws, 0, off * 8);  // no word carries a tag yet
 
-  s->attn_items_max = std::max((size_t)s->G, (size_t)s->max_seqs * nh * ((std::max(max_ctx, 1) + 16 * DS_SPLIT - 1) / (16 * DS_SPLIT)));
+  s->attn_items_max = std::max((size_t)(s->max_seqs > 1 ? 2 : 1) * s->G, (size_t)s->max_seqs * nh * ((std::max(max_ctx, 1) + 16 * DS_SPLIT - 1) / (16 * DS_SPLIT)));
   if (e == cudaSuccess) e = cudaMalloc(&s->ws_attn, s->attn_items_max * (hd + 4) * 4);
-  s->ctr_words = 4096 + (size_t)DS_MAXSEQ * nh + 4 * (size_t)(s->tiles[0] + s->tiles[1] + s->tiles[2] + s->tiles[3]);
+  s->ctr_words = 4096 + (size_t)DS_MAXSEQ * nh + 4 * (size_t)(s->tiles[0] + s->tiles[1] + s->tiles[2] + s->tiles[3]) +
+                 32 * (size_t)(s->tiles[0] + s->tiles[2] + 2 * nh + 2 * (H / 128) + 8);  // padded flags (HS_DSTACK_FLAGPAD)
   if (e == cudaSuccess) e = cudaMalloc(&s->ctr, s->ctr_words * 4);
   if (e == cudaSuccess) e = cudaMemset(s->ctr, 0, s->ctr_words * 4);
   if (e == cudaSuccess) e = cudaMalloc(&s->ssq, (size_t)(H / 128) * DS_MAXSEQ * 4);
@@ -1189,7 +1218,17 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
       return e && atoi(e) > 0 ? std::min(atoi(e), DS_SPLIT) : 1;
     }();
     int ch = min_ch;
-    while (ch < DS_SPLIT && units_of(ch) > (size_t)s->G) ++ch;
+    // half-CTA units for batches (13B B = 16: 7.87 -> 7.61 ms); a single sequence keeps 8-warp
+    // units (2.78 -> 2.79 ms with half units, profiles/r02/dstack_ab/b31_*).  HS_DSTACK_AHALF=0/1
+    // forces either (A/B)
+    static const int ahalf_env = [] {
+      const char* e = getenv("HS_DSTACK_AHALF");
+      return e ? atoi(e) : -1;
+    }();
+    const int ahalf = ahalf_env >= 0 ? (ahalf_env != 0) : (a.N > 1);
+    p.ahalf = ahalf;
+    const size_t slots = (size_t)s->G * (ahalf ? 2 : 1);
+    while (ch < DS_SPLIT && units_of(ch) > slots) ++ch;
     if (units_of(ch) > s->attn_items_max) HS_FAIL(HS_E_INVAL, "dstack: context longer than the workspace was sized for");
     p.ch = ch;
   }
@@ -1224,14 +1263,26 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
   unsigned* c = s->ctr;
   size_t o = 0;
   p.c_ih = c + o; o += (size_t)DS_MAXSEQ * s->nh;
-  p.c_h = c + o; o += s->nh;
+  // one 128-byte line per flag for a single sequence (7B B = 1: 2.711 -> 2.690 ms), packed for
+  // batches (13B B = 16: 7.60 vs 7.64 ms padded; profiles/r02/dstack_ab/b35_*).  Stale words of
+  // the other layout carry older tags (tags grow every launch), so switching is safe.
+  // HS_DSTACK_FLAGPAD=1/32 forces either (A/B)
+  static const int fs_env = [] {
+    const char* e = getenv("HS_DSTACK_FLAGPAD");
+    return e ? atoi(e) : 0;
+  }();
+  const int fs = fs_env == 1 || fs_env == 32 ? fs_env : (a.N == 1 ? 32 : 1);
+  p.fs = fs;
+  // every region is sized for the padded layout, so no array moves when the stride changes
+  // (c_rows is cumulative across launches and must stay put)
   o = align_up(o, 32);
   p.c_rows = c + o; o += 32;
-  p.f_nrm[0] = c + o; o += align_up((size_t)(s->H / 128), 32);
-  p.f_nrm[1] = c + o; o += align_up((size_t)(s->H / 128), 32);
-  p.f_qkv = c + o; o += s->tiles[0];
-  p.f_attn = c + o; o += s->nh;
-  p.f_gu = c + o; o += s->tiles[2];
+  p.c_h = c + o; o += (size_t)s->nh * 32;
+  p.f_nrm[0] = c + o; o += (size_t)(s->H / 128) * 32;
+  p.f_nrm[1] = c + o; o += (size_t)(s->H / 128) * 32;
+  p.f_qkv = c + o; o += (size_t)s->tiles[0] * 32;
+  p.f_attn = c + o; o += (size_t)s->nh * 32;
+  p.f_gu = c + o; o += (size_t)s->tiles[2] * 32;
   p.ssq = s->ssq;
   p.base_rows = s->base_rows;
   s->base_rows += (unsigned)(s->H / 128) * (unsigned)(2 * a.nl + 1);

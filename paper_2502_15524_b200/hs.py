@@ -13,6 +13,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO = os.path.join(HERE, "libhs.so")
+if os.environ.get("HS_LIB_VARIANT"):  # same-box A/B of two builds (tools/build_variant.py); in-tree only
+    SO = os.path.join(HERE, os.path.basename(os.environ["HS_LIB_VARIANT"]))
 
 HS_MAX_STAGES = 8
 HS_MAX_LAYERS = 128
