@@ -440,17 +440,20 @@ def run_ours(args):
 
 def link_probe(torch, dist, rank, world, nbytes=1 << 30):
     """Pinned host -> HBM copy bandwidth of this rank's GPU (GB/s): isolated (the ranks take
-    turns) and concurrent (all at once); best of 3 each, CUDA events on the copy."""
+    turns) and concurrent (all at once); best of 5 each, CUDA events around the copy of 1 GiB
+    as 32 back-to-back 32 MiB copies (the loader's chunk size)."""
     src = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
     src.fill_(1)
     dst = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    chunk = 32 << 20
 
     def timed():
         best = 1e9
-        for _ in range(3):
+        for _ in range(5):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            dst.copy_(src, non_blocking=True)
+            for o in range(0, nbytes, chunk):
+                dst[o:o + chunk].copy_(src[o:o + chunk], non_blocking=True)
             e1.record()
             e1.synchronize()
             best = min(best, e0.elapsed_time(e1) / 1e3)
