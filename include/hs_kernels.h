@@ -53,6 +53,15 @@ hs_status hs_debug_gemm_trace(int32_t enable, void* host_out, int32_t n_ctas);
  * host_out (optional) receives n_words uint64.  enable == 0 frees the buffer. */
 hs_status hs_debug_dstack_trace(int32_t enable, void* host_out, int64_t n_words);
 
+/* Test-only: protocol-failure records of the decode-stack kernel.  A flag or stream-K part
+ * wait that has not been satisfied after ~4 s of SM cycles (a protocol bug, not a slow step) writes one
+ * row per (CTA, warp) into mapped pinned host memory and then traps (the call that launched
+ * it returns HS_E_CUDA, the context is lost).  This call reads those rows on the host (no CUDA
+ * call, so it works after the failure); print != 0 writes each row to stderr, naming the wait
+ * site, the CTA, the flag / workspace region and index, the value seen and the value wanted.
+ * Returns the number of rows (0: no failure recorded). */
+int32_t hs_debug_dstack_diag(int32_t print);
+
 #ifdef __cplusplus
 }
 #endif

@@ -25,7 +25,9 @@
 // h = x + o W_o^T, a = silu(g) u, x' = h + a W_d^T, RMSNorm outputs).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "dstack.h"
@@ -159,6 +161,30 @@ __device__ __constant__ int p_early_parts = 1;
 // Trace only (HS_DSTACK_TRACE_K): the GEMM kind whose stream-K fix-up the TR_Q_* stamps follow
 __device__ __constant__ int p_trace_k = 0;
 
+// Protocol-failure record (hs_debug_dstack_diag): a wait that times out writes one row per
+// (CTA, warp) into mapped pinned host memory before it traps, so the host can read which wait
+// of which CTA failed after the context is lost.  Row: magic, site, CTA, thread, address,
+// value seen, value wanted, %globaltimer.  nullptr: no record.
+__device__ __constant__ unsigned long long* p_diag = nullptr;
+enum { DG_TAG = 1, DG_PART = 2, DG_PARTS = 3, DG_NLAST = 4, DG_ACT = 5 };
+
+__device__ __noinline__ void ds_fail(int site, const void* addr, unsigned long long seen, unsigned long long want) {
+  if (p_diag) {
+    volatile unsigned long long* r = p_diag + ((size_t)blockIdx.x * (DS_THREADS / 32) + (threadIdx.x >> 5)) * 8;
+    r[1] = (unsigned long long)site;
+    r[2] = blockIdx.x;
+    r[3] = threadIdx.x;
+    r[4] = (unsigned long long)addr;
+    r[5] = seen;
+    r[6] = want;
+    r[7] = gtimer();
+    __threadfence_system();
+    r[0] = 0xD1A6ull;
+    __threadfence_system();
+  }
+  __trap();
+}
+
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -171,16 +197,16 @@ __device__ __forceinline__ void publish(unsigned* f, unsigned tag) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(tag) : "memory");
 }
 
-// Waits until the flag reached `tag` (wrap-safe); traps after ~2 s (protocol bug: end the
+// Waits until the flag reached `tag` (wrap-safe); traps after ~4 s (kSpinTimeout) (protocol bug: end the
 // kernel rather than hang the GPU).
 // Polls back off (nanosleep) so that many waiters on one flag do not saturate its L2 slice.
 __device__ __noinline__ void wait_tag(const unsigned* f, unsigned tag) {
   if ((int)(ld_acquire(f) - tag) >= 0) return;
-  const unsigned long long t0 = gtimer();
+  const unsigned long long t0 = spin_clock();
   for (unsigned it = 1;; ++it) {
     __nanosleep(p_backoff_ns);
     if ((int)(ld_acquire(f) - tag) >= 0) return;
-    if ((it & 255) == 0 && gtimer() - t0 > 2000000000ull) __trap();
+    if ((it & 255) == 0 && spin_clock() - t0 > kSpinTimeout) ds_fail(DG_TAG, f, ld_acquire(f), tag);
   }
 }
 
@@ -485,21 +511,21 @@ __device__ __forceinline__ void ds_attn_unit(const DsParams& p, int l, unsigned 
   named_bar(BAR, NT);  // sm reusable
 }
 
-// Slow path of an early read: the part was not written yet.  Traps after ~2 s (protocol bug).
+// Slow path of an early read: the part was not written yet.  Traps after ~4 s (kSpinTimeout; protocol bug).
 __device__ __noinline__ float wait_part(const unsigned long long* a, unsigned tag) {
-  const unsigned long long t0 = gtimer();
+  const unsigned long long t0 = spin_clock();
   for (;;) {
     const unsigned long long w = ld_part(a);
     if ((unsigned)(w >> 32) == tag) return __uint_as_float((unsigned)w);
     __nanosleep(64);
-    if (gtimer() - t0 > 2000000000ull) __trap();
+    if (spin_clock() - t0 > kSpinTimeout) ds_fail(DG_PART, a, w, tag);
   }
 }
 
 // a[j] += the stream-K parts p0 .. np - 1 (in part order) of tile row ml, tokens n0 + j, with
 // every load of a part group in flight together (the tail of each tile is latency bound).  A
 // group not written yet is re-read as a whole (one round trip per poll, not one per word);
-// traps after ~2 s (protocol bug).
+// traps after ~4 s (kSpinTimeout) (protocol bug).
 template <int NC>
 __device__ __forceinline__ void ds_add_parts(const unsigned long long* tws, int p0, int np, int n0, int N, int ml,
                                              float* a, int BN, unsigned tag) {
@@ -513,10 +539,10 @@ __device__ __forceinline__ void ds_add_parts(const unsigned long long* tws, int 
 #pragma unroll
     for (int j = 0; j < NC; ++j) ok = ok && (unsigned)(w[j] >> 32) == tag;
     if (!ok) {
-      const unsigned long long t0 = gtimer();
+      const unsigned long long t0 = spin_clock();
       do {
         __nanosleep(64);
-        if (gtimer() - t0 > 2000000000ull) __trap();
+        if (spin_clock() - t0 > kSpinTimeout) ds_fail(DG_PARTS, src, w[0], ((unsigned long long)pt << 32) | tag);
 #pragma unroll
         for (int j = 0; j < NC; ++j)
           if (n0 + j < N && (unsigned)(w[j] >> 32) != tag) w[j] = ld_part(src + (size_t)j * 128);
@@ -598,7 +624,7 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
     if (hold) {
       held_t = t;
       held_buf = buf;
-      if (nlast == 4) __trap();
+      if (nlast == 4) ds_fail(DG_NLAST, tws, (unsigned long long)t, (unsigned long long)k);
       lastt[nlast++] = t;
       if (k == p_trace_k && et == 0 && cur == beg) DS_TR(TR_Q_DRAIN);
       cur += kb_hi - kb_lo;
@@ -625,7 +651,7 @@ __device__ __forceinline__ int ds_segments(const DsParams& p, int k, int l, unsi
     if (k == p_trace_k && et == 0 && first_seg) DS_TR(TR_Q_DRAIN);
     cur += kb_hi - kb_lo;
     if (np == 1) {  // a whole tile inside the range, not its last segment
-      if (nlast == 4) __trap();
+      if (nlast == 4) ds_fail(DG_NLAST, tws, (unsigned long long)t, (unsigned long long)k);
       lastt[nlast++] = t;
     }
   }
@@ -930,8 +956,9 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
               issued = upto;
             } else {
               __nanosleep(p_backoff_ns);
-              if (t_spin == 0) t_spin = gtimer();
-              else if (gtimer() - t_spin > 2000000000ull) __trap();
+              if (t_spin == 0) t_spin = spin_clock();
+              else if (spin_clock() - t_spin > kSpinTimeout)
+                ds_fail(DG_ACT, f, ld_acquire(f), ((unsigned long long)(l * 4 + k) << 32) | tag);
             }
           }
         }
@@ -1084,6 +1111,22 @@ struct DstackState {
   float* ssq = nullptr;                 // [H / 128][64] row sum-of-squares partials
   unsigned base_rows = 0;  // cumulative c_rows value at the next launch
 };
+
+// Protocol-failure rows (p_diag), mapped pinned host memory, and the address map of the
+// latest launch to name the region a failed wait polled (hs_debug_dstack_diag)
+static constexpr size_t kDiagRows = (size_t)160 * (DS_THREADS / 32);
+static unsigned long long* g_diag_host = nullptr;
+struct DiagRegion {
+  const char* name;
+  unsigned long long lo, hi, stride;
+};
+struct DiagState {
+  const void* state;
+  DiagRegion map[16];
+  int nmap;
+  unsigned tag0, base_rows;
+};
+static DiagState g_diag[16];  // per DstackState (stages sharing a device), latest launch each
 
 // HS debug: per-CTA phase timestamps of the last launch (hs_debug_dstack_trace)
 static unsigned long long* g_ds_trace = nullptr;
@@ -1256,6 +1299,13 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
       const char* e3 = getenv("HS_DSTACK_NOMMA");
       const int nomma = e3 ? atoi(e3) : 0;
       HS_CUDA(cudaMemcpyToSymbol(p_nomma, &nomma, sizeof(nomma)));
+      if (!g_diag_host) {
+        HS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&g_diag_host), kDiagRows * 64, cudaHostAllocMapped | cudaHostAllocPortable));
+        memset(g_diag_host, 0, kDiagRows * 64);
+      }
+      unsigned long long* dptr = nullptr;
+      HS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dptr), g_diag_host, 0));
+      HS_CUDA(cudaMemcpyToSymbol(p_diag, &dptr, sizeof(dptr)));
       bo_set[s->device] = true;
     }
   }
@@ -1287,6 +1337,33 @@ hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st) {
   p.base_rows = s->base_rows;
   s->base_rows += (unsigned)(s->H / 128) * (unsigned)(2 * a.nl + 1);
   if (o > s->ctr_words) HS_FAIL(HS_E_INVAL, "dstack: counter layout overflow");
+  {  // address map for hs_debug_dstack_diag (host bookkeeping only)
+    auto reg = [](const char* n, const void* lo, size_t words, size_t wb, size_t stride) {
+      const unsigned long long b = (unsigned long long)(uintptr_t)lo;
+      return DiagRegion{n, b, b + words * wb, stride};
+    };
+    int si = 0;
+    while (si < 15 && g_diag[si].state && g_diag[si].state != s) ++si;
+    DiagState& d = g_diag[si];
+    d.state = s;
+    DiagRegion* g_diag_map = d.map;
+    int m = 0;
+    g_diag_map[m++] = reg("c_rows", p.c_rows, 1, 4, 4);
+    g_diag_map[m++] = reg("c_h", p.c_h, (size_t)s->nh * 32, 4, 4 * fs);
+    g_diag_map[m++] = reg("f_nrm0", p.f_nrm[0], (size_t)(s->H / 128) * 32, 4, 4 * fs);
+    g_diag_map[m++] = reg("f_nrm1", p.f_nrm[1], (size_t)(s->H / 128) * 32, 4, 4 * fs);
+    g_diag_map[m++] = reg("f_qkv", p.f_qkv, (size_t)s->tiles[0] * 32, 4, 4 * fs);
+    g_diag_map[m++] = reg("f_attn", p.f_attn, (size_t)s->nh * 32, 4, 4 * fs);
+    g_diag_map[m++] = reg("f_gu", p.f_gu, (size_t)s->tiles[2] * 32, 4, 4 * fs);
+    g_diag_map[m++] = reg("c_ih", p.c_ih, (size_t)DS_MAXSEQ * s->nh, 4, 4);
+    static const char* wsn[4] = {"ws_qkv", "ws_o", "ws_gu", "ws_d"};
+    for (int k = 0; k < 4; ++k)
+      g_diag_map[m++] = reg(wsn[k], p.ws[k], (size_t)s->tiles[k] * s->maxp[k] * s->bn_max * 128, 8,
+                            (size_t)s->maxp[k] * s->bn_max * 128 * 8);
+    d.nmap = m;
+    d.tag0 = p.tag0;
+    d.base_rows = p.base_rows;
+  }
   switch (BN) {
     case 16: return a.N == 1 ? launch_bn<16, 1>(s, a, p, bi, st) : launch_bn<16, 8>(s, a, p, bi, st);
     case 32: return launch_bn<32, 8>(s, a, p, bi, st);
@@ -1307,6 +1384,36 @@ void warm_dstack() {
 }
 
 }  // namespace hs
+
+extern "C" int32_t hs_debug_dstack_diag(int32_t print) {
+  using namespace hs;
+  if (!g_diag_host) return 0;
+  int n = 0;
+  for (size_t r = 0; r < kDiagRows; ++r) {
+    const volatile unsigned long long* w = g_diag_host + r * 8;
+    if (w[0] != 0xD1A6ull) continue;
+    ++n;
+    if (!print) continue;
+    static const char* sites[] = {"?", "wait_tag", "wait_part", "add_parts", "nlast", "act_flag"};
+    const unsigned long long a = w[4];
+    const char* reg = "?";
+    long long idx = -1;
+    int st = -1;
+    for (int si = 0; si < 16; ++si)
+      for (int m = 0; m < g_diag[si].nmap; ++m)
+        if (a >= g_diag[si].map[m].lo && a < g_diag[si].map[m].hi) {
+          reg = g_diag[si].map[m].name;
+          idx = (long long)((a - g_diag[si].map[m].lo) / g_diag[si].map[m].stride);
+          st = si;
+        }
+    fprintf(stderr,
+            "dstack diag: site=%s cta=%llu thread=%llu region=%s[%lld] seen=0x%llx want=0x%llx t=%llu "
+            "(state %d, its last launch tag0=0x%x base_rows=%u)\n",
+            sites[w[1] < 6 ? w[1] : 0], w[2], w[3], reg, idx, w[5], w[6], w[7], st, st >= 0 ? g_diag[st].tag0 : 0u,
+            st >= 0 ? g_diag[st].base_rows : 0u);
+  }
+  return n;
+}
 
 extern "C" hs_status hs_debug_dstack_trace(int32_t enable, void* host_out, int64_t n_words) {
   using namespace hs;

@@ -678,16 +678,14 @@ void launch_send(const void* src, void* dst, uint64_t bytes, unsigned* done_ctr,
 __global__ void wait_kernel(const unsigned* flag, unsigned epoch, int* err) {
   PDL_LAUNCH();
   PDL_WAIT();
-  uint64_t t0;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  // SM cycles, not %globaltimer (re-synchronised by the driver, it can step backwards; tc.h)
+  const long long t0 = clock64();
   for (;;) {
     unsigned v;
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
     if ((int)(v - epoch) >= 0) return;
     __nanosleep(200);
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 20000000000ull) {  // 20 s: the peer never signalled
+    if (clock64() - t0 > 40000000000ll) {  // ~20 s at the boost clock: the peer never signalled
       *err = 1;
       return;
     }

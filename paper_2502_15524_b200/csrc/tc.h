@@ -18,6 +18,14 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+// Spin-wait timeouts count SM cycles (clock64: per-SM, monotonic), never %globaltimer: the
+// driver re-synchronises %globaltimer to the host clock, so it can step backwards, and an
+// unsigned difference of two readings across such a step is a huge "elapsed" time that
+// trapped healthy waits (run 40: 7B decode tests on one box, 2 of 2 runs).
+// kSpinTimeout: ~4 s at the 1.965 GHz boost clock, longer at lower clocks.
+constexpr unsigned long long kSpinTimeout = 8000000000ull;
+__device__ __forceinline__ unsigned long long spin_clock() { return (unsigned long long)clock64(); }
+
 // Bounded wait: traps after ~4 s so a protocol bug ends the kernel instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
@@ -33,10 +41,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
     if (done) return;
     if ((it & 1023) == 0) {
-      uint64_t t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (t0 == 0) t0 = t;
-      else if (t - t0 > 4000000000ull) __trap();
+      const uint64_t t = spin_clock();
+      if (it == 0) t0 = t;
+      else if (t - t0 > kSpinTimeout) __trap();
     }
   }
 }

@@ -118,7 +118,7 @@ SYMBOLS = ["hs_image_layout", "hs_plan_stages", "hs_predict_ttft_eq1", "hs_predi
            "hs_debug_poison_weights", "hs_debug_launch_count", "hs_stage_timing_get", "hs_profile_enable",
            "hs_profile_read", "hs_debug_comm_selftest",
            "hs_k_gemm", "hs_k_rmsnorm", "hs_k_rope_kv", "hs_k_attention", "hs_k_argmax", "hs_k_embed",
-           "hs_k_span_copy", "hs_debug_gemm_trace", "hs_debug_dstack_trace", "hs_plan_auto", "hs_links_create", "hs_links_admit",
+           "hs_k_span_copy", "hs_debug_gemm_trace", "hs_debug_dstack_trace", "hs_debug_dstack_diag", "hs_plan_auto", "hs_links_create", "hs_links_admit",
            "hs_links_settle", "hs_links_complete", "hs_links_pending", "hs_links_destroy",
            "hs_load_background_async", "hs_scale_up", "hs_release_peer_memory", "hs_debug_capture",
            "hs_debug_read_hidden", "hs_debug_set_prefill_chunking", "hs_prefetch_start", "hs_prefetch_wait",
@@ -175,6 +175,8 @@ def lib():
     L.hs_k_span_copy.argtypes = [VP, VP, I32, U64, VP]
     L.hs_debug_gemm_trace.argtypes = [I32, VP, I32]
     L.hs_debug_dstack_trace.argtypes = [I32, VP, C.c_int64]
+    L.hs_debug_dstack_diag.argtypes = [I32]
+    L.hs_debug_dstack_diag.restype = I32
     L.hs_plan_auto.argtypes = [P(ModelCfg), P(Gpu), I32, P(Slo), P(Plan), P(I32)]
     L.hs_links_create.argtypes = [I32, P(C.c_double), P(VP)]
     L.hs_links_admit.argtypes = [VP, I32, C.c_double, C.c_double, C.c_double, P(I32), P(C.c_int64)]
@@ -200,7 +202,10 @@ def lib():
 
 def check(code):
     if code != 0:
-        raise HsError(code, lib().hs_last_error().decode())
+        msg = lib().hs_last_error().decode()
+        if code == 2:  # HS_E_CUDA: name the decode-stack wait that trapped, if one did
+            lib().hs_debug_dstack_diag(1)
+        raise HsError(code, msg)
 
 
 def model_cfg(cfg: dict) -> ModelCfg:

@@ -17,7 +17,7 @@ def declared_symbols():
     names = []
     for h in ("hs.h", "hs_kernels.h"):
         src = open(os.path.join(ROOT, "include", h)).read()
-        names += re.findall(r"^\s*(?:hs_status|double|const char\*)\s+(hs_\w+)\s*\(", src, re.M)
+        names += re.findall(r"^\s*(?:hs_status|double|int32_t|const char\*)\s+(hs_\w+)\s*\(", src, re.M)
     return names
 
 
