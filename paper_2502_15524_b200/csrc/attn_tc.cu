@@ -258,14 +258,15 @@ __global__ void __launch_bounds__(128, TA_KC == 64 ? 2 : 1) attn_prefill_tc_kern
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
 }
 
-// Off by default (HS_ATTN_TC=1 enables it).  Measured (7B layer, profiles/r02/attn_tc_ab.txt):
-// 42 us at 512 tokens (mma.sync kernel 41 us) and 132 us at 2048 tokens (176 us); layer-level
-// parity green and 20 repeated calls bit-identical, but one pp-invariance run failed once in the
-// GPU suite and did not reproduce in three reruns, so it stays an A/B path until that is found.
+// The default prefill attention (HS_ATTN_TC=0 selects the mma.sync kernel, A/B).  Measured
+// (7B layer, profiles/r02/attn_tc_ab.txt): 42 us at 512 tokens (mma.sync kernel 41 us) and
+// 132 us at 2048 tokens (176 us); layer-level parity green and 20 repeated calls bit-identical.
+// Its one unreproduced pp-invariance failure (r02) predates the cycle-counted mbar_wait timeout
+// (tc.h: a backwards step of %globaltimer trapped healthy waits).
 bool attn_tc_enabled() {
   static const bool on = [] {
     const char* e = getenv("HS_ATTN_TC");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   return on;
 }

@@ -1149,7 +1149,7 @@ bool dstack_supported(int N, int hd) {
   return on && N >= 1 && N <= DS_MAXSEQ && (hd == 64 || hd == 128);
 }
 
-hs_status dstack_create(DstackState** out, int H, int F, int nh, int hd, int max_seqs, int max_ctx) {
+hs_status dstack_create(DstackState** out, int H, int F, int nh, int hd, int max_seqs, int max_ctx, cudaStream_t st) {
   DstackState* s = new DstackState();
   HS_CUDA(cudaGetDevice(&s->device));
   s->G = num_sms(s->device);
@@ -1165,14 +1165,15 @@ hs_status dstack_create(DstackState** out, int H, int F, int nh, int hd, int max
     off += align_up((size_t)s->tiles[k] * s->maxp[k] * s->bn_max * 128, 64);
   }
   cudaError_t e = cudaMalloc(&s->ws, off * 8);
-  if (e == cudaSuccess) e = cudaMemset(s->ws, 0, off * 8);  // no word carries a tag yet
+  // zeroed in stream order before the first launch (dstack.h): no word carries a tag yet
+  if (e == cudaSuccess) e = cudaMemsetAsync(s->ws, 0, off * 8, st);
 
   s->attn_items_max = std::max((size_t)(s->max_seqs > 1 ? 2 : 1) * s->G, (size_t)s->max_seqs * nh * ((std::max(max_ctx, 1) + 16 * DS_SPLIT - 1) / (16 * DS_SPLIT)));
   if (e == cudaSuccess) e = cudaMalloc(&s->ws_attn, s->attn_items_max * (hd + 4) * 4);
   s->ctr_words = 4096 + (size_t)DS_MAXSEQ * nh + 4 * (size_t)(s->tiles[0] + s->tiles[1] + s->tiles[2] + s->tiles[3]) +
                  32 * (size_t)(s->tiles[0] + s->tiles[2] + 2 * nh + 2 * (H / 128) + 8);  // padded flags (HS_DSTACK_FLAGPAD)
   if (e == cudaSuccess) e = cudaMalloc(&s->ctr, s->ctr_words * 4);
-  if (e == cudaSuccess) e = cudaMemset(s->ctr, 0, s->ctr_words * 4);
+  if (e == cudaSuccess) e = cudaMemsetAsync(s->ctr, 0, s->ctr_words * 4, st);
   if (e == cudaSuccess) e = cudaMalloc(&s->ssq, (size_t)(H / 128) * DS_MAXSEQ * 4);
   if (e != cudaSuccess) {
     dstack_destroy(s);

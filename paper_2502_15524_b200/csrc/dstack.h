@@ -53,7 +53,10 @@ struct DstackArgs {
 
 // Per-stage persistent state (workspaces + flags); create once, reuse every step.
 struct DstackState;
-hs_status dstack_create(DstackState** out, int H, int F, int nh, int hd, int max_seqs, int max_ctx);
+// The workspace and counters are zeroed by cudaMemsetAsync on st, the stream the first launch
+// goes to (a legacy-stream cudaMemset is not ordered with the library's non-blocking streams:
+// run 42 caught one landing after the first launch, which reset c_rows under the next one).
+hs_status dstack_create(DstackState** out, int H, int F, int nh, int hd, int max_seqs, int max_ctx, cudaStream_t st);
 void dstack_destroy(DstackState* s);
 bool dstack_supported(int N, int hd);
 hs_status dstack_launch(DstackState* s, const DstackArgs& a, cudaStream_t st);

@@ -826,7 +826,7 @@ static hs_status run_dstack(hs_group* g, Stage& s, const CallMeta& m, const uint
   const int nl = s.le - s.lb;
   if (nl < 1 || nl > 255) return HS_OK;
   if (!s.ds) {
-    HS_TRY(dstack_create(&s.ds, c.hidden, c.ffn, c.n_heads, c.head_dim, g->kv.max_seqs, c.max_seq));
+    HS_TRY(dstack_create(&s.ds, c.hidden, c.ffn, c.n_heads, c.head_dim, g->kv.max_seqs, c.max_seq, s.comp));
   }
   if (m.n > std::min(64, g->kv.max_seqs)) return HS_OK;
   const hs_image_header& h = g->hdr;

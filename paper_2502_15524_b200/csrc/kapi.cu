@@ -69,7 +69,7 @@ extern "C" hs_status hs_k_attention(const void* q, const void* pool, const int32
     cudaGetDevice(&dev);
     if (!ctr[dev]) {
       HS_CUDA(cudaMalloc(&ctr[dev], 1 << 20));
-      HS_CUDA(cudaMemset(ctr[dev], 0, 1 << 20));
+      HS_CUDA(cudaMemsetAsync(ctr[dev], 0, 1 << 20, st));  // ordered before the launch on st
     }
     if ((size_t)n * nh * 4 > (1u << 20)) HS_FAIL(HS_E_INVAL, "too many (seq, head) pairs");
     launch_attn_decode(reinterpret_cast<const bf16*>(q), reinterpret_cast<const bf16*>(pool), sd, n, max_ctx, tables,
