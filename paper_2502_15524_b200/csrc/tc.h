@@ -20,8 +20,7 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 
 // Spin-wait timeouts count SM cycles (clock64: per-SM, monotonic), never %globaltimer: the
 // driver re-synchronises %globaltimer to the host clock, so it can step backwards, and an
-// unsigned difference of two readings across such a step is a huge "elapsed" time that
-// trapped healthy waits (run 40: 7B decode tests on one box, 2 of 2 runs).
+// unsigned difference of two readings across such a step would be a huge "elapsed" time.
 // kSpinTimeout: ~4 s at the 1.965 GHz boost clock, longer at lower clocks.
 constexpr unsigned long long kSpinTimeout = 8000000000ull;
 __device__ __forceinline__ unsigned long long spin_clock() { return (unsigned long long)clock64(); }
