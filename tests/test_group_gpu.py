@@ -569,3 +569,36 @@ def test_background_nvlink_pull_then_kv_only_consolidation(image, oracle_run, pp
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     g.destroy()
     g1.destroy()
+
+
+@pytest.mark.parametrize("pp", [1, 2])
+def test_decode_stack_state_zeroed_in_stream_order(image, pp):
+    """Regression (run 42, DESIGN.md §7.1 "Intermittent decode traps"): the decode stack's state
+    is created at a group's first decode step and its counters must be zeroed in the order of
+    the stage's stream.  Here the legacy default stream is kept busy (torch.cuda._sleep) across
+    the first decode steps, so a legacy-stream memset would land behind the sleep, after the
+    first launches had counted, and trap a later step.  Every step must equal a reference
+    group's, and the steps must outlast the sleep (else the window was not covered)."""
+    prompts = hsgen.prompts(2, 32, CFG["vocab"])
+    n_max = 600
+    ref = make_group(image, pp, num_blocks=128)
+    ref.load_stage_async(-1)
+    ref.prefill([0, 1], prompts)
+    want = [ref.decode_step([0, 1])[0] for _ in range(n_max)]
+    ref.destroy()
+    g = make_group(image, pp, num_blocks=128)
+    g.load_stage_async(-1)
+    g.prefill([0, 1], prompts)
+    torch.cuda.synchronize()
+    sleep_s = 0.03
+    t0 = time.time()
+    torch.cuda._sleep(int(sleep_s * 2.0e9))  # ~30 ms of SM cycles on the legacy default stream
+    got = []
+    while len(got) < n_max and (len(got) < 50 or time.time() - t0 < 4 * sleep_s):
+        got.append(g.decode_step([0, 1])[0])
+    covered = time.time() - t0
+    torch.cuda.synchronize()
+    g.destroy()
+    assert covered > 2 * sleep_s, f"decode steps ended after {covered:.3f} s, inside the sleep window"
+    for i, a in enumerate(got):
+        assert np.array_equal(a, want[i]), f"step {i}"
