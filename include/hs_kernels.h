@@ -58,8 +58,8 @@ hs_status hs_debug_dstack_trace(int32_t enable, void* host_out, int64_t n_words)
  * row per (CTA, warp) into mapped pinned host memory and then traps (the call that launched
  * it returns HS_E_CUDA, the context is lost).  This call reads those rows on the host (no CUDA
  * call, so it works after the failure); print != 0 writes each row to stderr, naming the wait
- * site, the CTA, the flag / workspace region and index, the value seen and the value wanted.
- * Returns the number of rows (0: no failure recorded). */
+ * site, the CTA, the flag / workspace region and index, the value seen and the value wanted,
+ * and clears the rows it printed.  Returns the number of rows (0: no failure recorded). */
 int32_t hs_debug_dstack_diag(int32_t print);
 
 #ifdef __cplusplus

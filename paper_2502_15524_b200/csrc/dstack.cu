@@ -1412,6 +1412,7 @@ extern "C" int32_t hs_debug_dstack_diag(int32_t print) {
             "(state %d, its last launch tag0=0x%x base_rows=%u)\n",
             sites[w[1] < 6 ? w[1] : 0], w[2], w[3], reg, idx, w[5], w[6], w[7], st, st >= 0 ? g_diag[st].tag0 : 0u,
             st >= 0 ? g_diag[st].base_rows : 0u);
+    g_diag_host[r * 8] = 0;  // each record is reported once
   }
   return n;
 }
