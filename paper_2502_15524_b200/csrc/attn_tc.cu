@@ -110,14 +110,17 @@ __global__ void __launch_bounds__(128, TA_KC == 64 ? 2 : 1) attn_prefill_tc_kern
   };
   PDL_WAIT();
   issue(0, true, true);
-  // Q rows: thread t loads query q0 + t (rows past n_q repeat the last row: never stored)
+  // Q rows: thread t loads query q0 + t (rows past n_q repeat the last row: never stored).
+  // L2 loads (__ldcg), not the non-coherent path: q is written by the previous kernel, which
+  // under PDL still runs during this kernel's lifetime (ld.global.nc requires data read-only
+  // for the whole lifetime)
   const int qi = min(q0 + t, s.n_q - 1);
   const int pos = s.pos0 + q0 + t;  // this row's position (causal bound)
   {
     const uint4* src = reinterpret_cast<const uint4*>(q + (size_t)(s.q_start + qi) * H + head * D);
 #pragma unroll
     for (int c = 0; c < D / 8; ++c)
-      *reinterpret_cast<uint4*>(sQ + (c >> 3) * (TA_Q * 128) + sw128(t, c & 7)) = __ldg(src + c);
+      *reinterpret_cast<uint4*>(sQ + (c >> 3) * (TA_Q * 128) + sw128(t, c & 7)) = __ldcg(src + c);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
