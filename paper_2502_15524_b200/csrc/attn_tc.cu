@@ -50,6 +50,12 @@ __global__ void __launch_bounds__(128, TA_KC == 64 ? 2 : 1) attn_prefill_tc_kern
     const int* __restrict__ tables, int max_blocks, bf16* __restrict__ o, int nh, int nblocks) {
   using C = TaCfg<D>;
   PDL_LAUNCH();
+  // before the first read of the call's metadata (seqs, tables): they are staged into device
+  // memory by a kernel earlier in the same stream, and with every kernel triggering its
+  // dependents at entry a whole chain of them can be resident before that copy ends.  Reading
+  // seqs before this wait (run 45 / 47: a stale n_q returned CTAs early) made the kernel
+  // nondeterministic.
+  PDL_WAIT();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if (threadIdx.x == 0 && (smem_u32(smem) & 1023)) __trap();  // the SW128 tiles need 1024-byte alignment
@@ -108,7 +114,6 @@ __global__ void __launch_bounds__(128, TA_KC == 64 ? 2 : 1) attn_prefill_tc_kern
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  PDL_WAIT();
   issue(0, true, true);
   // Q rows: thread t loads query q0 + t (rows past n_q repeat the last row: never stored).
   // L2 loads (__ldcg), not the non-coherent path: q is written by the previous kernel, which
