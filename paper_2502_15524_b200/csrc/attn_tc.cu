@@ -266,18 +266,15 @@ __global__ void __launch_bounds__(128, TA_KC == 64 ? 2 : 1) attn_prefill_tc_kern
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
 }
 
-// Off by default (HS_ATTN_TC=1 enables it).  Measured (7B layer, profiles/r02/attn_tc_ab.txt):
-// 42 us at 512 tokens (mma.sync kernel 41 us) and 132 us at 2048 tokens (176 us); layer-level
-// parity green and 20 repeated calls bit-identical.  Made the default in run 43, where the full
-// GPU suite passed once and then failed once: test_background_host_load_then_kv_only_
-// consolidation[4] saw PP=4 logits differ from PP=1 (tokens equal) during its first decode steps,
-// a test that passed in all 20 earlier runs with the mma.sync kernel.  With its earlier
-// unreproduced PP-invariance failure that makes it the suspect of a rare nondeterminism, so it
-// stays an A/B path until that is found.
+// The default prefill attention (HS_ATTN_TC=0 selects the mma.sync kernel, A/B).  Measured
+// (7B layer, profiles/r02/attn_tc_ab.txt): 42 us at 512 tokens (mma.sync kernel 41 us) and
+// 132 us at 2048 tokens (176 us).  Its PP-split nondeterminism (runs 43 / 45 / 47: up to 9 of
+// 30 processes) was the metadata read before griddepcontrol.wait (fixed above): 30 of 30 clean
+// and the full GPU suite 81 / 81 after the fix (run 49, profiles/r02/attn_tc_flaky/).
 bool attn_tc_enabled() {
   static const bool on = [] {
     const char* e = getenv("HS_ATTN_TC");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   return on;
 }

@@ -31,7 +31,7 @@ void launch_rope_kv(const bf16* qkv, const int* pos, const int* slot, const floa
 
 // Causal attention of the packed queries against the paged cache (a9).  Prefill layout:
 // one CTA per (16-query tile, head, sequence).
-// tcgen05 prefill attention (attn_tc.cu), off by default; HS_ATTN_TC=1 selects it (A/B)
+// tcgen05 prefill attention (attn_tc.cu), the default; HS_ATTN_TC=0 selects the mma.sync kernel (A/B)
 bool attn_tc_enabled();
 void launch_attn_prefill_tc(const bf16* q, const bf16* pool, const SeqDesc* seqs, int n_seqs, int max_nq,
                             const int* tables, int max_blocks, bf16* o, int nh, int d, int nblocks, cudaStream_t st);
